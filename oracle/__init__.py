@@ -1,0 +1,115 @@
+"""Oracle — TEST INFRASTRUCTURE ONLY.
+
+Plain, slow, obviously correct CPU implementations of what the CUDA path computes, written from
+the paper (arxiv 1604.04689, /root/reference/PAPER.md) and SURVEY.md §8(c):
+
+* ``liboracle.so`` (oracle.cpp): the paper's serial baseline — loop over all elements into a
+  per-node std::set (node mode) / std::vector (element mode), flattened to CSR.
+* ``stages`` (stages.py): the paper's GPU pipeline written out step by step in numpy, in the
+  paper's order (pair creation §2.2.1 step 1, sort step 2, segmented reduction + scan step 3),
+  one function per step, for per-step parity of the CUDA kernels.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / ``--impl reference`` leg may
+import this package.  The product (paper_1604_04689_b200) never imports it, and it never imports
+the product.  Parity status of every function is listed in DESIGN.md §"Oracle pins".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "oracle.cpp")
+
+OK, ERR_ARG, ERR_RANGE, ERR_DEGENERATE = 0, 1, 2, 3
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.cpp with plain g++ (no CUDA)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", _SRC, "-o", _SO])
+    return _SO
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        p64 = ctypes.POINTER(ctypes.c_int64)
+        pp64 = ctypes.POINTER(ctypes.POINTER(ctypes.c_int64))
+        pp32 = ctypes.POINTER(ctypes.POINTER(ctypes.c_int32))
+        p32 = ctypes.POINTER(ctypes.c_int32)
+        lib.oracle_validate.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
+                                        ctypes.c_int64, p64, p32]
+        lib.oracle_validate.restype = ctypes.c_int
+        for fn in (lib.oracle_node_csr, lib.oracle_elem_csr):
+            fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                           pp64, pp32, p64, p64, p32]
+            fn.restype = ctypes.c_int
+        lib.oracle_free.argtypes = [ctypes.c_void_p]
+        lib.oracle_free.restype = None
+        _lib = lib
+    return _lib
+
+
+class OracleMeshError(Exception):
+    def __init__(self, code, elem, pos):
+        super().__init__(f"oracle: code={code} elem={elem} pos={pos}")
+        self.code, self.elem, self.pos = code, elem, pos
+
+
+def _as_conn(conn) -> np.ndarray:
+    if hasattr(conn, "detach"):
+        conn = conn.detach().cpu().numpy()
+    conn = np.ascontiguousarray(conn, dtype=np.int32)
+    return conn
+
+
+def validate(etype: int, conn, num_nodes: int):
+    """(code, elem, pos) of the first invalid element, or (OK, -1, -1)."""
+    lib = _load()
+    c = _as_conn(conn)
+    ee, ep = ctypes.c_int64(-1), ctypes.c_int32(-1)
+    rc = lib.oracle_validate(etype, c.ctypes.data, c.shape[0] if c.ndim else 0, num_nodes,
+                             ctypes.byref(ee), ctypes.byref(ep))
+    return rc, ee.value, ep.value
+
+
+def _csr(fn, etype, conn, num_nodes):
+    lib = _load()
+    c = _as_conn(conn)
+    M = c.shape[0] if c.size else 0
+    off = ctypes.POINTER(ctypes.c_int64)()
+    idx = ctypes.POINTER(ctypes.c_int32)()
+    nnz = ctypes.c_int64(0)
+    ee, ep = ctypes.c_int64(-1), ctypes.c_int32(-1)
+    rc = fn(etype, c.ctypes.data, M, num_nodes, ctypes.byref(off), ctypes.byref(idx),
+            ctypes.byref(nnz), ctypes.byref(ee), ctypes.byref(ep))
+    if rc != OK:
+        raise OracleMeshError(rc, ee.value, ep.value)
+    offsets = np.ctypeslib.as_array(off, shape=(num_nodes + 1,)).copy()
+    indices = (np.ctypeslib.as_array(idx, shape=(nnz.value,)).copy() if nnz.value
+               else np.zeros(0, np.int32))
+    lib.oracle_free(ctypes.cast(off, ctypes.c_void_p))
+    lib.oracle_free(ctypes.cast(idx, ctypes.c_void_p))
+    return offsets, indices
+
+
+def node_csr(etype: int, conn, num_nodes: int):
+    """One-ring neighbouring nodes of every vertex as CSR (int64 offsets, int32 indices)."""
+    return _csr(_load().oracle_node_csr, etype, conn, num_nodes)
+
+
+def elem_csr(etype: int, conn, num_nodes: int):
+    """One-ring neighbouring elements of every vertex as CSR (int64 offsets, int32 indices)."""
+    return _csr(_load().oracle_elem_csr, etype, conn, num_nodes)
+
+
+from . import stages  # noqa: E402,F401  (numpy step-by-step oracle)

@@ -1,0 +1,121 @@
+// oracle/oracle.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// A plain, slow, obviously correct CPU implementation of what the CUDA path computes: the
+// paper's serial baseline (§1 "loop over all elements in a mesh to identify
+// (1) which pair of nodes is connected by an edge and (2) which nodes are contained in an
+// element"; §3.2.2 "a STL container ... to dynamically store the indices of
+// neighboring nodes for each vertex"), with a std::set per node as north_star asks, flattened
+// to CSR.
+//
+// Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg may
+// load this library.  It shares no code, header, table or helper with paper_1604_04689_b200/:
+// the edge tables below are written out here independently from the paper's definitions.
+//
+// Readings of the paper (DESIGN.md §"Readings"): duplicate pairs are collapsed (a one-ring is a
+// set), lists are ascending, invalid input is rejected reporting the lowest element id, then
+// the lowest position, range errors before repeated-node errors within an element.
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <set>
+#include <vector>
+
+namespace {
+
+// Element edge tables (§2.1.1: "any pair of neighboring nodes is connected
+// using an edge"; the paper spells out triangles only, §2.2; the other element types
+// follow DESIGN.md reading R4: quad ring, all 6 tet edges, VTK hexahedron's 12 edges).
+struct EdgeTable { int arity; int nedges; int a[12]; int b[12]; };
+
+const EdgeTable kTables[4] = {
+    // TRI3: three edges of the triangle (§2.2.1)
+    {3, 3, {0, 1, 2}, {1, 2, 0}},
+    // QUAD4: the 4 ring edges, no diagonals
+    {4, 4, {0, 1, 2, 3}, {1, 2, 3, 0}},
+    // TET4: every pair of the 4 nodes
+    {4, 6, {0, 0, 0, 1, 1, 2}, {1, 2, 3, 2, 3, 3}},
+    // HEX8 (VTK order: 0-3 bottom ring, 4-7 top ring, node 4 above node 0)
+    {8, 12, {0, 1, 2, 3, 4, 5, 6, 7, 0, 1, 2, 3}, {1, 2, 3, 0, 5, 6, 7, 4, 4, 5, 6, 7}},
+};
+
+enum { OK = 0, ERR_ARG = 1, ERR_RANGE = 2, ERR_DEGENERATE = 3 };
+
+// Validation in ascending element order; the first offending element decides.
+int validate(int etype, const int32_t* conn, int64_t M, int64_t N, int64_t* eelem, int32_t* epos) {
+  const int k = kTables[etype].arity;
+  for (int64_t e = 0; e < M; ++e) {
+    const int32_t* row = conn + e * k;
+    for (int p = 0; p < k; ++p) {
+      if (row[p] < 0 || (int64_t)row[p] >= N) { *eelem = e; *epos = p; return ERR_RANGE; }
+    }
+    for (int p = 1; p < k; ++p) {
+      for (int q = 0; q < p; ++q) {
+        if (row[q] == row[p]) { *eelem = e; *epos = p; return ERR_DEGENERATE; }
+      }
+    }
+  }
+  return OK;
+}
+
+template <class Container>
+void flatten(const std::vector<Container>& lists, int64_t N, int64_t** offsets, int32_t** indices,
+             int64_t* nnz) {
+  int64_t* off = (int64_t*)std::malloc(sizeof(int64_t) * (size_t)(N + 1));
+  off[0] = 0;
+  for (int64_t v = 0; v < N; ++v) off[v + 1] = off[v] + (int64_t)lists[v].size();
+  int32_t* idx = (int32_t*)std::malloc(sizeof(int32_t) * (size_t)(off[N] > 0 ? off[N] : 1));
+  int64_t pos = 0;
+  for (int64_t v = 0; v < N; ++v)
+    for (int32_t x : lists[v]) idx[pos++] = x;
+  *offsets = off;
+  *indices = idx;
+  *nnz = off[N];
+}
+
+}  // namespace
+
+extern "C" {
+
+int oracle_validate(int etype, const int32_t* conn, int64_t M, int64_t N, int64_t* err_elem,
+                    int32_t* err_pos) {
+  if (etype < 0 || etype > 3 || M < 0 || N < 0) return ERR_ARG;
+  *err_elem = -1;
+  *err_pos = -1;
+  return validate(etype, conn, M, N, err_elem, err_pos);
+}
+
+// Node mode: adj(v) = { u != v : some element has an edge {u, v} }, ascending.
+int oracle_node_csr(int etype, const int32_t* conn, int64_t M, int64_t N, int64_t** offsets,
+                    int32_t** indices, int64_t* nnz, int64_t* err_elem, int32_t* err_pos) {
+  int rc = oracle_validate(etype, conn, M, N, err_elem, err_pos);
+  if (rc != OK) return rc;
+  const EdgeTable& t = kTables[etype];
+  std::vector<std::set<int32_t>> S((size_t)N);
+  for (int64_t e = 0; e < M; ++e) {
+    const int32_t* row = conn + e * t.arity;
+    for (int j = 0; j < t.nedges; ++j) {
+      int32_t a = row[t.a[j]], b = row[t.b[j]];
+      S[(size_t)a].insert(b);
+      S[(size_t)b].insert(a);
+    }
+  }
+  flatten(S, N, offsets, indices, nnz);
+  return OK;
+}
+
+// Element mode: inc(v) = { e : v in conn[e] }, ascending (elements are visited in order).
+int oracle_elem_csr(int etype, const int32_t* conn, int64_t M, int64_t N, int64_t** offsets,
+                    int32_t** indices, int64_t* nnz, int64_t* err_elem, int32_t* err_pos) {
+  int rc = oracle_validate(etype, conn, M, N, err_elem, err_pos);
+  if (rc != OK) return rc;
+  const int k = kTables[etype].arity;
+  std::vector<std::vector<int32_t>> L((size_t)N);
+  for (int64_t e = 0; e < M; ++e)
+    for (int p = 0; p < k; ++p) L[(size_t)conn[e * k + p]].push_back((int32_t)e);
+  flatten(L, N, offsets, indices, nnz);
+  return OK;
+}
+
+void oracle_free(void* p) { std::free(p); }
+
+}  // extern "C"
