@@ -1,0 +1,226 @@
+/* meshnbr.h — C ABI of libmeshnbr.so: one-ring nodal neighbours of generic meshes on B200.
+ *
+ * Method: Mei, Xu, Tian, Li, "A Parallel Solution to Finding Nodal Neighbors in Generic Meshes"
+ * (arXiv 1604.04689; /root/reference/PAPER.md).  Every vertex gets
+ *   - its one-ring neighbouring NODES: "any pair of nodes connected by an edge is the one-ring
+ *     neighboring node for each other" (§1, §2.1.1), and
+ *   - its one-ring neighbouring ELEMENTS: "any element is directly the one-ring neighboring
+ *     element for those nodes it contains" (§1, §2.1.2),
+ * returned as CSR: int64 offsets[N+1] + int32 indices[nnz], every slice strictly ascending
+ * (the paper's "number" and "first indices" of each vertex's neighbours, L234-237, L487-489;
+ * readings R1-R3, R7, R12, R13 of DESIGN.md).
+ *
+ * Conventions for every entry point below
+ *   - Pointers named d_* are CUDA device pointers, h_* host pointers.  Connectivity is
+ *     int32 conn[num_elems][arity] row-major, 0-based, owned by the caller, read-only here.
+ *   - All work is stream-ordered on `stream` (a cudaStream_t passed as void*; NULL = legacy
+ *     default stream).  The mn_find_* calls block the calling thread exactly once (to read the
+ *     validation word and nnz: the output size is data-dependent) and return with the outputs
+ *     complete on `stream`.  Stage primitives (mn_emit_*, mn_radix_sort_*, ...) do not block
+ *     unless stated.
+ *   - Memory: outputs and workspace come from the caller's mn_allocator (NULL = the library's
+ *     cudaMallocAsync on `stream`).  Outputs are owned by the caller; release them with
+ *     mn_csr_release.  Workspace is released before return.  No global state except the
+ *     optional profiler (not thread-safe; bench only).
+ *   - Errors: invalid input is reported as the LOWEST offending element id, then the lowest
+ *     position in it; an index outside [0, N) is reported before a repeated node of the same
+ *     element (reading R8).  On any error no output is returned (out->offsets == NULL).
+ *   - Deterministic: identical inputs give bit-identical outputs.
+ *   - Limits: 0 <= num_nodes <= INT32_MAX, 0 <= num_elems, num_elems*arity*... pairs < 2^53.
+ */
+#ifndef MESHNBR_H_
+#define MESHNBR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MN_ABI_VERSION 1
+
+/* Element types (arity): edge sets per DESIGN.md reading R4 — TRI3 3 edges,
+ * QUAD4 4 ring edges, TET4 all 6 node pairs, HEX8 the 12 edges of a VTK_HEXAHEDRON (nodes 0-3
+ * bottom ring, 4-7 top ring, 4 above 0). */
+typedef enum { MN_TRI3 = 0, MN_QUAD4 = 1, MN_TET4 = 2, MN_HEX8 = 3 } mn_elem_type;
+
+typedef enum {
+  MN_OK = 0,
+  MN_ERR_INVALID_ARG = 1,        /* null pointer, negative size, N > INT32_MAX, unknown type   */
+  MN_ERR_INDEX_OUT_OF_RANGE = 2, /* conn[e][p] < 0 or >= N; detail = (e, p)                     */
+  MN_ERR_DEGENERATE = 3,         /* conn[e][p] == conn[e][q] for some q < p; detail = (e, p)    */
+  MN_ERR_CAPACITY = 4,           /* too many pairs for the 54-bit counters, or caller capacity */
+  MN_ERR_OOM = 5,                /* the allocator returned NULL                                  */
+  MN_ERR_CUDA = 6                /* a CUDA runtime error (launch, copy, sync)                    */
+} mn_status;
+
+typedef void* mn_stream; /* cudaStream_t */
+
+/* Stream-ordered allocator.  alloc returns NULL on failure; release may be called with NULL. */
+typedef struct mn_allocator {
+  void* (*alloc)(void* ctx, size_t bytes, mn_stream stream);
+  void (*release)(void* ctx, void* ptr, mn_stream stream);
+  void* ctx;
+} mn_allocator;
+
+/* CSR result.  offsets: num_nodes+1 entries, offsets[0] = 0, offsets[num_nodes] = nnz.
+ * indices: nnz entries (NULL when nnz == 0); the slice of vertex v, indices[offsets[v] ..
+ * offsets[v+1]), is strictly ascending.  Both arrays were obtained from `owner`. */
+typedef struct mn_csr {
+  int64_t num_nodes;
+  int64_t nnz;
+  int64_t* offsets;
+  int32_t* indices;
+  mn_allocator owner;
+} mn_csr;
+
+typedef struct mn_error_detail {
+  int64_t elem; /* offending element id, -1 if none */
+  int32_t pos;  /* offending local position, -1 if none */
+} mn_error_detail;
+
+/* ---------------------------------------------------------------------------------------------
+ * Whole path
+ * ------------------------------------------------------------------------------------------- */
+
+/* One-ring neighbouring NODES of every vertex (§2.2.1: create the pairs of
+ * every edge in both directions, sort them by the first integer, segmented reduction and scan).
+ * d_conn: device int32[num_elems * arity].  out: device CSR (allocator `alloc`).  err: nullable. */
+mn_status mn_find_node_neighbors(mn_elem_type type, const int32_t* d_conn, int64_t num_elems,
+                                 int64_t num_nodes, const mn_allocator* alloc, mn_stream stream,
+                                 mn_csr* out, mn_error_detail* err);
+
+/* One-ring neighbouring ELEMENTS of every vertex (§2.2.2: pairs (node, element
+ * itself), sorted by node, segmented reduction and scan).  Slices list element ids ascending. */
+mn_status mn_find_elem_neighbors(mn_elem_type type, const int32_t* d_conn, int64_t num_elems,
+                                 int64_t num_nodes, const mn_allocator* alloc, mn_stream stream,
+                                 mn_csr* out, mn_error_detail* err);
+
+/* Both outputs from one validation/histogram read of the connectivity (the bench's "step"). */
+mn_status mn_find_neighbors_both(mn_elem_type type, const int32_t* d_conn, int64_t num_elems,
+                                 int64_t num_nodes, const mn_allocator* alloc, mn_stream stream,
+                                 mn_csr* node_out, mn_csr* elem_out, mn_error_detail* err);
+
+/* Same as mn_find_neighbors_both with HOST buffers: h_conn is host memory (pinned for full PCIe
+ * speed); the connectivity is copied to the device, both CSRs are computed and copied back into
+ * host memory obtained from `host_alloc` (its alloc receives the byte count; stream unused).
+ * Device workspace comes from `dev_alloc`.  The outputs' `owner` is host_alloc. */
+mn_status mn_find_neighbors_both_host(mn_elem_type type, const int32_t* h_conn, int64_t num_elems,
+                                      int64_t num_nodes, const mn_allocator* dev_alloc,
+                                      const mn_allocator* host_alloc, mn_stream stream,
+                                      mn_csr* node_out, mn_csr* elem_out, mn_error_detail* err);
+
+/* Releases offsets/indices through csr->owner on `stream` and zeroes the struct. */
+void mn_csr_release(mn_csr* csr, mn_stream stream);
+
+const char* mn_status_string(mn_status status);
+int mn_abi_version(void);
+
+/* Peak device workspace (bytes, excluding the returned outputs) of the call above for this mesh
+ * (the memory cost the paper names as its shortcoming, §3.2.2).
+ * modes: 1 = nodes, 2 = elements, 3 = both. */
+mn_status mn_workspace_bytes(mn_elem_type type, int64_t num_elems, int64_t num_nodes, int modes,
+                             size_t* bytes);
+
+/* ---------------------------------------------------------------------------------------------
+ * Stage primitives (one per §8(a) row; the tests check each against oracle/stages.py)
+ * ------------------------------------------------------------------------------------------- */
+
+/* Node-key width in bytes for a mesh of num_nodes nodes: 4 when 2*b <= 32, else 8, where
+ * b = max(1, bit_length(num_nodes - 1)).  Key of pair (a, v) = (a << b) | v. */
+int mn_node_key_bits(int64_t num_nodes);   /* returns b */
+int mn_node_key_bytes(int64_t num_nodes);
+
+/* Row a1 — validate + create the node pairs of PAPER.md §2.2.1 L220-226 ("a triangle can produce
+ * six pairs"): for element e and edge j=(i0,i1) of the type's edge table, slot e*2E + 2j holds the
+ * packed key (conn[e][i0], conn[e][i1]) and slot e*2E + 2j + 1 the reverse.  d_keys: device,
+ * 2*E*num_elems keys of mn_node_key_bytes(num_nodes) bytes.  Blocks once (validation result). */
+mn_status mn_emit_node_pairs(mn_elem_type type, const int32_t* d_conn, int64_t num_elems,
+                             int64_t num_nodes, void* d_keys, mn_stream stream,
+                             mn_error_detail* err);
+
+/* Row a2 — validate + create the element pairs of PAPER.md §2.2.2: slot e*arity + p
+ * holds key conn[e][p] and value e.  d_keys, d_vals: device uint32[arity*num_elems]. */
+mn_status mn_emit_elem_pairs(mn_elem_type type, const int32_t* d_conn, int64_t num_elems,
+                             int64_t num_nodes, uint32_t* d_keys, uint32_t* d_vals,
+                             mn_stream stream, mn_error_detail* err);
+
+/* Row a3 — LSD radix sort (onesweep: decoupled look-back digit scans) of n unsigned keys of
+ * key_bytes (4 or 8) bytes, ascending on their low key_bits bits (bits above must be 0).
+ * In place on d_keys (workspace from alloc).  Stream-ordered, no blocking. */
+mn_status mn_radix_sort_keys(void* d_keys, int key_bytes, int64_t n, int key_bits,
+                             const mn_allocator* alloc, mn_stream stream);
+
+/* Row a3e — STABLE LSD radix sort of uint32 (key, value) pairs on the low key_bits key bits. */
+mn_status mn_radix_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_vals, int64_t n, int key_bits,
+                                  const mn_allocator* alloc, mn_stream stream);
+
+/* Rows a4+a5 (node mode) — from n ascending packed node keys (key_bytes 4/8, node bits b =
+ * mn_node_key_bits(num_nodes)): drop keys equal to their predecessor (reading R1), write the
+ * neighbour part (key & (2^b - 1)) of each survivor to d_indices (capacity n) and the CSR
+ * offsets of every node to d_offsets[num_nodes+1] (run lengths of the node part, exclusive scan;
+ * PAPER.md L234-245).  *h_nnz receives the survivor count (blocks once). */
+mn_status mn_unique_node_csr(const void* d_sorted_keys, int key_bytes, int64_t n,
+                             int64_t num_nodes, int64_t* d_offsets, int32_t* d_indices,
+                             int64_t* h_nnz, const mn_allocator* alloc, mn_stream stream);
+
+/* Rows a4+a5 (element mode) — CSR offsets d_offsets[num_nodes+1] from n ascending uint32 node
+ * keys (run lengths per node, exclusive scan; no dedupe: element pairs are unique).  No blocking. */
+mn_status mn_elem_offsets(const uint32_t* d_sorted_keys, int64_t n, int64_t num_nodes,
+                          int64_t* d_offsets, mn_stream stream);
+
+/* Row a5 — exclusive scan (single pass, decoupled look-back): d_out[0] = 0,
+ * d_out[i+1] = d_out[i] + d_counts[i], for n int32 counts -> n+1 int64.  No blocking. */
+mn_status mn_exclusive_scan_i32(const int32_t* d_counts, int64_t n, int64_t* d_out,
+                                const mn_allocator* alloc, mn_stream stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Multi-GPU building blocks: nodes are owned in contiguous ranges
+ * [r*ceil(N/G), (r+1)*ceil(N/G)); each rank holds an element shard with global element base.
+ * The exchange between the two calls is done by the caller (torch.distributed all_to_all over
+ * NCCL / NVLink); see paper_1604_04689_b200/dist.py.
+ * ------------------------------------------------------------------------------------------- */
+
+/* Validate the shard and bucket its node pairs and element pairs by owner rank.  Writes, for
+ * each destination rank g (0 <= g < world), the pairs it owns, contiguously in rank order:
+ *   d_node_keys: packed (a << b | v) uint64 keys, b = mn_node_key_bits(num_nodes), sorted by
+ *                owner, creation order kept inside each bucket;
+ *   d_elem_pairs: uint64 (node << 32 | global element id), same bucketing, creation order kept
+ *                (element-major, so each bucket is ascending in element id per node);
+ *   h_node_counts[g], h_elem_counts[g]: pair counts per destination (host, world entries).
+ * Buffers hold 2*E*shard_elems and arity*shard_elems entries.  Blocks once. */
+mn_status mn_dist_bucket(mn_elem_type type, const int32_t* d_conn_shard, int64_t shard_elems,
+                         int64_t global_elem_base, int64_t num_nodes, int world,
+                         uint64_t* d_node_keys, uint64_t* d_elem_pairs, int64_t* h_node_counts,
+                         int64_t* h_elem_counts, const mn_allocator* alloc, mn_stream stream,
+                         mn_error_detail* err);
+
+/* Finish on the owner: from the received node keys (any order) and element pairs (concatenated
+ * in source-rank order, so element ids ascend per node), build the CSR slice of nodes [lo, hi):
+ * offsets are local (slice offsets[0] = 0), indices global node / element ids. */
+mn_status mn_dist_finish(const uint64_t* d_node_keys, int64_t n_node_keys,
+                         const uint64_t* d_elem_pairs, int64_t n_elem_pairs, int64_t num_nodes,
+                         int64_t lo, int64_t hi, const mn_allocator* alloc, mn_stream stream,
+                         mn_csr* node_slice, mn_csr* elem_slice);
+
+/* ---------------------------------------------------------------------------------------------
+ * Instrumentation (bench only; not thread-safe)
+ * ------------------------------------------------------------------------------------------- */
+/* Count of kernels this library has launched since load. */
+int64_t mn_launch_count(void);
+/* When enabled, every kernel launch is bracketed by CUDA events on its stream. */
+void mn_profile_enable(int on);
+void mn_profile_reset(void);
+/* Synchronises the recorded events and returns the number of distinct kernel names. */
+int mn_profile_collect(void);
+/* Entry i of the collected table: kernel name, launches, total device ms, algorithmic bytes
+ * (sum over launches of the bytes the stage must move by definition, DESIGN.md §"Roofline"). */
+mn_status mn_profile_entry(int i, const char** name, int64_t* launches, double* total_ms,
+                           double* alg_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MESHNBR_H_ */

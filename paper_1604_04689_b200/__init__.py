@@ -1,0 +1,461 @@
+"""paper_1604_04689_b200 — B200-native one-ring nodal neighbours (Mei et al., arXiv 1604.04689).
+
+Thin ctypes binding over ``libmeshnbr.so`` (C ABI: include/meshnbr.h).  Argument marshalling only:
+every step of the path runs in the library's sm_100a kernels; torch supplies device memory (its
+caching allocator is handed to the library as an ``mn_allocator``), streams and process groups.
+There is no CPU fallback: if the library is missing or no CUDA device is present, calls raise.
+
+    import paper_1604_04689_b200 as mn
+    offsets, indices = mn.find_node_neighbors(conn_cuda_int32, "tet4", num_nodes)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+__all__ = [
+    "TRI3", "QUAD4", "TET4", "HEX8", "MeshError", "lib_path", "load",
+    "find_node_neighbors", "find_elem_neighbors", "find_neighbors", "find_neighbors_host",
+    "workspace_bytes", "node_key_bits", "node_key_bytes",
+    "emit_node_pairs", "emit_elem_pairs", "radix_sort_keys", "radix_sort_pairs_u32",
+    "unique_node_csr", "elem_offsets", "exclusive_scan",
+    "dist_bucket", "dist_finish",
+    "launch_count", "profile_enable", "profile_reset", "profile_collect",
+]
+
+TRI3, QUAD4, TET4, HEX8 = 0, 1, 2, 3
+ARITY = {TRI3: 3, QUAD4: 4, TET4: 4, HEX8: 8}
+_NAMES = {"tri3": TRI3, "tri": TRI3, "quad4": QUAD4, "quad": QUAD4, "tet4": TET4, "tet": TET4,
+          "hex8": HEX8, "hex": HEX8}
+
+MN_OK, MN_ERR_INVALID_ARG, MN_ERR_INDEX_OUT_OF_RANGE, MN_ERR_DEGENERATE = 0, 1, 2, 3
+MN_ERR_CAPACITY, MN_ERR_OOM, MN_ERR_CUDA = 4, 5, 6
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+
+
+def lib_path() -> str:
+    return os.path.join(_PKG, "libmeshnbr.so")
+
+
+class MeshError(RuntimeError):
+    """Raised for a non-OK mn_status; (code, elem, pos) as in include/meshnbr.h."""
+
+    def __init__(self, code: int, msg: str, elem: int = -1, pos: int = -1):
+        super().__init__(f"{msg} (status {code}, elem {elem}, pos {pos})")
+        self.code, self.elem, self.pos = code, elem, pos
+
+
+# ------------------------------------------------------------------------------------------------
+# ctypes declarations (mirror include/meshnbr.h)
+# ------------------------------------------------------------------------------------------------
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+_RELEASE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class _Allocator(ctypes.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("release", _RELEASE_FN), ("ctx", ctypes.c_void_p)]
+
+
+class _Csr(ctypes.Structure):
+    _fields_ = [("num_nodes", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("offsets", ctypes.c_void_p), ("indices", ctypes.c_void_p), ("owner", _Allocator)]
+
+
+class _ErrDetail(ctypes.Structure):
+    _fields_ = [("elem", ctypes.c_int64), ("pos", ctypes.c_int32)]
+
+
+_lib = None
+_VP, _I64, _I32, _INT = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
+_P = ctypes.POINTER
+
+
+def _declare(lib):
+    S = ctypes.c_int
+    sig = {
+        "mn_find_node_neighbors": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _VP, _P(_Csr), _P(_ErrDetail)]),
+        "mn_find_elem_neighbors": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _VP, _P(_Csr), _P(_ErrDetail)]),
+        "mn_find_neighbors_both": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _VP, _P(_Csr), _P(_Csr),
+                                       _P(_ErrDetail)]),
+        "mn_find_neighbors_both_host": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _P(_Allocator), _VP,
+                                            _P(_Csr), _P(_Csr), _P(_ErrDetail)]),
+        "mn_csr_release": (None, [_P(_Csr), _VP]),
+        "mn_status_string": (ctypes.c_char_p, [_INT]),
+        "mn_abi_version": (_INT, []),
+        "mn_workspace_bytes": (S, [_INT, _I64, _I64, _INT, _P(ctypes.c_size_t)]),
+        "mn_node_key_bits": (_INT, [_I64]),
+        "mn_node_key_bytes": (_INT, [_I64]),
+        "mn_emit_node_pairs": (S, [_INT, _VP, _I64, _I64, _VP, _VP, _P(_ErrDetail)]),
+        "mn_emit_elem_pairs": (S, [_INT, _VP, _I64, _I64, _VP, _VP, _VP, _P(_ErrDetail)]),
+        "mn_radix_sort_keys": (S, [_VP, _INT, _I64, _INT, _P(_Allocator), _VP]),
+        "mn_radix_sort_pairs_u32": (S, [_VP, _VP, _I64, _INT, _P(_Allocator), _VP]),
+        "mn_unique_node_csr": (S, [_VP, _INT, _I64, _I64, _VP, _VP, _P(_I64), _P(_Allocator), _VP]),
+        "mn_elem_offsets": (S, [_VP, _I64, _I64, _VP, _VP]),
+        "mn_exclusive_scan_i32": (S, [_VP, _I64, _VP, _P(_Allocator), _VP]),
+        "mn_dist_bucket": (S, [_INT, _VP, _I64, _I64, _I64, _INT, _VP, _VP, _P(_I64), _P(_I64),
+                               _P(_Allocator), _VP, _P(_ErrDetail)]),
+        "mn_dist_finish": (S, [_VP, _I64, _VP, _I64, _I64, _I64, _I64, _P(_Allocator), _VP, _P(_Csr),
+                               _P(_Csr)]),
+        "mn_launch_count": (_I64, []),
+        "mn_profile_enable": (None, [_INT]),
+        "mn_profile_reset": (None, []),
+        "mn_profile_collect": (_INT, []),
+        "mn_profile_entry": (S, [_INT, _P(ctypes.c_char_p), _P(_I64), _P(ctypes.c_double),
+                                 _P(ctypes.c_double)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+def load():
+    """Load libmeshnbr.so (built by __graft_entry__.build() / python -m paper_1604_04689_b200.build).
+    Raises if it is missing: there is no fallback path."""
+    global _lib
+    if _lib is None:
+        path = lib_path()
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: run `python -m paper_1604_04689_b200.build` "
+                              "(nvcc, sm_100a). There is no CPU fallback.")
+        lib = ctypes.CDLL(path)
+        _declare(lib)
+        _lib = lib
+    return _lib
+
+
+# ------------------------------------------------------------------------------------------------
+# torch caching allocator -> mn_allocator
+# ------------------------------------------------------------------------------------------------
+class _TorchAllocator:
+    """Hands out torch uint8 CUDA tensors; keeps them alive until released or adopted."""
+
+    def __init__(self, device):
+        self.device = device
+        self.live = {}
+        self._a = _ALLOC_FN(self._alloc)
+        self._r = _RELEASE_FN(self._release)
+        self.struct = _Allocator(self._a, self._r, None)
+
+    def _alloc(self, ctx, nbytes, stream):
+        try:
+            t = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        except RuntimeError:
+            return None
+        p = t.data_ptr()
+        self.live[p] = t
+        return p
+
+    def _release(self, ctx, ptr, stream):
+        if ptr:
+            self.live.pop(int(ptr), None)
+
+    def adopt(self, ptr, count, dtype):
+        """Take ownership of a library output as a typed tensor view."""
+        if not ptr or count == 0:
+            return torch.empty(0, dtype=dtype, device=self.device)
+        t = self.live.pop(int(ptr))
+        return t[: count * torch.empty(0, dtype=dtype).element_size()].view(dtype)
+
+
+class _PinnedAllocator:
+    """Host allocator for mn_find_neighbors_both_host: pinned torch CPU tensors."""
+
+    def __init__(self):
+        self.live = {}
+        self._a = _ALLOC_FN(self._alloc)
+        self._r = _RELEASE_FN(self._release)
+        self.struct = _Allocator(self._a, self._r, None)
+
+    def _alloc(self, ctx, nbytes, stream):
+        t = torch.empty(int(nbytes), dtype=torch.uint8, pin_memory=True)
+        self.live[t.data_ptr()] = t
+        return t.data_ptr()
+
+    def _release(self, ctx, ptr, stream):
+        if ptr:
+            self.live.pop(int(ptr), None)
+
+    def adopt(self, ptr, count, dtype):
+        if not ptr or count == 0:
+            return torch.empty(0, dtype=dtype)
+        t = self.live.pop(int(ptr))
+        return t[: count * torch.empty(0, dtype=dtype).element_size()].view(dtype)
+
+
+def _etype(t) -> int:
+    if isinstance(t, str):
+        return _NAMES[t.lower()]
+    t = int(t)
+    if t not in ARITY:
+        raise ValueError(f"unknown element type {t}")
+    return t
+
+
+def _stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check(rc, err=None):
+    if rc != MN_OK:
+        msg = load().mn_status_string(rc).decode()
+        raise MeshError(rc, msg, err.elem if err is not None else -1, err.pos if err is not None else -1)
+
+
+def _conn_arg(conn, etype):
+    if not isinstance(conn, torch.Tensor) or not conn.is_cuda:
+        raise TypeError("conn must be a CUDA tensor (there is no CPU path)")
+    if conn.dtype != torch.int32:
+        raise TypeError("conn must be int32")
+    k = ARITY[etype]
+    if conn.numel() % k:
+        raise ValueError(f"conn has {conn.numel()} entries, not a multiple of arity {k}")
+    return conn.contiguous(), conn.numel() // k
+
+
+def _take(al, csr):
+    n = int(csr.num_nodes)
+    off = al.adopt(csr.offsets, n + 1, torch.int64)
+    idx = al.adopt(csr.indices, int(csr.nnz), torch.int32)
+    return off, idx
+
+
+# ------------------------------------------------------------------------------------------------
+# whole path
+# ------------------------------------------------------------------------------------------------
+def find_node_neighbors(conn: torch.Tensor, etype, num_nodes: int, stream=None):
+    """One-ring neighbouring nodes of every vertex: (offsets int64[N+1], indices int32[nnz])."""
+    et = _etype(etype)
+    c, M = _conn_arg(conn, et)
+    lib = load()
+    al = _TorchAllocator(c.device)
+    out, err = _Csr(), _ErrDetail()
+    with torch.cuda.device(c.device):
+        rc = lib.mn_find_node_neighbors(et, c.data_ptr(), M, int(num_nodes), ctypes.byref(al.struct),
+                                        _stream_ptr(stream), ctypes.byref(out), ctypes.byref(err))
+    _check(rc, err)
+    return _take(al, out)
+
+
+def find_elem_neighbors(conn: torch.Tensor, etype, num_nodes: int, stream=None):
+    """One-ring neighbouring elements of every vertex: (offsets int64[N+1], indices int32[nnz])."""
+    et = _etype(etype)
+    c, M = _conn_arg(conn, et)
+    lib = load()
+    al = _TorchAllocator(c.device)
+    out, err = _Csr(), _ErrDetail()
+    with torch.cuda.device(c.device):
+        rc = lib.mn_find_elem_neighbors(et, c.data_ptr(), M, int(num_nodes), ctypes.byref(al.struct),
+                                        _stream_ptr(stream), ctypes.byref(out), ctypes.byref(err))
+    _check(rc, err)
+    return _take(al, out)
+
+
+def find_neighbors(conn: torch.Tensor, etype, num_nodes: int, stream=None):
+    """Both CSRs from one call: ((node_offsets, node_indices), (elem_offsets, elem_indices))."""
+    et = _etype(etype)
+    c, M = _conn_arg(conn, et)
+    lib = load()
+    al = _TorchAllocator(c.device)
+    no, eo, err = _Csr(), _Csr(), _ErrDetail()
+    with torch.cuda.device(c.device):
+        rc = lib.mn_find_neighbors_both(et, c.data_ptr(), M, int(num_nodes), ctypes.byref(al.struct),
+                                        _stream_ptr(stream), ctypes.byref(no), ctypes.byref(eo),
+                                        ctypes.byref(err))
+    _check(rc, err)
+    return _take(al, no), _take(al, eo)
+
+
+def find_neighbors_host(conn_host: torch.Tensor, etype, num_nodes: int, device=None, stream=None):
+    """End-to-end form: host (ideally pinned) int32 connectivity in, both CSRs back in pinned host
+    memory.  The H2D copy, the kernels and the D2H copies all run inside the library call."""
+    et = _etype(etype)
+    if conn_host.is_cuda or conn_host.dtype != torch.int32:
+        raise TypeError("conn_host must be a host int32 tensor")
+    c = conn_host.contiguous()
+    M = c.numel() // ARITY[et]
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    lib = load()
+    dal, hal = _TorchAllocator(dev), _PinnedAllocator()
+    no, eo, err = _Csr(), _Csr(), _ErrDetail()
+    with torch.cuda.device(dev):
+        rc = lib.mn_find_neighbors_both_host(et, c.data_ptr(), M, int(num_nodes), ctypes.byref(dal.struct),
+                                             ctypes.byref(hal.struct), _stream_ptr(stream), ctypes.byref(no),
+                                             ctypes.byref(eo), ctypes.byref(err))
+    _check(rc, err)
+    return _take(hal, no), _take(hal, eo)
+
+
+def workspace_bytes(etype, num_elems: int, num_nodes: int, modes: int = 3) -> int:
+    out = ctypes.c_size_t(0)
+    _check(load().mn_workspace_bytes(_etype(etype), int(num_elems), int(num_nodes), int(modes),
+                                     ctypes.byref(out)))
+    return int(out.value)
+
+
+def node_key_bits(num_nodes: int) -> int:
+    return int(load().mn_node_key_bits(int(num_nodes)))
+
+
+def node_key_bytes(num_nodes: int) -> int:
+    return int(load().mn_node_key_bytes(int(num_nodes)))
+
+
+# ------------------------------------------------------------------------------------------------
+# stage primitives (one per §8(a) row)
+# ------------------------------------------------------------------------------------------------
+def emit_node_pairs(conn: torch.Tensor, etype, num_nodes: int, stream=None) -> torch.Tensor:
+    """Row a1: packed node-pair keys in creation order (int64 for 8-byte keys, int32 bit pattern
+    of uint32 for 4-byte keys)."""
+    et = _etype(etype)
+    c, M = _conn_arg(conn, et)
+    kb = node_key_bytes(num_nodes)
+    E = {TRI3: 3, QUAD4: 4, TET4: 6, HEX8: 12}[et]
+    keys = torch.empty(2 * E * M, dtype=torch.int64 if kb == 8 else torch.int32, device=c.device)
+    err = _ErrDetail()
+    with torch.cuda.device(c.device):
+        rc = load().mn_emit_node_pairs(et, c.data_ptr(), M, int(num_nodes), keys.data_ptr(),
+                                       _stream_ptr(stream), ctypes.byref(err))
+    _check(rc, err)
+    return keys
+
+
+def emit_elem_pairs(conn: torch.Tensor, etype, num_nodes: int, stream=None):
+    """Row a2: (node keys, element values) in creation order, both int32 tensors."""
+    et = _etype(etype)
+    c, M = _conn_arg(conn, et)
+    n = ARITY[et] * M
+    keys = torch.empty(n, dtype=torch.int32, device=c.device)
+    vals = torch.empty(n, dtype=torch.int32, device=c.device)
+    err = _ErrDetail()
+    with torch.cuda.device(c.device):
+        rc = load().mn_emit_elem_pairs(et, c.data_ptr(), M, int(num_nodes), keys.data_ptr(), vals.data_ptr(),
+                                       _stream_ptr(stream), ctypes.byref(err))
+    _check(rc, err)
+    return keys, vals
+
+
+def radix_sort_keys(keys: torch.Tensor, key_bits: int, stream=None) -> torch.Tensor:
+    """Row a3: in-place ascending LSD sort of int64 (u64) or int32 (u32 bit pattern) keys."""
+    kb = keys.element_size()
+    al = _TorchAllocator(keys.device)
+    with torch.cuda.device(keys.device):
+        rc = load().mn_radix_sort_keys(keys.data_ptr(), kb, keys.numel(), int(key_bits), ctypes.byref(al.struct),
+                                       _stream_ptr(stream))
+    _check(rc)
+    return keys
+
+
+def radix_sort_pairs_u32(keys: torch.Tensor, vals: torch.Tensor, key_bits: int, stream=None):
+    """Row a3e: in-place stable LSD sort of uint32 (key, value) pairs."""
+    al = _TorchAllocator(keys.device)
+    with torch.cuda.device(keys.device):
+        rc = load().mn_radix_sort_pairs_u32(keys.data_ptr(), vals.data_ptr(), keys.numel(), int(key_bits),
+                                            ctypes.byref(al.struct), _stream_ptr(stream))
+    _check(rc)
+    return keys, vals
+
+
+def unique_node_csr(sorted_keys: torch.Tensor, num_nodes: int, stream=None):
+    """Rows a4+a5 (node mode): (offsets int64[N+1], indices int32[nnz]) from sorted packed keys."""
+    n = sorted_keys.numel()
+    off = torch.empty(int(num_nodes) + 1, dtype=torch.int64, device=sorted_keys.device)
+    idx = torch.empty(max(n, 1), dtype=torch.int32, device=sorted_keys.device)
+    nnz = ctypes.c_int64(0)
+    al = _TorchAllocator(sorted_keys.device)
+    with torch.cuda.device(sorted_keys.device):
+        rc = load().mn_unique_node_csr(sorted_keys.data_ptr(), sorted_keys.element_size(), n, int(num_nodes),
+                                       off.data_ptr(), idx.data_ptr(), ctypes.byref(nnz), ctypes.byref(al.struct),
+                                       _stream_ptr(stream))
+    _check(rc)
+    return off, idx[: nnz.value]
+
+
+def elem_offsets(sorted_keys: torch.Tensor, num_nodes: int, stream=None) -> torch.Tensor:
+    """Rows a4+a5 (element mode): offsets int64[N+1] from stably sorted node keys."""
+    off = torch.empty(int(num_nodes) + 1, dtype=torch.int64, device=sorted_keys.device)
+    with torch.cuda.device(sorted_keys.device):
+        rc = load().mn_elem_offsets(sorted_keys.data_ptr(), sorted_keys.numel(), int(num_nodes), off.data_ptr(),
+                                    _stream_ptr(stream))
+    _check(rc)
+    return off
+
+
+def exclusive_scan(counts: torch.Tensor, stream=None) -> torch.Tensor:
+    """Row a5: int32 counts -> int64 exclusive scan with the total appended (n+1 entries)."""
+    out = torch.empty(counts.numel() + 1, dtype=torch.int64, device=counts.device)
+    al = _TorchAllocator(counts.device)
+    with torch.cuda.device(counts.device):
+        rc = load().mn_exclusive_scan_i32(counts.data_ptr(), counts.numel(), out.data_ptr(), ctypes.byref(al.struct),
+                                          _stream_ptr(stream))
+    _check(rc)
+    return out
+
+
+# ------------------------------------------------------------------------------------------------
+# multi-GPU building blocks (orchestrated by paper_1604_04689_b200.dist)
+# ------------------------------------------------------------------------------------------------
+def dist_bucket(conn_shard: torch.Tensor, etype, global_elem_base: int, num_nodes: int, world: int, stream=None):
+    """Bucket this shard's node pairs and element pairs by owner rank.
+    Returns (node_keys int64, node_counts[world], elem_pairs int64, elem_counts[world])."""
+    et = _etype(etype)
+    c, M = _conn_arg(conn_shard, et)
+    E = {TRI3: 3, QUAD4: 4, TET4: 6, HEX8: 12}[et]
+    nk = torch.empty(2 * E * M, dtype=torch.int64, device=c.device)
+    ep = torch.empty(ARITY[et] * M, dtype=torch.int64, device=c.device)
+    hn = (ctypes.c_int64 * world)()
+    he = (ctypes.c_int64 * world)()
+    al = _TorchAllocator(c.device)
+    err = _ErrDetail()
+    with torch.cuda.device(c.device):
+        rc = load().mn_dist_bucket(et, c.data_ptr(), M, int(global_elem_base), int(num_nodes), int(world),
+                                   nk.data_ptr(), ep.data_ptr(), hn, he, ctypes.byref(al.struct),
+                                   _stream_ptr(stream), ctypes.byref(err))
+    _check(rc, err)
+    return nk, list(hn), ep, list(he)
+
+
+def dist_finish(node_keys: torch.Tensor, elem_pairs: torch.Tensor, num_nodes: int, lo: int, hi: int, stream=None):
+    """CSR slices of the owned node range [lo, hi) from the received pairs."""
+    dev = node_keys.device
+    al = _TorchAllocator(dev)
+    ns, es = _Csr(), _Csr()
+    with torch.cuda.device(dev):
+        rc = load().mn_dist_finish(node_keys.data_ptr() if node_keys.numel() else None, node_keys.numel(),
+                                   elem_pairs.data_ptr() if elem_pairs.numel() else None, elem_pairs.numel(),
+                                   int(num_nodes), int(lo), int(hi), ctypes.byref(al.struct), _stream_ptr(stream),
+                                   ctypes.byref(ns), ctypes.byref(es))
+    _check(rc)
+    return _take(al, ns), _take(al, es)
+
+
+# ------------------------------------------------------------------------------------------------
+# instrumentation
+# ------------------------------------------------------------------------------------------------
+def launch_count() -> int:
+    return int(load().mn_launch_count())
+
+
+def profile_enable(on: bool = True):
+    load().mn_profile_enable(1 if on else 0)
+
+
+def profile_reset():
+    load().mn_profile_reset()
+
+
+def profile_collect():
+    """[{name, launches, ms, alg_bytes}] per kernel name since the last reset."""
+    lib = load()
+    n = lib.mn_profile_collect()
+    out = []
+    for i in range(n):
+        name = ctypes.c_char_p()
+        la, ms, by = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
+        lib.mn_profile_entry(i, ctypes.byref(name), ctypes.byref(la), ctypes.byref(ms), ctypes.byref(by))
+        out.append(dict(name=name.value.decode(), launches=la.value, ms=ms.value, alg_bytes=by.value))
+    return out

@@ -1,0 +1,132 @@
+// common.cuh — shared device definitions of libmeshnbr (sm_100a only).
+//
+// Nothing here is shared with oracle/: the element tables below are this side's own encoding of
+// DESIGN.md reading R4/R5 (edge lists) — see the comments next to each literal.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "meshnbr.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libmeshnbr is written for sm_100a (B200) only"
+#endif
+
+namespace mn {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint64_t ERR_NONE = ~0ull;
+
+// ------------------------------------------------------------------------------------------------
+// Validation word: the lowest (element, kind, position) wins an atomicMin.
+//   word = elem << 5 | kind << 4 | pos ; kind 0 = index out of range, 1 = repeated node (R8)
+// ------------------------------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t err_encode(uint64_t elem, int kind, int pos) {
+  return (elem << 5) | ((uint64_t)kind << 4) | (uint64_t)pos;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Look-back status words (decoupled look-back, Merrill & Garland 2016 / onesweep, Adinets &
+// Merrill 2022).  64-bit so a digit bucket may exceed 2^30 pairs (config 5 has 2.36e9 pairs):
+//   [63:56] epoch (pass number + 1; a word from an earlier pass reads as "not ready")
+//   [55:54] flag  (1 = tile aggregate, 2 = inclusive prefix)
+//   [53:0]  value
+// ------------------------------------------------------------------------------------------------
+constexpr uint64_t ST_AGG = 1, ST_INC = 2;
+constexpr uint64_t ST_VMASK = (1ull << 54) - 1;
+
+__device__ __forceinline__ uint64_t st_pack(uint32_t epoch, uint64_t flag, uint64_t v) {
+  return ((uint64_t)epoch << 56) | (flag << 54) | v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Wait for the status word of one predecessor and return (flag, value).
+__device__ __forceinline__ uint64_t lookback_wait(const uint64_t* p, uint32_t epoch) {
+  uint64_t w = ld_relaxed_u64(p);
+  int spins = 0;
+  while ((uint32_t)(w >> 56) != epoch || ((w >> 54) & 3u) == 0) {
+    if (++spins > 4) __nanosleep(32);
+    w = ld_relaxed_u64(p);
+  }
+  return w;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Streaming loads that do not pollute L1 (each key is read exactly once per pass).
+__device__ __forceinline__ uint64_t ld_stream(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Element types.  For node pairs, slot r in [0, 2E) of an element holds (conn[la(r)], conn[lb(r)]):
+// r = 2j is edge j forward, r = 2j+1 edge j reversed (R5).  la/lb are 4-bit local
+// indices packed into 128-bit literals (slot r at bits 4r..4r+3).
+// ------------------------------------------------------------------------------------------------
+template <int T> struct Elem;
+template <> struct Elem<MN_TRI3> {   // edges (0,1) (1,2) (2,0)
+  static constexpr int K = 3, E = 3, C = 2;          // C = edges incident to each local node
+  static constexpr uint64_t A_LO = 0x22110ull, A_HI = 0, B_LO = 0x201201ull, B_HI = 0;
+};
+template <> struct Elem<MN_QUAD4> {  // ring edges (0,1) (1,2) (2,3) (3,0), no diagonals
+  static constexpr int K = 4, E = 4, C = 2;
+  static constexpr uint64_t A_LO = 0x3322110ull, A_HI = 0, B_LO = 0x30231201ull, B_HI = 0;
+};
+template <> struct Elem<MN_TET4> {   // (0,1) (0,2) (0,3) (1,2) (1,3) (2,3)
+  static constexpr int K = 4, E = 6, C = 3;
+  static constexpr uint64_t A_LO = 0x323121302010ull, A_HI = 0, B_LO = 0x231312030201ull, B_HI = 0;
+};
+template <> struct Elem<MN_HEX8> {   // VTK: (0,1)(1,2)(2,3)(3,0)(4,5)(5,6)(6,7)(7,4)(0,4)(1,5)(2,6)(3,7)
+  static constexpr int K = 8, E = 12, C = 3;
+  static constexpr uint64_t A_LO = 0x4776655403322110ull, A_HI = 0x73625140ull,
+                            B_LO = 0x7467564530231201ull, B_HI = 0x37261504ull;
+};
+
+template <int T>
+__device__ __forceinline__ void slot_locals(int r, int& la, int& lb) {
+  using EL = Elem<T>;
+  if (EL::A_HI == 0 || r < 16) {
+    la = (int)((EL::A_LO >> (4 * r)) & 0xF);
+    lb = (int)((EL::B_LO >> (4 * r)) & 0xF);
+  } else {
+    la = (int)((EL::A_HI >> (4 * (r - 16))) & 0xF);
+    lb = (int)((EL::B_HI >> (4 * (r - 16))) & 0xF);
+  }
+}
+
+inline int arity_of(int t) { return t == MN_TRI3 ? 3 : (t == MN_HEX8 ? 8 : 4); }
+inline int edges_of(int t) { return t == MN_TRI3 ? 3 : t == MN_QUAD4 ? 4 : t == MN_TET4 ? 6 : 12; }
+
+// Bits of a node id: b = max(1, bit_length(N - 1)) (R11).
+inline int node_bits(int64_t N) {
+  int b = 0;
+  uint64_t x = N > 1 ? (uint64_t)(N - 1) : 0;
+  while (x) { ++b; x >>= 1; }
+  return b < 1 ? 1 : b;
+}
+
+}  // namespace mn

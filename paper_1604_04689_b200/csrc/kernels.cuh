@@ -1,0 +1,597 @@
+// kernels.cuh — the hot-path kernels of libmeshnbr (sm_100a).
+//
+// Method (§2.2.1, §2.2.2): create (node, neighbour) and (node,
+// element) integer pairs, sort them by the first integer, then segmented reduction + scan give
+// each vertex's count and first index.  B200 design (DESIGN.md §"Kernels"):
+//   k_hist_validate   validate conn + digit histograms of the node ids (one read of conn)
+//   k_bucket_bases    per-pass global digit bucket bases (exclusive scan of the histograms)
+//   k_onesweep        one LSD digit pass: warp-match ranking, decoupled look-back, smem scatter;
+//                     pass 0 creates the pairs from conn on the fly (no emitted-pair round trip)
+//   k_unique_node     fused adjacent-difference dedupe + compaction + run length -> offsets
+//   k_elem_offsets    run starts of the sorted element-pair keys -> offsets
+//   k_scan_i32        single-pass look-back exclusive scan (standalone row a5)
+#pragma once
+
+#include "common.cuh"
+
+namespace mn {
+
+// ================================================================================================
+// Digit plan.  A node id of b bits is split into nd digits (widths w_j, shifts s_j).  Node keys
+// (a << b | v) are sorted LSD over the v digits then the a digits; element keys (node) over the nd
+// digits.  Because every local node of a TRI3/QUAD4/TET4/HEX8 element has the same number C of
+// incident element edges, the histogram of any node-key digit equals C x the histogram of that
+// digit over the conn entries — so one pass over conn yields every pass's bucket sizes.
+// ================================================================================================
+struct DigitPlan {
+  int nd;
+  int shift[4];
+  int width[4];
+};
+
+struct PassDigit {   // digit(key) = OWNER ? (key >> shift) / div : (key >> shift) & mask
+  int shift;
+  uint32_t mask;
+  uint64_t div;
+};
+
+template <typename KeyT, bool OWNER>
+__device__ __forceinline__ uint32_t digit_of(KeyT key, const PassDigit& pd, uint32_t maxbin) {
+  if (OWNER) {
+    uint64_t d = ((uint64_t)key >> pd.shift) / pd.div;
+    return d > maxbin ? maxbin : (uint32_t)d;
+  } else {
+    return (uint32_t)(key >> pd.shift) & pd.mask;
+  }
+}
+
+// ================================================================================================
+// k_hist_validate: one thread per element.  Validation (reading R8) + per-digit histograms of the
+// node ids of valid elements.  Histograms are CTA-private in shared memory, flushed once.
+// ================================================================================================
+template <int T, int BINS>
+__global__ void __launch_bounds__(256)
+k_hist_validate(const int32_t* __restrict__ conn, int64_t M, int64_t N, int64_t elem_base,
+                DigitPlan dp, int owner_hist, uint64_t owner_div,
+                unsigned long long* __restrict__ hist, unsigned long long* __restrict__ err) {
+  constexpr int K = Elem<T>::K;
+  __shared__ uint32_t sh[4 * BINS];
+  const int nh = owner_hist ? 1 : dp.nd;
+  for (int i = threadIdx.x; i < nh * BINS; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < M;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int v[K];
+#pragma unroll
+    for (int p = 0; p < K; ++p) v[p] = __ldg(conn + e * K + p);
+    int bad = -1, kind = 0;
+#pragma unroll
+    for (int p = K - 1; p >= 0; --p)
+      if (v[p] < 0 || (int64_t)v[p] >= N) bad = p;
+    if (bad < 0) {
+#pragma unroll
+      for (int p = K - 1; p >= 1; --p) {
+        bool dup = false;
+#pragma unroll
+        for (int q = 0; q < p; ++q) dup |= (v[q] == v[p]);
+        if (dup) { bad = p; kind = 1; }
+      }
+    }
+    if (bad >= 0) {
+      atomicMin(err, (unsigned long long)err_encode((uint64_t)(elem_base + e), kind, bad));
+      continue;
+    }
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      if (owner_hist) {
+        uint64_t d = (uint64_t)v[p] / owner_div;
+        atomicAdd(&sh[d < BINS ? d : BINS - 1], 1u);
+      } else {
+        for (int j = 0; j < dp.nd; ++j)
+          atomicAdd(&sh[j * BINS + (((uint32_t)v[p] >> dp.shift[j]) & ((1u << dp.width[j]) - 1))], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nh * BINS; i += blockDim.x)
+    if (sh[i]) atomicAdd(hist + i, (unsigned long long)sh[i]);
+}
+
+// Histograms of arbitrary keys (generic sort entry point): all digits of 8 bits.
+template <typename KeyT>
+__global__ void __launch_bounds__(256)
+k_hist_keys(const KeyT* __restrict__ keys, int64_t n, int ndig, unsigned long long* __restrict__ hist) {
+  __shared__ uint32_t sh[8 * 256];
+  for (int i = threadIdx.x; i < ndig * 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    KeyT k = keys[i];
+    for (int j = 0; j < ndig; ++j) atomicAdd(&sh[j * 256 + (uint32_t)((k >> (8 * j)) & 0xFF)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ndig * 256; i += blockDim.x)
+    if (sh[i]) atomicAdd(hist + i, (unsigned long long)sh[i]);
+}
+
+// ================================================================================================
+// k_bucket_bases: block q computes bases[q][d] = mult_q * sum_{d' < d} hist[hidx_q][d'].
+// ================================================================================================
+struct BasesDesc {
+  int npass;
+  int hidx[16];
+  int mult[16];
+};
+
+template <int BINS>
+__global__ void __launch_bounds__(BINS)
+k_bucket_bases(const unsigned long long* __restrict__ hist, BasesDesc bd, uint64_t* __restrict__ bases,
+               const unsigned long long* __restrict__ err) {
+  if (err && *err != ERR_NONE) return;
+  __shared__ uint64_t wsum[BINS / 32];
+  const int q = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  uint64_t x = (uint64_t)bd.mult[q] * hist[bd.hidx[q] * BINS + t];
+  uint64_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t y = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  uint64_t pre = 0;
+  for (int i = 0; i < w; ++i) pre += wsum[i];
+  bases[q * BINS + t] = pre + inc - x;
+}
+
+// ================================================================================================
+// k_onesweep: one stable LSD digit pass (onesweep).
+//   SRC 0: keys (and values) from arrays
+//   SRC 1: node pair keys (a << b | v) created from conn on the fly (slot order e*2E + r)
+//   SRC 2: element pair keys conn[i] with value i / K created from conn on the fly
+//   SRC 3: element pairs packed (node << 32 | elem_base + i / K) created from conn (dist bucketing)
+// Tile = THREADS*ITEMS items in warp-striped order (warp w owns a contiguous 32*ITEMS chunk, item
+// i of lane l is chunk[i*32 + l]), so the per-warp running histogram ranks keys stably.
+// ================================================================================================
+struct PassArgs {
+  const void* keys_in;
+  void* keys_out;
+  const uint32_t* vals_in;
+  uint32_t* vals_out;
+  const int32_t* conn;
+  int node_bits;       // SRC 1: b
+  int64_t elem_base;   // SRC 3
+  int64_t n;
+  PassDigit pd;
+  const uint64_t* bases;   // [BINS]
+  uint64_t* status;        // [tiles][BINS]
+  uint32_t* ticket;
+  uint32_t epoch;
+  const unsigned long long* err;
+};
+
+template <int THREADS, int ITEMS, int BINS>
+struct OnesweepSmem {
+  static constexpr int WARPS = THREADS / 32;
+  uint32_t whist[WARPS][BINS];
+  uint32_t binstart[BINS];
+  uint64_t gofs[BINS];
+  uint64_t wsum[WARPS];
+  uint32_t tile;
+};
+
+template <typename KeyT, int SRC, int T, bool PAYLOAD, bool OWNER, int BINS, int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS)
+k_onesweep(PassArgs pa) {
+  constexpr int WARPS = THREADS / 32;
+  constexpr int TILE = THREADS * ITEMS;
+  constexpr int BPT = BINS / THREADS;   // bins owned per thread (contiguous)
+  static_assert(BINS % THREADS == 0, "BINS must be a multiple of THREADS");
+  using Sm = OnesweepSmem<THREADS, ITEMS, BINS>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
+  KeyT* skeys = reinterpret_cast<KeyT*>(smem_raw + ((sizeof(Sm) + 15) & ~size_t(15)));
+  uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + TILE);
+
+  if (*pa.err != ERR_NONE) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) sm.tile = atomicAdd(pa.ticket, 1u);
+  for (int i = tid; i < WARPS * BINS; i += THREADS) (&sm.whist[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile = sm.tile;
+  const int64_t base = (int64_t)tile * TILE;
+  const int64_t chunk = base + (int64_t)warp * 32 * ITEMS;
+
+  // ---- load (pair creation for pass 0) ----
+  KeyT key[ITEMS];
+  uint32_t val[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t idx = chunk + i * 32 + lane;
+    val[i] = 0;
+    if (idx < pa.n) {
+      if (SRC == 0) {
+        key[i] = ld_stream(reinterpret_cast<const KeyT*>(pa.keys_in) + idx);
+        if (PAYLOAD) val[i] = ld_stream(pa.vals_in + idx);
+      } else if (SRC == 1) {
+        constexpr int K = Elem<T>::K, S = 2 * Elem<T>::E;
+        const int64_t e = idx / S;
+        const int r = (int)(idx - e * S);
+        int la, lb;
+        slot_locals<T>(r, la, lb);
+        const uint32_t a = (uint32_t)__ldg(pa.conn + e * K + la);
+        const uint32_t v = (uint32_t)__ldg(pa.conn + e * K + lb);
+        key[i] = (KeyT)(((KeyT)a << pa.node_bits) | (KeyT)v);
+      } else if (SRC == 2) {
+        constexpr int K = Elem<T>::K;
+        key[i] = (KeyT)(uint32_t)__ldg(pa.conn + idx);
+        val[i] = (uint32_t)(idx / K);
+      } else {
+        constexpr int K = Elem<T>::K;
+        key[i] = (KeyT)(((uint64_t)(uint32_t)__ldg(pa.conn + idx) << 32) |
+                        (uint64_t)(pa.elem_base + idx / K));
+      }
+    } else {
+      key[i] = (KeyT)~(KeyT)0;
+    }
+  }
+
+  // ---- rank: per-warp running digit histogram, warp-match aggregated ----
+  uint32_t rank[ITEMS];
+  uint32_t dig[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t idx = chunk + i * 32 + lane;
+    const uint32_t d = idx < pa.n ? digit_of<KeyT, OWNER>(key[i], pa.pd, BINS - 1) : (uint32_t)(BINS - 1);
+    dig[i] = d;
+    const unsigned peers = __match_any_sync(FULL, d);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (lane == leader) {
+      old = sm.whist[warp][d];
+      sm.whist[warp][d] = old + __popc(peers);
+    }
+    old = __shfl_sync(FULL, old, leader);
+    rank[i] = old + __popc(peers & lanemask_lt());
+  }
+  __syncthreads();
+
+  // ---- tile digit counts, publish aggregates ----
+  const int64_t nvalid64 = pa.n - base;
+  const int nvalid = nvalid64 >= TILE ? TILE : (int)nvalid64;
+  uint32_t cnt[BPT];
+  uint32_t tsum = 0;
+#pragma unroll
+  for (int j = 0; j < BPT; ++j) {
+    const int b = tid * BPT + j;
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      const uint32_t t = sm.whist[w][b];
+      sm.whist[w][b] = run;
+      run += t;
+    }
+    cnt[j] = run;
+    tsum += run;
+    const uint32_t pub = (b == BINS - 1) ? run - (uint32_t)(TILE - nvalid) : run;
+    st_relaxed_u64(pa.status + (size_t)tile * BINS + b, st_pack(pa.epoch, tile == 0 ? ST_INC : ST_AGG, pub));
+  }
+  // ---- local exclusive scan of the tile counts over bins ----
+  uint32_t inc = tsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) sm.wsum[warp] = inc;
+  __syncthreads();
+  uint32_t pre = 0;
+#pragma unroll
+  for (int w = 0; w < WARPS; ++w)
+    if (w < warp) pre += (uint32_t)sm.wsum[w];
+  uint32_t run = pre + inc - tsum;
+#pragma unroll
+  for (int j = 0; j < BPT; ++j) {
+    sm.binstart[tid * BPT + j] = run;
+    run += cnt[j];
+  }
+  __syncthreads();
+
+  // ---- scatter keys (and values) into shared memory in local digit order ----
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t d = dig[i];
+    const uint32_t pos = sm.binstart[d] + sm.whist[warp][d] + rank[i];
+    if (pos < (uint32_t)nvalid) {
+      skeys[pos] = key[i];
+      if (PAYLOAD || SRC == 2) svals[pos] = val[i];
+    }
+  }
+
+  // ---- decoupled look-back over the previous tiles, per owned digit ----
+#pragma unroll
+  for (int j = 0; j < BPT; ++j) {
+    const int b = tid * BPT + j;
+    uint64_t excl = 0;
+    if (tile > 0) {
+      int64_t t = (int64_t)tile - 1;
+      while (true) {
+        const uint64_t w = lookback_wait(pa.status + (size_t)t * BINS + b, pa.epoch);
+        excl += w & ST_VMASK;
+        if (((w >> 54) & 3u) == ST_INC) break;
+        --t;
+      }
+      const uint32_t mine = (b == BINS - 1) ? cnt[j] - (uint32_t)(TILE - nvalid) : cnt[j];
+      st_relaxed_u64(pa.status + (size_t)tile * BINS + b, st_pack(pa.epoch, ST_INC, excl + mine));
+    }
+    sm.gofs[b] = pa.bases[b] + excl - sm.binstart[b];
+  }
+  __syncthreads();
+
+  // ---- write out: consecutive local slots of a digit go to consecutive global slots ----
+  KeyT* kout = reinterpret_cast<KeyT*>(pa.keys_out);
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const int li = j * THREADS + tid;
+    if (li < nvalid) {
+      const KeyT k = skeys[li];
+      const uint64_t g = sm.gofs[digit_of<KeyT, OWNER>(k, pa.pd, BINS - 1)] + li;
+      kout[g] = k;
+      if (PAYLOAD || SRC == 2) pa.vals_out[g] = svals[li];
+    }
+  }
+}
+
+// ================================================================================================
+// k_unique_node: rows a4 + a5 fused for node mode.  Sorted keys in, warp-striped tiles:
+//   flag(i)   = i == 0 || key[i] != key[i-1]                       (adjacent-difference dedupe)
+//   pos(i)    = number of flags before i  (ballot/popc in the warp, look-back across tiles)
+//   indices[pos(i)] = key[i] & (2^b - 1)  for flagged i             (compaction)
+//   at a node change, offsets[x] = pos(i) for every node x in (node(key[i-1]), node(key[i])]
+//   the last key fills offsets[x] = nnz for x in (node(last), N]     (run length + scan fused)
+// ================================================================================================
+struct UniqueArgs {
+  const void* keys;
+  int64_t n;
+  int b;
+  int64_t N;
+  int64_t* offsets;
+  uint32_t* indices;
+  uint64_t* status;   // [tiles]
+  uint32_t* ticket;
+  uint32_t epoch;
+  unsigned long long* nnz;
+  const unsigned long long* err;
+};
+
+template <typename KeyT, int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS)
+k_unique_node(UniqueArgs ua) {
+  constexpr int WARPS = THREADS / 32;
+  constexpr int TILE = THREADS * ITEMS;
+  __shared__ uint32_t s_wcount[WARPS];
+  __shared__ uint64_t s_texcl;
+  __shared__ uint32_t s_tile;
+  if (*ua.err != ERR_NONE) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(ua.ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t chunk = (int64_t)tile * TILE + (int64_t)warp * 32 * ITEMS;
+  const KeyT* keys = reinterpret_cast<const KeyT*>(ua.keys);
+
+  KeyT key[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t idx = chunk + i * 32 + lane;
+    key[i] = idx < ua.n ? ld_stream(keys + idx) : (KeyT)0;
+  }
+  KeyT before = (KeyT)0;   // the key preceding this warp's chunk
+  if (lane == 0 && chunk > 0 && chunk < ua.n) before = keys[chunk - 1];
+  before = __shfl_sync(FULL, before, 0);
+
+  unsigned bal[ITEMS];
+  uint32_t wcount = 0;
+  KeyT prevk[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t idx = chunk + i * 32 + lane;
+    const KeyT up = __shfl_up_sync(FULL, key[i], 1);
+    const KeyT last = __shfl_sync(FULL, i > 0 ? key[i > 0 ? i - 1 : 0] : before, 31);
+    const KeyT p = lane > 0 ? up : (i > 0 ? last : before);
+    prevk[i] = p;
+    const bool f = idx < ua.n && (idx == 0 || key[i] != p);
+    bal[i] = __ballot_sync(FULL, f);
+    wcount += __popc(bal[i]);
+  }
+  if (lane == 0) s_wcount[warp] = wcount;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t tot = 0;
+    for (int w = 0; w < WARPS; ++w) {
+      const uint32_t c = s_wcount[w];
+      s_wcount[w] = tot;
+      tot += c;
+    }
+    uint64_t excl = 0;
+    if (tile == 0) {
+      st_relaxed_u64(ua.status, st_pack(ua.epoch, ST_INC, tot));
+    } else {
+      st_relaxed_u64(ua.status + tile, st_pack(ua.epoch, ST_AGG, tot));
+      int64_t t = (int64_t)tile - 1;
+      while (true) {
+        const uint64_t w = lookback_wait(ua.status + t, ua.epoch);
+        excl += w & ST_VMASK;
+        if (((w >> 54) & 3u) == ST_INC) break;
+        --t;
+      }
+      st_relaxed_u64(ua.status + tile, st_pack(ua.epoch, ST_INC, excl + tot));
+    }
+    s_texcl = excl;
+  }
+  __syncthreads();
+  uint64_t pos = s_texcl + s_wcount[warp];
+  const KeyT vmask = (KeyT)(((KeyT)1 << ua.b) - 1);
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t idx = chunk + i * 32 + lane;
+    const bool f = (bal[i] >> lane) & 1u;
+    const uint64_t mypos = pos + __popc(bal[i] & lanemask_lt());
+    if (f) {
+      ua.indices[mypos] = (uint32_t)(key[i] & vmask);
+      const int64_t a = (int64_t)(key[i] >> ua.b);
+      const int64_t pa = idx == 0 ? -1 : (int64_t)(prevk[i] >> ua.b);
+      for (int64_t x = pa + 1; x <= a; ++x) ua.offsets[x] = (int64_t)mypos;
+    }
+    if (idx == ua.n - 1) {
+      const uint64_t total = mypos + (f ? 1 : 0);
+      for (int64_t x = (int64_t)(key[i] >> ua.b) + 1; x <= ua.N; ++x) ua.offsets[x] = (int64_t)total;
+      *ua.nnz = total;
+    }
+    pos += __popc(bal[i]);
+  }
+}
+
+// ================================================================================================
+// k_elem_offsets: offsets from the stably sorted element-pair keys (no dedupe needed: (node,
+// element) pairs are unique once the input is validated).
+// ================================================================================================
+__global__ void __launch_bounds__(256)
+k_elem_offsets(const uint32_t* __restrict__ keys, int64_t n, int64_t N, int64_t* __restrict__ offsets,
+               const unsigned long long* __restrict__ err) {
+  if (err && *err != ERR_NONE) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = keys[i];
+    const int64_t pk = i == 0 ? -1 : (int64_t)keys[i - 1];
+    for (int64_t x = pk + 1; x <= k; ++x) offsets[x] = i;
+    if (i == n - 1)
+      for (int64_t x = k + 1; x <= N; ++x) offsets[x] = n;
+  }
+}
+
+// ================================================================================================
+// k_scan_i32: exclusive scan int32 -> int64 (out has n+1 entries), single pass, decoupled
+// look-back; warp-striped tiles, warp shuffles inside.
+// ================================================================================================
+template <int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS)
+k_scan_i32(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out, uint64_t* status,
+           uint32_t* ticket, uint32_t epoch) {
+  constexpr int WARPS = THREADS / 32;
+  constexpr int TILE = THREADS * ITEMS;
+  __shared__ uint64_t s_w[WARPS];
+  __shared__ uint64_t s_texcl;
+  __shared__ uint32_t s_tile;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t chunk = (int64_t)tile * TILE + (int64_t)warp * 32 * ITEMS;
+  int64_t v[ITEMS];
+  uint64_t wtot = 0;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t idx = chunk + i * 32 + lane;
+    int64_t x = idx < n ? (int64_t)in[idx] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    v[i] = x + (int64_t)wtot;               // inclusive within the warp chunk
+    wtot += (uint64_t)__shfl_sync(FULL, x, 31);
+  }
+  if (lane == 0) s_w[warp] = wtot;
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t tot = 0;
+    for (int w = 0; w < WARPS; ++w) {
+      const uint64_t c = s_w[w];
+      s_w[w] = tot;
+      tot += c;
+    }
+    uint64_t excl = 0;
+    if (tile == 0) {
+      st_relaxed_u64(status, st_pack(epoch, ST_INC, tot));
+    } else {
+      st_relaxed_u64(status + tile, st_pack(epoch, ST_AGG, tot));
+      int64_t t = (int64_t)tile - 1;
+      while (true) {
+        const uint64_t w = lookback_wait(status + t, epoch);
+        excl += w & ST_VMASK;
+        if (((w >> 54) & 3u) == ST_INC) break;
+        --t;
+      }
+      st_relaxed_u64(status + tile, st_pack(epoch, ST_INC, excl + tot));
+    }
+    s_texcl = excl;
+  }
+  __syncthreads();
+  const int64_t add = (int64_t)(s_texcl + s_w[warp]);
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t idx = chunk + i * 32 + lane;
+    if (idx < n) out[idx + 1] = v[i] + add;
+  }
+  if (tile == 0 && tid == 0) out[0] = 0;
+}
+
+// ================================================================================================
+// Stage kernels for the per-row entry points (emission materialised in slot order).
+// ================================================================================================
+template <int T, typename KeyT>
+__global__ void __launch_bounds__(256)
+k_emit_node(const int32_t* __restrict__ conn, int64_t P, int b, KeyT* __restrict__ keys,
+            const unsigned long long* __restrict__ err) {
+  if (*err != ERR_NONE) return;
+  constexpr int K = Elem<T>::K, S = 2 * Elem<T>::E;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / S;
+    const int r = (int)(i - e * S);
+    int la, lb;
+    slot_locals<T>(r, la, lb);
+    const uint32_t a = (uint32_t)__ldg(conn + e * K + la);
+    const uint32_t v = (uint32_t)__ldg(conn + e * K + lb);
+    keys[i] = (KeyT)(((KeyT)a << b) | (KeyT)v);
+  }
+}
+
+template <int T>
+__global__ void __launch_bounds__(256)
+k_emit_elem(const int32_t* __restrict__ conn, int64_t P, uint32_t* __restrict__ keys,
+            uint32_t* __restrict__ vals, const unsigned long long* __restrict__ err) {
+  if (*err != ERR_NONE) return;
+  constexpr int K = Elem<T>::K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = (uint32_t)__ldg(conn + i);
+    vals[i] = (uint32_t)(i / K);
+  }
+}
+
+// Multi-GPU finish: rebase received pairs onto the local node range.
+__global__ void __launch_bounds__(256)
+k_rebase_node(const uint64_t* __restrict__ in, int64_t n, int b, int64_t lo, uint64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = in[i];
+    const uint64_t a = (k >> b) - (uint64_t)lo;
+    out[i] = (a << b) | (k & ((1ull << b) - 1));
+  }
+}
+
+__global__ void __launch_bounds__(256)
+k_split_elem(const uint64_t* __restrict__ in, int64_t n, int64_t lo, uint32_t* __restrict__ keys,
+             uint32_t* __restrict__ vals) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = in[i];
+    keys[i] = (uint32_t)((int64_t)(k >> 32) - lo);
+    vals[i] = (uint32_t)(k & 0xffffffffull);
+  }
+}
+
+}  // namespace mn

@@ -1,0 +1,1007 @@
+// meshnbr.cu — host orchestration + C ABI of libmeshnbr.so (declared in include/meshnbr.h).
+//
+// Pipeline of mn_find_neighbors_both (DESIGN.md §"Path"):
+//   memset(status, tickets, err)               once per call
+//   k_hist_validate                            a1/a2 validation + digit histograms (reads conn)
+//   k_bucket_bases                             bucket bases of every LSD pass
+//   k_onesweep x 2*nd (node, pass 0 from conn) a1 + a3n
+//   k_unique_node                              a4 + a5 (node)
+//   k_onesweep x nd   (elem, pass 0 from conn) a2 + a3e
+//   k_elem_offsets                             a4 + a5 (elem; indices are the sorted payloads)
+//   D2H(err, nnz) + one stream sync            a6
+//   exact-size node indices + D2D copy         a6
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace mn {
+
+// ================================================================================================
+// instrumentation
+// ================================================================================================
+static std::atomic<int64_t> g_launches{0};
+static bool g_prof = false;
+struct ProfRec { const char* name; cudaEvent_t a, b; double bytes; };
+static std::vector<ProfRec> g_recs;
+static std::vector<cudaEvent_t> g_evpool;
+struct ProfEntry { std::string name; int64_t launches; double ms; double bytes; };
+static std::vector<ProfEntry> g_table;
+
+static cudaEvent_t ev_get() {
+  if (!g_evpool.empty()) { cudaEvent_t e = g_evpool.back(); g_evpool.pop_back(); return e; }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+template <class F>
+static cudaError_t launch(const char* name, double alg_bytes, cudaStream_t s, F&& f) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (g_prof) { a = ev_get(); b = ev_get(); cudaEventRecord(a, s); }
+  f();
+  cudaError_t e = cudaGetLastError();
+  if (g_prof) { cudaEventRecord(b, s); g_recs.push_back({name, a, b, alg_bytes}); }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return e;
+}
+
+// ================================================================================================
+// memory
+// ================================================================================================
+static void* default_alloc(void*, size_t bytes, mn_stream s) {
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, (cudaStream_t)s) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  return p;
+}
+static void default_release(void*, void* p, mn_stream s) {
+  if (p) cudaFreeAsync(p, (cudaStream_t)s);
+}
+static const mn_allocator kDefaultAlloc = {default_alloc, default_release, nullptr};
+
+struct Mem {
+  mn_allocator a;
+  cudaStream_t s;
+  Mem(const mn_allocator* al, cudaStream_t st) : a(al && al->alloc ? *al : kDefaultAlloc), s(st) {}
+  void* get(size_t bytes) { return a.alloc(a.ctx, bytes ? bytes : 16, (mn_stream)s); }
+  void put(void* p) { if (p) a.release(a.ctx, p, (mn_stream)s); }
+};
+
+// Carves one workspace allocation into 256-byte aligned pieces (dry run with base == nullptr).
+struct Arena {
+  char* base = nullptr;
+  size_t off = 0;
+  template <typename X>
+  X* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    // with base == nullptr the returned "pointer" is the byte offset (relocated by the caller)
+    X* p = reinterpret_cast<X*>(reinterpret_cast<uintptr_t>(base) + off);
+    off += count * sizeof(X);
+    return p;
+  }
+};
+
+// Per-thread pinned staging word pair for the one blocking read of (err, nnz).
+static uint64_t* pinned_pair() {
+  static thread_local uint64_t* p = nullptr;
+  if (!p) {
+    if (cudaMallocHost(&p, 4 * sizeof(uint64_t)) != cudaSuccess) { cudaGetLastError(); p = nullptr; }
+  }
+  return p;
+}
+
+static mn_status decode_err(uint64_t w, mn_error_detail* err) {
+  if (w == ERR_NONE) return MN_OK;
+  if (err) { err->elem = (int64_t)(w >> 5); err->pos = (int32_t)(w & 15); }
+  return ((w >> 4) & 1) ? MN_ERR_DEGENERATE : MN_ERR_INDEX_OUT_OF_RANGE;
+}
+
+#define MN_CUDA(x)                                        \
+  do {                                                    \
+    cudaError_t _e = (x);                                 \
+    if (_e != cudaSuccess) { st = MN_ERR_CUDA; goto done; } \
+  } while (0)
+
+// ================================================================================================
+// plans
+// ================================================================================================
+constexpr int kThreads = 256;
+constexpr int kItems = 16;
+constexpr int kTile = kThreads * kItems;           // keys per onesweep / unique tile
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kThreads * kScanItems;
+
+struct Plan {
+  int T, K, E, C;
+  int64_t M, N;
+  int b;
+  bool key64;
+  int bins;
+  DigitPlan dp;
+  int64_t Pn, Pe;
+};
+
+static DigitPlan make_digits(int bits, int* bins) {
+  DigitPlan dp{};
+  const int nd9 = (bits + 8) / 9, nd8 = (bits + 7) / 8;
+  dp.nd = nd9;
+  *bins = (nd8 == nd9) ? 256 : 512;
+  int s = 0;
+  for (int j = 0; j < dp.nd; ++j) {
+    dp.width[j] = bits / dp.nd + (j < bits % dp.nd ? 1 : 0);
+    dp.shift[j] = s;
+    s += dp.width[j];
+  }
+  return dp;
+}
+
+static Plan make_plan(int T, int64_t M, int64_t N) {
+  Plan P{};
+  P.T = T; P.K = arity_of(T); P.E = edges_of(T); P.C = 2 * P.E / P.K;
+  P.M = M; P.N = N;
+  P.b = node_bits(N);
+  P.key64 = 2 * P.b > 32;
+  P.dp = make_digits(P.b, &P.bins);
+  P.Pn = 2 * (int64_t)P.E * M;
+  P.Pe = (int64_t)P.K * M;
+  return P;
+}
+
+static int64_t tiles_of(int64_t n, int tile) { return (n + tile - 1) / tile; }
+static int hist_grid(int64_t M) {
+  int64_t g = (M + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  return g < 1 ? 1 : (int)g;
+}
+static int stream_grid(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  return g < 1 ? 1 : (int)g;
+}
+
+// ================================================================================================
+// one onesweep pass
+// ================================================================================================
+template <typename KeyT, int SRC, int T, bool PAYLOAD, bool OWNER, int BINS>
+static cudaError_t run_pass(PassArgs pa, cudaStream_t s, const char* name, double bytes) {
+  using Sm = OnesweepSmem<kThreads, kItems, BINS>;
+  const int64_t tiles = tiles_of(pa.n, kTile);
+  if (tiles == 0) return cudaSuccess;
+  const size_t smem = ((sizeof(Sm) + 15) & ~size_t(15)) + (size_t)kTile * sizeof(KeyT) +
+                      ((PAYLOAD || SRC == 2) ? (size_t)kTile * 4 : 0);
+  auto kern = k_onesweep<KeyT, SRC, T, PAYLOAD, OWNER, BINS, kThreads, kItems>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  return launch(name, bytes, s, [&] { kern<<<(unsigned)tiles, kThreads, smem, s>>>(pa); });
+}
+
+static PassDigit mask_digit(int shift, int width) {
+  PassDigit pd{};
+  pd.shift = shift;
+  pd.mask = (1u << width) - 1u;
+  pd.div = 1;
+  return pd;
+}
+
+// ================================================================================================
+// the whole path
+// ================================================================================================
+template <int T, typename KeyT, int BINS>
+static mn_status pipeline(const Plan& P, const int32_t* conn, Mem& mem, bool want_node,
+                          bool want_elem, mn_csr* node_out, mn_csr* elem_out,
+                          mn_error_detail* err) {
+  cudaStream_t s = mem.s;
+  mn_status st = MN_OK;
+  const int nd = P.dp.nd;
+  const int nnode_pass = want_node ? 2 * nd : 0;
+  const int nelem_pass = want_elem ? nd : 0;
+  const int npass = nnode_pass + nelem_pass;
+  const int64_t node_tiles = tiles_of(P.Pn, kTile), elem_tiles = tiles_of(P.Pe, kTile);
+  const int64_t st_tiles = std::max(want_node ? node_tiles : 0, want_elem ? elem_tiles : 0);
+  const int64_t uq_tiles = want_node ? node_tiles : 0;
+  const size_t w = sizeof(KeyT);
+  // elem arrays alias the dead node key buffer when it is large enough
+  const bool alias = want_node && want_elem && (size_t)P.Pn * w >= (size_t)16 * P.Pe;
+
+  int64_t *node_off = nullptr, *elem_off = nullptr;
+  int32_t *elem_idx = nullptr, *node_idx = nullptr;
+  void* ws = nullptr;
+  uint64_t* host = pinned_pair();
+  if (!host) return MN_ERR_CUDA;
+
+  // ---- outputs known in size up front ----
+  if (want_node) {
+    node_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
+    if (!node_off) { st = MN_ERR_OOM; goto done; }
+  }
+  if (want_elem) {
+    elem_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
+    elem_idx = P.Pe ? (int32_t*)mem.get((size_t)P.Pe * 4) : nullptr;
+    if (!elem_off || (P.Pe && !elem_idx)) { st = MN_ERR_OOM; goto done; }
+  }
+
+  if (P.M == 0) {  // no pairs: every slice empty
+    if (node_off) MN_CUDA(cudaMemsetAsync(node_off, 0, (size_t)(P.N + 1) * 8, s));
+    if (elem_off) MN_CUDA(cudaMemsetAsync(elem_off, 0, (size_t)(P.N + 1) * 8, s));
+    MN_CUDA(cudaStreamSynchronize(s));
+    goto finish;
+  }
+
+  {
+    // ---- workspace layout ----
+    Arena ar;
+    size_t head = 0;
+    auto layout = [&](Arena& a, unsigned long long*& errw, unsigned long long*& nnz, uint32_t*& tickets,
+                      unsigned long long*& hist, uint64_t*& bases, uint64_t*& status, uint64_t*& ustatus,
+                      KeyT*& kA, KeyT*& kB, uint32_t*& ekA, uint32_t*& ekB, uint32_t*& epA, uint32_t*& epB) {
+      errw = a.take<unsigned long long>(2);   // [0] validation word, [1] node nnz (one D2H read)
+      nnz = errw + 1;
+      tickets = a.take<uint32_t>(32);
+      hist = a.take<unsigned long long>((size_t)nd * BINS);
+      bases = a.take<uint64_t>((size_t)(npass ? npass : 1) * BINS);
+      status = a.take<uint64_t>((size_t)st_tiles * BINS);
+      ustatus = a.take<uint64_t>((size_t)(uq_tiles ? uq_tiles : 1));
+      head = a.off;   // everything above is zero-initialised once per call
+      kA = kB = nullptr;
+      ekA = ekB = epA = epB = nullptr;
+      if (want_node) { kA = a.take<KeyT>(P.Pn); kB = a.take<KeyT>(P.Pn); }
+      if (want_elem) {
+        if (alias && kB) {
+          uint32_t* r = reinterpret_cast<uint32_t*>(kB);
+          ekA = r; ekB = r + P.Pe; epA = r + 2 * P.Pe; epB = r + 3 * P.Pe;
+        } else {
+          ekA = a.take<uint32_t>(P.Pe); ekB = a.take<uint32_t>(P.Pe);
+          epA = a.take<uint32_t>(P.Pe); epB = a.take<uint32_t>(P.Pe);
+        }
+      }
+    };
+    unsigned long long *errw, *nnz, *hist;
+    uint32_t* tickets;
+    uint64_t *bases, *status, *ustatus;
+    KeyT *kA, *kB;
+    uint32_t *ekA, *ekB, *epA, *epB;
+    layout(ar, errw, nnz, tickets, hist, bases, status, ustatus, kA, kB, ekA, ekB, epA, epB);
+    ws = mem.get(ar.off);
+    if (!ws) { st = MN_ERR_OOM; goto done; }
+    ar = Arena{};
+    ar.base = (char*)ws;
+    layout(ar, errw, nnz, tickets, hist, bases, status, ustatus, kA, kB, ekA, ekB, epA, epB);
+
+    MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
+    MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
+
+    // ---- a1/a2: validate + histograms ----
+    MN_CUDA(launch("hist_validate", 4.0 * P.K * P.M, s, [&] {
+      k_hist_validate<T, BINS><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, 0, P.dp, 0, 1, hist, errw);
+    }));
+    BasesDesc bd{};
+    bd.npass = npass;
+    for (int q = 0; q < nnode_pass; ++q) { bd.hidx[q] = q % nd; bd.mult[q] = P.C; }
+    for (int q = 0; q < nelem_pass; ++q) { bd.hidx[nnode_pass + q] = q; bd.mult[nnode_pass + q] = 1; }
+    MN_CUDA(launch("bucket_bases", 0.0, s, [&] {
+      k_bucket_bases<BINS><<<npass, BINS, 0, s>>>(hist, bd, bases, errw);
+    }));
+
+    uint32_t epoch = 0;
+    // ---- a1 + a3n: node pairs, LSD over v digits then a digits ----
+    if (want_node) {
+      KeyT* in = nullptr;
+      KeyT* bufs[2] = {kA, kB};
+      for (int q = 0; q < nnode_pass; ++q) {
+        const int j = q % nd;
+        const int shift = (q < nd ? 0 : P.b) + P.dp.shift[j];
+        PassArgs pa{};
+        pa.keys_in = in;
+        pa.keys_out = bufs[q & 1];
+        pa.conn = conn;
+        pa.node_bits = P.b;
+        pa.n = P.Pn;
+        pa.pd = mask_digit(shift, P.dp.width[j]);
+        pa.bases = bases + (size_t)q * BINS;
+        pa.status = status;
+        pa.ticket = tickets + q;
+        pa.epoch = ++epoch;
+        pa.err = errw;
+        if (q == 0) {
+          MN_CUDA((run_pass<KeyT, 1, T, false, false, BINS>(pa, s, "onesweep_node_first",
+                                                             4.0 * P.K * P.M + (double)w * P.Pn)));
+        } else {
+          MN_CUDA((run_pass<KeyT, 0, 0, false, false, BINS>(pa, s, "onesweep_node", 2.0 * w * P.Pn)));
+        }
+        in = bufs[q & 1];
+      }
+      // ---- a4 + a5: dedupe, compaction, run lengths, offsets ----
+      UniqueArgs ua{};
+      ua.keys = in;
+      ua.n = P.Pn;
+      ua.b = P.b;
+      ua.N = P.N;
+      ua.offsets = node_off;
+      ua.indices = reinterpret_cast<uint32_t*>(in == kA ? kB : kA);
+      ua.status = ustatus;
+      ua.ticket = tickets + 30;
+      ua.epoch = 1;
+      ua.nnz = nnz;
+      ua.err = errw;
+      MN_CUDA(launch("unique_node", (double)w * P.Pn + 8.0 * (P.N + 1), s, [&] {
+        k_unique_node<KeyT, kThreads, kItems><<<(unsigned)node_tiles, kThreads, 0, s>>>(ua);
+      }));
+      node_idx = reinterpret_cast<int32_t*>(ua.indices);
+    }
+
+    // ---- a2 + a3e: element pairs, stable LSD over the node digits ----
+    if (want_elem) {
+      uint32_t* kb[2] = {ekA, ekB};
+      uint32_t* vb[2] = {epA, epB};
+      const uint32_t* kin = nullptr;
+      const uint32_t* vin = nullptr;
+      for (int q = 0; q < nelem_pass; ++q) {
+        PassArgs pa{};
+        pa.keys_in = kin;
+        pa.vals_in = vin;
+        pa.keys_out = kb[q & 1];
+        pa.vals_out = (q == nelem_pass - 1) ? reinterpret_cast<uint32_t*>(elem_idx) : vb[q & 1];
+        pa.conn = conn;
+        pa.n = P.Pe;
+        pa.pd = mask_digit(P.dp.shift[q], P.dp.width[q]);
+        pa.bases = bases + (size_t)(nnode_pass + q) * BINS;
+        pa.status = status;
+        pa.ticket = tickets + 16 + q;
+        pa.epoch = ++epoch;
+        pa.err = errw;
+        if (q == 0) {
+          MN_CUDA((run_pass<uint32_t, 2, T, false, false, BINS>(pa, s, "onesweep_elem_first",
+                                                                 4.0 * P.Pe + 8.0 * P.Pe)));
+        } else {
+          MN_CUDA((run_pass<uint32_t, 0, 0, true, false, BINS>(pa, s, "onesweep_elem", 16.0 * P.Pe)));
+        }
+        kin = kb[q & 1];
+        vin = vb[q & 1];
+      }
+      MN_CUDA(launch("elem_offsets", 4.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
+        k_elem_offsets<<<stream_grid(P.Pe), 256, 0, s>>>(kin, P.Pe, P.N, elem_off, errw);
+      }));
+    }
+
+    // ---- a6: one blocking read of (err, nnz) ----
+    MN_CUDA(cudaMemcpyAsync(host, errw, 16, cudaMemcpyDeviceToHost, s));
+    MN_CUDA(cudaStreamSynchronize(s));
+    st = decode_err(host[0], err);
+    if (st != MN_OK) goto done;
+    if (want_node) {
+      const int64_t U = (int64_t)host[1];
+      int32_t* out = U ? (int32_t*)mem.get((size_t)U * 4) : nullptr;
+      if (U && !out) { st = MN_ERR_OOM; goto done; }
+      if (U) MN_CUDA(cudaMemcpyAsync(out, node_idx, (size_t)U * 4, cudaMemcpyDeviceToDevice, s));
+      node_out->nnz = U;
+      node_out->indices = out;
+      node_idx = out;
+    }
+  }
+
+finish:
+  if (want_node) {
+    node_out->num_nodes = P.N;
+    node_out->offsets = node_off;
+    if (P.M == 0) { node_out->nnz = 0; node_out->indices = nullptr; }
+    node_out->owner = mem.a;
+  }
+  if (want_elem) {
+    elem_out->num_nodes = P.N;
+    elem_out->offsets = elem_off;
+    elem_out->nnz = P.Pe;
+    elem_out->indices = elem_idx;
+    elem_out->owner = mem.a;
+  }
+  mem.put(ws);
+  return MN_OK;
+
+done:
+  if (ws) { cudaStreamSynchronize(s); mem.put(ws); }
+  mem.put(node_off);
+  mem.put(elem_off);
+  mem.put(elem_idx);
+  if (want_node && node_out) { std::memset(node_out, 0, sizeof(*node_out)); }
+  if (want_elem && elem_out) { std::memset(elem_out, 0, sizeof(*elem_out)); }
+  return st;
+}
+
+template <int T>
+static mn_status dispatch_key(const Plan& P, const int32_t* conn, Mem& mem, bool wn, bool we,
+                              mn_csr* no, mn_csr* eo, mn_error_detail* err) {
+  if (P.key64) {
+    if (P.bins == 256) return pipeline<T, uint64_t, 256>(P, conn, mem, wn, we, no, eo, err);
+    return pipeline<T, uint64_t, 512>(P, conn, mem, wn, we, no, eo, err);
+  }
+  if (P.bins == 256) return pipeline<T, uint32_t, 256>(P, conn, mem, wn, we, no, eo, err);
+  return pipeline<T, uint32_t, 512>(P, conn, mem, wn, we, no, eo, err);
+}
+
+static mn_status check_args(int t, const void* conn, int64_t M, int64_t N) {
+  if (t < 0 || t > 3 || M < 0 || N < 0 || N > INT32_MAX) return MN_ERR_INVALID_ARG;
+  if (M > 0 && !conn) return MN_ERR_INVALID_ARG;
+  if (M > INT32_MAX) return MN_ERR_CAPACITY;   // element ids are int32 in the output
+  return MN_OK;
+}
+
+static mn_status find(int t, const int32_t* conn, int64_t M, int64_t N, const mn_allocator* a,
+                      mn_stream stream, bool wn, bool we, mn_csr* no, mn_csr* eo, mn_error_detail* err) {
+  if (err) { err->elem = -1; err->pos = -1; }
+  mn_status st = check_args(t, conn, M, N);
+  if (st != MN_OK) return st;
+  if ((wn && !no) || (we && !eo)) return MN_ERR_INVALID_ARG;
+  Mem mem(a, (cudaStream_t)stream);
+  const Plan P = make_plan(t, M, N);
+  switch (t) {
+    case MN_TRI3: return dispatch_key<MN_TRI3>(P, conn, mem, wn, we, no, eo, err);
+    case MN_QUAD4: return dispatch_key<MN_QUAD4>(P, conn, mem, wn, we, no, eo, err);
+    case MN_TET4: return dispatch_key<MN_TET4>(P, conn, mem, wn, we, no, eo, err);
+    default: return dispatch_key<MN_HEX8>(P, conn, mem, wn, we, no, eo, err);
+  }
+}
+
+// ================================================================================================
+// generic LSD sorts (stage entry points and the multi-GPU finish)
+// ================================================================================================
+template <typename KeyT, bool PAYLOAD>
+static mn_status lsd_sort(KeyT* keys, uint32_t* vals, int64_t n, int bits, Mem& mem) {
+  cudaStream_t s = mem.s;
+  mn_status st = MN_OK;
+  if (n <= 1 || bits <= 0) return MN_OK;
+  const int p = (bits + 7) / 8;
+  const int64_t tiles = tiles_of(n, kTile);
+  Arena ar;
+  unsigned long long* errw = ar.take<unsigned long long>(1);
+  uint32_t* tickets = ar.take<uint32_t>(32);
+  unsigned long long* hist = ar.take<unsigned long long>((size_t)p * 256);
+  uint64_t* bases = ar.take<uint64_t>((size_t)p * 256);
+  uint64_t* status = ar.take<uint64_t>((size_t)tiles * 256);
+  const size_t head = ar.off;
+  KeyT* alt = ar.take<KeyT>(n);
+  uint32_t* valt = PAYLOAD ? ar.take<uint32_t>(n) : nullptr;
+  void* ws = mem.get(ar.off);
+  if (!ws) return MN_ERR_OOM;
+  {
+    char* b = (char*)ws;
+    auto fix = [&](auto* q) { return (decltype(q))(b + (size_t)q); };
+    errw = fix(errw); tickets = fix(tickets); hist = fix(hist); bases = fix(bases);
+    status = fix(status); alt = fix(alt);
+    if (PAYLOAD) valt = fix(valt);
+    MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
+    MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
+    MN_CUDA(launch("hist_keys", (double)sizeof(KeyT) * n, s, [&] {
+      k_hist_keys<KeyT><<<stream_grid(n), 256, 0, s>>>(keys, n, p, hist);
+    }));
+    BasesDesc bd{};
+    bd.npass = p;
+    for (int q = 0; q < p; ++q) { bd.hidx[q] = q; bd.mult[q] = 1; }
+    MN_CUDA(launch("bucket_bases", 0.0, s, [&] { k_bucket_bases<256><<<p, 256, 0, s>>>(hist, bd, bases, errw); }));
+    KeyT* kb[2] = {keys, alt};
+    uint32_t* vb[2] = {vals, valt};
+    for (int q = 0; q < p; ++q) {
+      PassArgs pa{};
+      pa.keys_in = kb[q & 1];
+      pa.keys_out = kb[(q + 1) & 1];
+      pa.vals_in = vb[q & 1];
+      pa.vals_out = vb[(q + 1) & 1];
+      pa.n = n;
+      const int width = std::min(8, bits - 8 * q);
+      pa.pd = mask_digit(8 * q, width);
+      pa.bases = bases + (size_t)q * 256;
+      pa.status = status;
+      pa.ticket = tickets + q;
+      pa.epoch = (uint32_t)(q + 1);
+      pa.err = errw;
+      MN_CUDA((run_pass<KeyT, 0, 0, PAYLOAD, false, 256>(pa, s, "onesweep_generic",
+                                                          (double)(PAYLOAD ? 2 * (sizeof(KeyT) + 4) : 2 * sizeof(KeyT)) * n)));
+    }
+    if (p & 1) {
+      MN_CUDA(cudaMemcpyAsync(keys, alt, (size_t)n * sizeof(KeyT), cudaMemcpyDeviceToDevice, s));
+      if (PAYLOAD) MN_CUDA(cudaMemcpyAsync(vals, valt, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+done:
+  mem.put(ws);
+  return st;
+}
+
+// Unique + offsets on arbitrary sorted node keys (stage entry point, multi-GPU finish).
+template <typename KeyT>
+static mn_status unique_csr(const KeyT* keys, int64_t n, int b, int64_t N, int64_t* offsets,
+                            int32_t* indices, int64_t* h_nnz, Mem& mem) {
+  cudaStream_t s = mem.s;
+  mn_status st = MN_OK;
+  uint64_t* host = pinned_pair();
+  if (!host) return MN_ERR_CUDA;
+  if (n == 0) {
+    if (cudaMemsetAsync(offsets, 0, (size_t)(N + 1) * 8, s) != cudaSuccess) return MN_ERR_CUDA;
+    *h_nnz = 0;
+    return MN_OK;
+  }
+  const int64_t tiles = tiles_of(n, kTile);
+  Arena ar;
+  unsigned long long* errw = ar.take<unsigned long long>(2);
+  uint32_t* ticket = ar.take<uint32_t>(1);
+  uint64_t* status = ar.take<uint64_t>((size_t)tiles);
+  void* ws = mem.get(ar.off);
+  if (!ws) return MN_ERR_OOM;
+  {
+    char* bb = (char*)ws;
+    errw = (unsigned long long*)(bb + (size_t)errw);
+    unsigned long long* nnz = errw + 1;
+    ticket = (uint32_t*)(bb + (size_t)ticket);
+    status = (uint64_t*)(bb + (size_t)status);
+    MN_CUDA(cudaMemsetAsync(ws, 0, ar.off, s));
+    MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
+    UniqueArgs ua{};
+    ua.keys = keys; ua.n = n; ua.b = b; ua.N = N; ua.offsets = offsets;
+    ua.indices = reinterpret_cast<uint32_t*>(indices);
+    ua.status = status; ua.ticket = ticket; ua.epoch = 1; ua.nnz = nnz; ua.err = errw;
+    MN_CUDA(launch("unique_node", (double)sizeof(KeyT) * n + 8.0 * (N + 1), s, [&] {
+      k_unique_node<KeyT, kThreads, kItems><<<(unsigned)tiles, kThreads, 0, s>>>(ua);
+    }));
+    MN_CUDA(cudaMemcpyAsync(host, errw, 16, cudaMemcpyDeviceToHost, s));
+    MN_CUDA(cudaStreamSynchronize(s));
+    *h_nnz = (int64_t)host[1];
+  }
+done:
+  mem.put(ws);
+  return st;
+}
+
+// Validation + emission kernels for the stage entry points.
+template <int T>
+static mn_status emit_stage(const int32_t* conn, int64_t M, int64_t N, void* keys, uint32_t* ekeys,
+                            uint32_t* evals, bool node, Mem& mem, mn_error_detail* err) {
+  cudaStream_t s = mem.s;
+  mn_status st = MN_OK;
+  uint64_t* host = pinned_pair();
+  if (!host) return MN_ERR_CUDA;
+  const Plan P = make_plan(T, M, N);
+  Arena ar;
+  unsigned long long* errw = ar.take<unsigned long long>(1);
+  unsigned long long* hist = ar.take<unsigned long long>(4 * 512);
+  void* ws = mem.get(ar.off);
+  if (!ws) return MN_ERR_OOM;
+  errw = (unsigned long long*)((char*)ws + (size_t)errw);
+  hist = (unsigned long long*)((char*)ws + (size_t)hist);
+  MN_CUDA(cudaMemsetAsync(ws, 0, ar.off, s));
+  MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
+  if (M > 0) {
+    MN_CUDA(launch("hist_validate", 4.0 * P.K * M, s, [&] {
+      k_hist_validate<T, 512><<<hist_grid(M), 256, 0, s>>>(conn, M, N, 0, P.dp, 0, 1, hist, errw);
+    }));
+    if (node) {
+      if (P.key64) {
+        MN_CUDA(launch("emit_node", 4.0 * P.K * M + 8.0 * P.Pn, s, [&] {
+          k_emit_node<T, uint64_t><<<stream_grid(P.Pn), 256, 0, s>>>(conn, P.Pn, P.b, (uint64_t*)keys, errw);
+        }));
+      } else {
+        MN_CUDA(launch("emit_node", 4.0 * P.K * M + 4.0 * P.Pn, s, [&] {
+          k_emit_node<T, uint32_t><<<stream_grid(P.Pn), 256, 0, s>>>(conn, P.Pn, P.b, (uint32_t*)keys, errw);
+        }));
+      }
+    } else {
+      MN_CUDA(launch("emit_elem", 12.0 * P.Pe, s, [&] {
+        k_emit_elem<T><<<stream_grid(P.Pe), 256, 0, s>>>(conn, P.Pe, ekeys, evals, errw);
+      }));
+    }
+  }
+  MN_CUDA(cudaMemcpyAsync(host, errw, 8, cudaMemcpyDeviceToHost, s));
+  MN_CUDA(cudaStreamSynchronize(s));
+  st = decode_err(host[0], err);
+done:
+  mem.put(ws);
+  return st;
+}
+
+// ================================================================================================
+// multi-GPU bucketing: stable owner partition fused with pair creation (one onesweep pass each)
+// ================================================================================================
+template <int T, int BINS>
+static mn_status dist_bucket_impl(const int32_t* conn, int64_t M, int64_t base, int64_t N, int world,
+                                  uint64_t* nkeys, uint64_t* epairs, int64_t* hn, int64_t* he,
+                                  Mem& mem, mn_error_detail* err) {
+  cudaStream_t s = mem.s;
+  mn_status st = MN_OK;
+  uint64_t* host = pinned_pair();
+  if (!host) return MN_ERR_CUDA;
+  const Plan P = make_plan(T, M, N);
+  const uint64_t chunk = (uint64_t)((N + world - 1) / world > 0 ? (N + world - 1) / world : 1);
+  const int64_t tiles = std::max(tiles_of(P.Pn, kTile), tiles_of(P.Pe, kTile));
+  std::vector<unsigned long long> hh(BINS);
+  Arena ar;
+  unsigned long long* errw = ar.take<unsigned long long>(1);
+  uint32_t* tickets = ar.take<uint32_t>(8);
+  unsigned long long* hist = ar.take<unsigned long long>(BINS);
+  uint64_t* bases = ar.take<uint64_t>(2 * BINS);
+  uint64_t* status = ar.take<uint64_t>((size_t)(tiles ? tiles : 1) * BINS);
+  void* ws = mem.get(ar.off);
+  if (!ws) return MN_ERR_OOM;
+  {
+    char* bb = (char*)ws;
+    errw = (unsigned long long*)(bb + (size_t)errw);
+    tickets = (uint32_t*)(bb + (size_t)tickets);
+    hist = (unsigned long long*)(bb + (size_t)hist);
+    bases = (uint64_t*)(bb + (size_t)bases);
+    status = (uint64_t*)(bb + (size_t)status);
+    MN_CUDA(cudaMemsetAsync(ws, 0, ar.off, s));
+    MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
+    if (M > 0) {
+      MN_CUDA(launch("hist_validate", 4.0 * P.K * M, s, [&] {
+        k_hist_validate<T, BINS><<<hist_grid(M), 256, 0, s>>>(conn, M, N, base, P.dp, 1, chunk, hist, errw);
+      }));
+      BasesDesc bd{};
+      bd.npass = 2;
+      bd.hidx[0] = 0; bd.mult[0] = P.C;
+      bd.hidx[1] = 0; bd.mult[1] = 1;
+      MN_CUDA(launch("bucket_bases", 0.0, s, [&] { k_bucket_bases<BINS><<<2, BINS, 0, s>>>(hist, bd, bases, errw); }));
+      PassArgs pa{};
+      pa.keys_out = nkeys; pa.conn = conn; pa.node_bits = P.b; pa.n = P.Pn;
+      pa.pd.shift = P.b; pa.pd.div = chunk; pa.pd.mask = 0;
+      pa.bases = bases; pa.status = status; pa.ticket = tickets; pa.epoch = 1; pa.err = errw;
+      MN_CUDA((run_pass<uint64_t, 1, T, false, true, BINS>(pa, s, "bucket_node", 4.0 * P.K * M + 8.0 * P.Pn)));
+      PassArgs pe{};
+      pe.keys_out = epairs; pe.conn = conn; pe.elem_base = base; pe.n = P.Pe;
+      pe.pd.shift = 32; pe.pd.div = chunk; pe.pd.mask = 0;
+      pe.bases = bases + BINS; pe.status = status; pe.ticket = tickets + 1; pe.epoch = 2; pe.err = errw;
+      MN_CUDA((run_pass<uint64_t, 3, T, false, true, BINS>(pe, s, "bucket_elem", 4.0 * P.Pe + 8.0 * P.Pe)));
+    }
+    MN_CUDA(cudaMemcpyAsync(hh.data(), hist, BINS * 8, cudaMemcpyDeviceToHost, s));
+    MN_CUDA(cudaMemcpyAsync(host, errw, 8, cudaMemcpyDeviceToHost, s));
+    MN_CUDA(cudaStreamSynchronize(s));
+    st = decode_err(host[0], err);
+    if (st == MN_OK) {
+      for (int g = 0; g < world; ++g) {
+        hn[g] = (int64_t)hh[g] * P.C;
+        he[g] = (int64_t)hh[g];
+      }
+    }
+  }
+done:
+  mem.put(ws);
+  return st;
+}
+
+}  // namespace mn
+
+// ==================================================================================================
+// C ABI
+// ==================================================================================================
+using namespace mn;
+
+extern "C" {
+
+int mn_abi_version(void) { return MN_ABI_VERSION; }
+
+const char* mn_status_string(mn_status s) {
+  switch (s) {
+    case MN_OK: return "ok";
+    case MN_ERR_INVALID_ARG: return "invalid argument";
+    case MN_ERR_INDEX_OUT_OF_RANGE: return "node index out of range";
+    case MN_ERR_DEGENERATE: return "degenerate element (repeated node)";
+    case MN_ERR_CAPACITY: return "capacity exceeded";
+    case MN_ERR_OOM: return "out of device memory";
+    case MN_ERR_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+int mn_node_key_bits(int64_t num_nodes) { return node_bits(num_nodes); }
+int mn_node_key_bytes(int64_t num_nodes) { return 2 * node_bits(num_nodes) > 32 ? 8 : 4; }
+
+mn_status mn_find_node_neighbors(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N,
+                                 const mn_allocator* a, mn_stream s, mn_csr* out, mn_error_detail* err) {
+  return find(t, d_conn, M, N, a, s, true, false, out, nullptr, err);
+}
+
+mn_status mn_find_elem_neighbors(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N,
+                                 const mn_allocator* a, mn_stream s, mn_csr* out, mn_error_detail* err) {
+  return find(t, d_conn, M, N, a, s, false, true, nullptr, out, err);
+}
+
+mn_status mn_find_neighbors_both(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N,
+                                 const mn_allocator* a, mn_stream s, mn_csr* no, mn_csr* eo,
+                                 mn_error_detail* err) {
+  return find(t, d_conn, M, N, a, s, true, true, no, eo, err);
+}
+
+mn_status mn_find_neighbors_both_host(mn_elem_type t, const int32_t* h_conn, int64_t M, int64_t N,
+                                      const mn_allocator* dev_alloc, const mn_allocator* host_alloc,
+                                      mn_stream stream, mn_csr* no, mn_csr* eo, mn_error_detail* err) {
+  mn_status st = check_args(t, h_conn, M, N);
+  if (st != MN_OK) return st;
+  if (!host_alloc || !host_alloc->alloc || !no || !eo) return MN_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  Mem mem(dev_alloc, s);
+  const size_t cbytes = (size_t)M * arity_of(t) * 4;
+  int32_t* d_conn = (int32_t*)mem.get(cbytes);
+  if (!d_conn) return MN_ERR_OOM;
+  mn_csr dn{}, de{};
+  if (cbytes && cudaMemcpyAsync(d_conn, h_conn, cbytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+    mem.put(d_conn);
+    return MN_ERR_CUDA;
+  }
+  st = find(t, d_conn, M, N, &mem.a, stream, true, true, &dn, &de, err);
+  if (st != MN_OK) { mem.put(d_conn); return st; }
+  mn_csr* outs[2] = {no, eo};
+  mn_csr* devs[2] = {&dn, &de};
+  for (int i = 0; i < 2 && st == MN_OK; ++i) {
+    mn_csr* o = outs[i];
+    mn_csr* d = devs[i];
+    std::memset(o, 0, sizeof(*o));
+    o->num_nodes = d->num_nodes;
+    o->nnz = d->nnz;
+    o->owner = *host_alloc;
+    o->offsets = (int64_t*)host_alloc->alloc(host_alloc->ctx, (size_t)(N + 1) * 8, stream);
+    o->indices = d->nnz ? (int32_t*)host_alloc->alloc(host_alloc->ctx, (size_t)d->nnz * 4, stream) : nullptr;
+    if (!o->offsets || (d->nnz && !o->indices)) { st = MN_ERR_OOM; break; }
+    if (cudaMemcpyAsync(o->offsets, d->offsets, (size_t)(N + 1) * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        (d->nnz && cudaMemcpyAsync(o->indices, d->indices, (size_t)d->nnz * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess))
+      st = MN_ERR_CUDA;
+  }
+  if (st == MN_OK && cudaStreamSynchronize(s) != cudaSuccess) st = MN_ERR_CUDA;
+  mn_csr_release(&dn, stream);
+  mn_csr_release(&de, stream);
+  mem.put(d_conn);
+  if (st != MN_OK) { mn_csr_release(no, stream); mn_csr_release(eo, stream); }
+  return st;
+}
+
+void mn_csr_release(mn_csr* c, mn_stream s) {
+  if (!c) return;
+  if (c->owner.release) {
+    if (c->offsets) c->owner.release(c->owner.ctx, c->offsets, s);
+    if (c->indices) c->owner.release(c->owner.ctx, c->indices, s);
+  }
+  std::memset(c, 0, sizeof(*c));
+}
+
+mn_status mn_workspace_bytes(mn_elem_type t, int64_t M, int64_t N, int modes, size_t* bytes) {
+  mn_status st = check_args(t, (const void*)1, M, N);
+  if (st != MN_OK || !bytes || modes < 1 || modes > 3) return MN_ERR_INVALID_ARG;
+  const Plan P = make_plan(t, M, N);
+  const bool wn = modes & 1, we = modes & 2;
+  const size_t w = P.key64 ? 8 : 4;
+  const int64_t st_tiles = std::max(wn ? tiles_of(P.Pn, kTile) : 0, we ? tiles_of(P.Pe, kTile) : 0);
+  size_t b = 4096 + (size_t)st_tiles * P.bins * 8 + (wn ? (size_t)tiles_of(P.Pn, kTile) * 8 : 0);
+  if (wn) b += 2 * (size_t)P.Pn * w;
+  const bool alias = wn && we && (size_t)P.Pn * w >= (size_t)16 * P.Pe;
+  if (we && !alias) b += 16 * (size_t)P.Pe;
+  *bytes = b;
+  return MN_OK;
+}
+
+mn_status mn_emit_node_pairs(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N, void* d_keys,
+                             mn_stream stream, mn_error_detail* err) {
+  if (err) { err->elem = -1; err->pos = -1; }
+  mn_status st = check_args(t, d_conn, M, N);
+  if (st != MN_OK) return st;
+  if (M > 0 && !d_keys) return MN_ERR_INVALID_ARG;
+  Mem mem(nullptr, (cudaStream_t)stream);
+  switch (t) {
+    case MN_TRI3: return emit_stage<MN_TRI3>(d_conn, M, N, d_keys, nullptr, nullptr, true, mem, err);
+    case MN_QUAD4: return emit_stage<MN_QUAD4>(d_conn, M, N, d_keys, nullptr, nullptr, true, mem, err);
+    case MN_TET4: return emit_stage<MN_TET4>(d_conn, M, N, d_keys, nullptr, nullptr, true, mem, err);
+    default: return emit_stage<MN_HEX8>(d_conn, M, N, d_keys, nullptr, nullptr, true, mem, err);
+  }
+}
+
+mn_status mn_emit_elem_pairs(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N, uint32_t* d_keys,
+                             uint32_t* d_vals, mn_stream stream, mn_error_detail* err) {
+  if (err) { err->elem = -1; err->pos = -1; }
+  mn_status st = check_args(t, d_conn, M, N);
+  if (st != MN_OK) return st;
+  if (M > 0 && (!d_keys || !d_vals)) return MN_ERR_INVALID_ARG;
+  Mem mem(nullptr, (cudaStream_t)stream);
+  switch (t) {
+    case MN_TRI3: return emit_stage<MN_TRI3>(d_conn, M, N, nullptr, d_keys, d_vals, false, mem, err);
+    case MN_QUAD4: return emit_stage<MN_QUAD4>(d_conn, M, N, nullptr, d_keys, d_vals, false, mem, err);
+    case MN_TET4: return emit_stage<MN_TET4>(d_conn, M, N, nullptr, d_keys, d_vals, false, mem, err);
+    default: return emit_stage<MN_HEX8>(d_conn, M, N, nullptr, d_keys, d_vals, false, mem, err);
+  }
+}
+
+mn_status mn_radix_sort_keys(void* d_keys, int key_bytes, int64_t n, int key_bits, const mn_allocator* a,
+                             mn_stream stream) {
+  if (n < 0 || (n > 0 && !d_keys) || (key_bytes != 4 && key_bytes != 8) || key_bits < 0 ||
+      key_bits > 8 * key_bytes)
+    return MN_ERR_INVALID_ARG;
+  Mem mem(a, (cudaStream_t)stream);
+  if (key_bytes == 8) return lsd_sort<uint64_t, false>((uint64_t*)d_keys, nullptr, n, key_bits, mem);
+  return lsd_sort<uint32_t, false>((uint32_t*)d_keys, nullptr, n, key_bits, mem);
+}
+
+mn_status mn_radix_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_vals, int64_t n, int key_bits,
+                                  const mn_allocator* a, mn_stream stream) {
+  if (n < 0 || (n > 0 && (!d_keys || !d_vals)) || key_bits < 0 || key_bits > 32) return MN_ERR_INVALID_ARG;
+  Mem mem(a, (cudaStream_t)stream);
+  return lsd_sort<uint32_t, true>(d_keys, d_vals, n, key_bits, mem);
+}
+
+mn_status mn_unique_node_csr(const void* d_sorted_keys, int key_bytes, int64_t n, int64_t N,
+                             int64_t* d_offsets, int32_t* d_indices, int64_t* h_nnz,
+                             const mn_allocator* a, mn_stream stream) {
+  if (n < 0 || N < 0 || N > INT32_MAX || !d_offsets || !h_nnz || (n > 0 && (!d_sorted_keys || !d_indices)) ||
+      (key_bytes != 4 && key_bytes != 8))
+    return MN_ERR_INVALID_ARG;
+  Mem mem(a, (cudaStream_t)stream);
+  const int b = node_bits(N);
+  if (key_bytes == 8) return unique_csr<uint64_t>((const uint64_t*)d_sorted_keys, n, b, N, d_offsets, d_indices, h_nnz, mem);
+  return unique_csr<uint32_t>((const uint32_t*)d_sorted_keys, n, b, N, d_offsets, d_indices, h_nnz, mem);
+}
+
+mn_status mn_elem_offsets(const uint32_t* d_sorted_keys, int64_t n, int64_t N, int64_t* d_offsets,
+                          mn_stream stream) {
+  if (n < 0 || N < 0 || !d_offsets || (n > 0 && !d_sorted_keys)) return MN_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) return cudaMemsetAsync(d_offsets, 0, (size_t)(N + 1) * 8, s) == cudaSuccess ? MN_OK : MN_ERR_CUDA;
+  cudaError_t e = launch("elem_offsets", 4.0 * n + 8.0 * (N + 1), s, [&] {
+    k_elem_offsets<<<stream_grid(n), 256, 0, s>>>(d_sorted_keys, n, N, d_offsets, nullptr);
+  });
+  return e == cudaSuccess ? MN_OK : MN_ERR_CUDA;
+}
+
+mn_status mn_exclusive_scan_i32(const int32_t* d_counts, int64_t n, int64_t* d_out, const mn_allocator* a,
+                                mn_stream stream) {
+  if (n < 0 || !d_out || (n > 0 && !d_counts)) return MN_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) return cudaMemsetAsync(d_out, 0, 8, s) == cudaSuccess ? MN_OK : MN_ERR_CUDA;
+  Mem mem(a, s);
+  const int64_t tiles = tiles_of(n, kScanTile);
+  const size_t bytes = 256 + (size_t)tiles * 8;
+  char* ws = (char*)mem.get(bytes);
+  if (!ws) return MN_ERR_OOM;
+  mn_status st = MN_OK;
+  uint32_t* ticket = (uint32_t*)ws;
+  uint64_t* status = (uint64_t*)(ws + 256);
+  if (cudaMemsetAsync(ws, 0, bytes, s) != cudaSuccess) st = MN_ERR_CUDA;
+  if (st == MN_OK &&
+      launch("scan_i32", 4.0 * n + 8.0 * (n + 1), s, [&] {
+        k_scan_i32<kThreads, kScanItems><<<(unsigned)tiles, kThreads, 0, s>>>(d_counts, n, d_out, status, ticket, 1);
+      }) != cudaSuccess)
+    st = MN_ERR_CUDA;
+  mem.put(ws);
+  return st;
+}
+
+mn_status mn_dist_bucket(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t base, int64_t N, int world,
+                         uint64_t* d_node_keys, uint64_t* d_elem_pairs, int64_t* h_nc, int64_t* h_ec,
+                         const mn_allocator* a, mn_stream stream, mn_error_detail* err) {
+  if (err) { err->elem = -1; err->pos = -1; }
+  mn_status st = check_args(t, d_conn, M, N);
+  if (st != MN_OK) return st;
+  if (world < 1 || world > 512 || !h_nc || !h_ec || base < 0 || (M > 0 && (!d_node_keys || !d_elem_pairs)))
+    return MN_ERR_INVALID_ARG;
+  if (base + M > INT32_MAX) return MN_ERR_CAPACITY;
+  Mem mem(a, (cudaStream_t)stream);
+#define MN_DB(TT)                                                                                        \
+  return world <= 256 ? dist_bucket_impl<TT, 256>(d_conn, M, base, N, world, d_node_keys, d_elem_pairs, h_nc, h_ec, mem, err) \
+                      : dist_bucket_impl<TT, 512>(d_conn, M, base, N, world, d_node_keys, d_elem_pairs, h_nc, h_ec, mem, err)
+  switch (t) {
+    case MN_TRI3: MN_DB(MN_TRI3);
+    case MN_QUAD4: MN_DB(MN_QUAD4);
+    case MN_TET4: MN_DB(MN_TET4);
+    default: MN_DB(MN_HEX8);
+  }
+#undef MN_DB
+}
+
+mn_status mn_dist_finish(const uint64_t* d_node_keys, int64_t nn, const uint64_t* d_elem_pairs, int64_t ne,
+                         int64_t N, int64_t lo, int64_t hi, const mn_allocator* a, mn_stream stream,
+                         mn_csr* node_slice, mn_csr* elem_slice) {
+  if (nn < 0 || ne < 0 || N < 0 || N > INT32_MAX || lo < 0 || hi < lo || hi > N || !node_slice || !elem_slice ||
+      (nn > 0 && !d_node_keys) || (ne > 0 && !d_elem_pairs))
+    return MN_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  Mem mem(a, s);
+  mn_status st = MN_OK;
+  const int b = node_bits(N);
+  const int64_t nloc = hi - lo;
+  const int bl = node_bits(nloc);
+  std::memset(node_slice, 0, sizeof(*node_slice));
+  std::memset(elem_slice, 0, sizeof(*elem_slice));
+  uint64_t* tmp = nullptr;
+  uint32_t *ek = nullptr, *ev = nullptr;
+  int32_t* idx = nullptr;
+  int64_t* noff = (int64_t*)mem.get((size_t)(nloc + 1) * 8);
+  int64_t* eoff = (int64_t*)mem.get((size_t)(nloc + 1) * 8);
+  int64_t U = 0;
+  if (!noff || !eoff) { st = MN_ERR_OOM; goto fail; }
+  // node slice: rebase, sort on (bl + b) bits, dedupe/offsets against the local node count
+  if (nn > 0) {
+    tmp = (uint64_t*)mem.get((size_t)nn * 8);
+    idx = (int32_t*)mem.get((size_t)nn * 4);
+    if (!tmp || !idx) { st = MN_ERR_OOM; goto fail; }
+    if (launch("rebase_node", 16.0 * nn, s, [&] { k_rebase_node<<<stream_grid(nn), 256, 0, s>>>(d_node_keys, nn, b, lo, tmp); }) != cudaSuccess) { st = MN_ERR_CUDA; goto fail; }
+    st = lsd_sort<uint64_t, false>(tmp, nullptr, nn, bl + b, mem);
+    if (st != MN_OK) goto fail;
+  }
+  st = unique_csr<uint64_t>(tmp, nn, b, nloc, noff, idx, &U, mem);
+  if (st != MN_OK) goto fail;
+  mem.put(tmp);
+  tmp = nullptr;
+  node_slice->num_nodes = nloc;
+  node_slice->nnz = U;
+  node_slice->offsets = noff;
+  node_slice->owner = mem.a;
+  if (U) {
+    node_slice->indices = (int32_t*)mem.get((size_t)U * 4);
+    if (!node_slice->indices) { st = MN_ERR_OOM; goto fail; }
+    if (cudaMemcpyAsync(node_slice->indices, idx, (size_t)U * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess) { st = MN_ERR_CUDA; goto fail; }
+  }
+  mem.put(idx);
+  idx = nullptr;
+  noff = nullptr;
+  // element slice: split, stable sort on the local node bits, offsets
+  if (ne > 0) {
+    ek = (uint32_t*)mem.get((size_t)ne * 4);
+    ev = (uint32_t*)mem.get((size_t)ne * 4);
+    if (!ek || !ev) { st = MN_ERR_OOM; goto fail; }
+    if (launch("split_elem", 16.0 * ne, s, [&] { k_split_elem<<<stream_grid(ne), 256, 0, s>>>(d_elem_pairs, ne, lo, ek, ev); }) != cudaSuccess) { st = MN_ERR_CUDA; goto fail; }
+    st = lsd_sort<uint32_t, true>(ek, ev, ne, bl, mem);
+    if (st != MN_OK) goto fail;
+  }
+  if (mn_elem_offsets(ek, ne, nloc, eoff, stream) != MN_OK) { st = MN_ERR_CUDA; goto fail; }
+  mem.put(ek);
+  elem_slice->num_nodes = nloc;
+  elem_slice->nnz = ne;
+  elem_slice->offsets = eoff;
+  elem_slice->indices = (int32_t*)ev;
+  elem_slice->owner = mem.a;
+  if (cudaStreamSynchronize(s) != cudaSuccess) { mn_csr_release(node_slice, stream); mn_csr_release(elem_slice, stream); return MN_ERR_CUDA; }
+  return MN_OK;
+fail:
+  cudaStreamSynchronize(s);
+  mem.put(tmp); mem.put(idx); mem.put(ek); mem.put(ev); mem.put(noff); mem.put(eoff);
+  if (node_slice->indices) mem.put(node_slice->indices);
+  std::memset(node_slice, 0, sizeof(*node_slice));
+  std::memset(elem_slice, 0, sizeof(*elem_slice));
+  return st;
+}
+
+int64_t mn_launch_count(void) { return g_launches.load(); }
+
+void mn_profile_enable(int on) { g_prof = on != 0; }
+
+void mn_profile_reset(void) {
+  for (auto& r : g_recs) { g_evpool.push_back(r.a); g_evpool.push_back(r.b); }
+  g_recs.clear();
+  g_table.clear();
+}
+
+int mn_profile_collect(void) {
+  g_table.clear();
+  for (auto& r : g_recs) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    ProfEntry* e = nullptr;
+    for (auto& x : g_table)
+      if (x.name == r.name) { e = &x; break; }
+    if (!e) { g_table.push_back({r.name, 0, 0.0, 0.0}); e = &g_table.back(); }
+    e->launches += 1;
+    e->ms += ms;
+    e->bytes += r.bytes;
+  }
+  return (int)g_table.size();
+}
+
+mn_status mn_profile_entry(int i, const char** name, int64_t* launches, double* total_ms, double* alg_bytes) {
+  if (i < 0 || i >= (int)g_table.size()) return MN_ERR_INVALID_ARG;
+  if (name) *name = g_table[i].name.c_str();
+  if (launches) *launches = g_table[i].launches;
+  if (total_ms) *total_ms = g_table[i].ms;
+  if (alg_bytes) *alg_bytes = g_table[i].bytes;
+  return MN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,339 @@
+"""GPU parity: every §8(a) row of the CUDA path (through the C ABI) against the oracle, element by
+element, on seeded synthetic meshes; full-size configs on sampled vertices + properties that hold
+at any size.  Bar: bit-exact (integer work)."""
+import numpy as np
+import pytest
+import torch
+
+import meshgen
+import oracle
+from oracle import stages
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1604_04689_b200 import build
+    build.build()
+
+
+def mn():
+    import paper_1604_04689_b200 as m
+    return m
+
+
+def _perm_hex(n, node_seed, elem_seed):
+    conn, N = meshgen.hex_grid(n)
+    return meshgen.relabel(conn, N, node_seed, elem_seed), N
+
+
+# Small/medium meshes: several onesweep tiles (4096 keys) and ragged tails, every element type.
+SMALL = [
+    ("tri_grid_32", meshgen.TRI3, lambda: meshgen.tri_grid(32, 32)),          # config 1
+    ("tri_grid_77x41", meshgen.TRI3, lambda: meshgen.tri_grid(41, 77)),
+    ("quad_grid_60x33", meshgen.QUAD4, lambda: meshgen.quad_grid(33, 60)),
+    ("kuhn_11", meshgen.TET4, lambda: meshgen.kuhn_tets(11)),
+    ("hex_13_perm", meshgen.HEX8, lambda: _perm_hex(13, 1604, 4689)),
+    ("sphere_100x51", meshgen.TRI3, lambda: meshgen.uv_sphere(100, 51)),
+    ("rand_tri", meshgen.TRI3, lambda: meshgen.random_mesh(meshgen.TRI3, 3000, 700, seed=5)),
+    ("rand_tet_sparse", meshgen.TET4, lambda: meshgen.random_mesh(meshgen.TET4, 900, 5000, seed=6)),
+    ("rand_hex", meshgen.HEX8, lambda: meshgen.random_mesh(meshgen.HEX8, 700, 3000, seed=8)),
+    ("rand_quad_big_ids", meshgen.QUAD4, lambda: meshgen.random_mesh(meshgen.QUAD4, 800, 70000, seed=9)),
+    ("fan5", meshgen.TRI3, lambda: meshgen.nonmanifold_fan(5)),
+    ("single_tet", meshgen.TET4, lambda: (torch.tensor([[3, 1, 0, 2]], dtype=torch.int32), 4)),
+    ("hex_big_ids", meshgen.HEX8, lambda: _perm_hex(9, 77, None)),
+]
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _unpack(keys, N):
+    b = mn().node_key_bits(N)
+    k = _np(keys)
+    k = k.view(np.uint32).astype(np.uint64) if k.dtype == np.int32 else k.view(np.uint64)
+    return (k >> np.uint64(b)).astype(np.int64), (k & np.uint64((1 << b) - 1)).astype(np.int64)
+
+
+def _assert_csr(got, exp, what):
+    go, gi = (_np(x) for x in got)
+    eo, ei = exp
+    assert go.dtype == np.int64 and gi.dtype == np.int32, what
+    assert np.array_equal(go, eo), f"{what}: offsets differ at {np.nonzero(go != eo)[0][:5]}"
+    assert np.array_equal(gi, ei), f"{what}: indices differ at {np.nonzero(gi != ei)[0][:5]}"
+
+
+# ------------------------------------------------------------------------------------------------
+# row a1 / a2: pair creation
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name,et,make", SMALL)
+def test_row_a1_emit_node_pairs(name, et, make):
+    conn, N = make()
+    keys = mn().emit_node_pairs(conn.cuda(), et, N)
+    a, v = _unpack(keys, N)
+    ea, ev = stages.expand_node_pairs(et, conn)
+    assert np.array_equal(a, ea) and np.array_equal(v, ev), name
+
+
+@pytest.mark.parametrize("name,et,make", SMALL)
+def test_row_a2_emit_elem_pairs(name, et, make):
+    conn, N = make()
+    k, v = mn().emit_elem_pairs(conn.cuda(), et, N)
+    ek, ev = stages.expand_elem_pairs(et, conn)
+    assert np.array_equal(_np(k), ek) and np.array_equal(_np(v), ev), name
+
+
+# ------------------------------------------------------------------------------------------------
+# row a3: onesweep LSD radix sort
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name,et,make", SMALL)
+def test_row_a3n_sort_node_pairs(name, et, make):
+    conn, N = make()
+    keys = mn().emit_node_pairs(conn.cuda(), et, N)
+    mn().radix_sort_keys(keys, 2 * mn().node_key_bits(N))
+    a, v = _unpack(keys, N)
+    sa, sv = stages.sort_pairs(*stages.expand_node_pairs(et, conn))
+    assert np.array_equal(a, sa) and np.array_equal(v, sv), name
+
+
+@pytest.mark.parametrize("name,et,make", SMALL)
+def test_row_a3e_stable_sort_elem_pairs(name, et, make):
+    conn, N = make()
+    k, v = mn().emit_elem_pairs(conn.cuda(), et, N)
+    mn().radix_sort_pairs_u32(k, v, mn().node_key_bits(N))
+    sk, sv = stages.stable_sort_by_key(*stages.expand_elem_pairs(et, conn))
+    assert np.array_equal(_np(k), sk) and np.array_equal(_np(v), sv), name
+
+
+@pytest.mark.parametrize("n,bits,dist", [
+    (0, 20, "uniform"), (1, 20, "uniform"), (4095, 20, "uniform"), (4096, 20, "uniform"),
+    (4097, 20, "uniform"), (100003, 64, "uniform"), (300001, 37, "uniform"), (200000, 33, "equal"),
+    (250000, 50, "one_bucket"), (123457, 9, "skewed"), (77777, 1, "uniform"),
+])
+def test_row_a3_sort_adversarial_u64(n, bits, dist):
+    rng = np.random.default_rng(n + bits)
+    hi = (1 << bits) if bits < 64 else None
+    if dist == "uniform":
+        x = rng.integers(0, hi, size=n, dtype=np.uint64) if hi else rng.integers(0, 2 ** 63, size=n).astype(np.uint64) * np.uint64(2) + rng.integers(0, 2, size=n).astype(np.uint64)
+    elif dist == "equal":
+        x = np.full(n, (1 << (bits - 1)) + 12345, dtype=np.uint64)
+    elif dist == "one_bucket":        # every key shares all digits but the lowest
+        x = (np.uint64(0xABCDE) << np.uint64(20)) + rng.integers(0, 256, size=n, dtype=np.uint64)
+    else:                             # 90 % of keys in one bucket
+        x = np.where(rng.random(n) < 0.9, 7, rng.integers(0, 512, size=n)).astype(np.uint64)
+    t = torch.from_numpy(x.view(np.int64)).cuda()
+    mn().radix_sort_keys(t, bits)
+    assert np.array_equal(_np(t).view(np.uint64), np.sort(x))
+
+
+@pytest.mark.parametrize("n,bits", [(0, 8), (5, 3), (8191, 17), (50000, 32), (70001, 24)])
+def test_row_a3_sort_u32_and_pairs(n, bits):
+    rng = np.random.default_rng(n)
+    x = rng.integers(0, 1 << bits, size=n, dtype=np.uint64).astype(np.uint32)
+    t = torch.from_numpy(x.view(np.int32)).cuda()
+    mn().radix_sort_keys(t, bits)
+    assert np.array_equal(_np(t).view(np.uint32), np.sort(x))
+    # stable pairs: values record the original positions
+    k = torch.from_numpy(x.view(np.int32)).cuda()
+    v = torch.arange(n, dtype=torch.int32).cuda()
+    mn().radix_sort_pairs_u32(k, v, bits)
+    order = np.argsort(x, kind="stable")
+    assert np.array_equal(_np(k).view(np.uint32), x[order]) and np.array_equal(_np(v), order)
+
+
+# ------------------------------------------------------------------------------------------------
+# rows a4 + a5: dedupe, run lengths, offsets
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name,et,make", SMALL)
+def test_row_a4_a5_unique_node(name, et, make):
+    conn, N = make()
+    keys = mn().emit_node_pairs(conn.cuda(), et, N)
+    mn().radix_sort_keys(keys, 2 * mn().node_key_bits(N))
+    got = mn().unique_node_csr(keys, N)
+    k, v = stages.unique_pairs(*stages.sort_pairs(*stages.expand_node_pairs(et, conn)))
+    uk, cnt = stages.reduce_by_key_ones(k)
+    exp = (stages.exclusive_scan(stages.dense_counts(uk, cnt, N)), v.astype(np.int32))
+    _assert_csr(got, exp, name)
+
+
+@pytest.mark.parametrize("name,et,make", SMALL)
+def test_row_a4_a5_elem_offsets(name, et, make):
+    conn, N = make()
+    k, v = mn().emit_elem_pairs(conn.cuda(), et, N)
+    mn().radix_sort_pairs_u32(k, v, mn().node_key_bits(N))
+    off = mn().elem_offsets(k, N)
+    sk, _ = stages.stable_sort_by_key(*stages.expand_elem_pairs(et, conn))
+    uk, cnt = stages.reduce_by_key_ones(sk)
+    assert np.array_equal(_np(off), stages.exclusive_scan(stages.dense_counts(uk, cnt, N)))
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 4096, 4097, 100000, 1000003])
+def test_row_a5_exclusive_scan(n):
+    rng = np.random.default_rng(n)
+    c = rng.integers(0, 2000, size=n).astype(np.int32)
+    got = mn().exclusive_scan(torch.from_numpy(c).cuda())
+    assert np.array_equal(_np(got), stages.exclusive_scan(c))
+
+
+# ------------------------------------------------------------------------------------------------
+# whole path vs the std::set oracle
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name,et,make", SMALL)
+def test_whole_path_both(name, et, make):
+    conn, N = make()
+    (no, ni), (eo, ei) = mn().find_neighbors(conn.cuda(), et, N)
+    _assert_csr((no, ni), oracle.node_csr(et, conn, N), name + " node")
+    _assert_csr((eo, ei), oracle.elem_csr(et, conn, N), name + " elem")
+
+
+@pytest.mark.parametrize("name,et,make", SMALL[:6])
+def test_whole_path_single_modes(name, et, make):
+    conn, N = make()
+    _assert_csr(mn().find_node_neighbors(conn.cuda(), et, N), oracle.node_csr(et, conn, N), name)
+    _assert_csr(mn().find_elem_neighbors(conn.cuda(), et, N), oracle.elem_csr(et, conn, N), name)
+
+
+def test_whole_path_host_buffers():
+    conn, N = meshgen.kuhn_tets(9)
+    (no, ni), (eo, ei) = mn().find_neighbors_host(conn.pin_memory(), "tet4", N)
+    assert not no.is_cuda and no.is_pinned()
+    _assert_csr((no, ni), oracle.node_csr(meshgen.TET4, conn, N), "host node")
+    _assert_csr((eo, ei), oracle.elem_csr(meshgen.TET4, conn, N), "host elem")
+
+
+def test_config2_sphere_full():
+    et, conn, N = meshgen.make_config(2)
+    (no, ni), (eo, ei) = mn().find_neighbors(conn.cuda(), et, N)
+    _assert_csr((no, ni), oracle.node_csr(et, conn, N), "cfg2 node")
+    _assert_csr((eo, ei), oracle.elem_csr(et, conn, N), "cfg2 elem")
+    E = int(_np(no)[-1]) // 2
+    assert N - E + conn.shape[0] == 2          # Euler on the closed sphere
+
+
+# ------------------------------------------------------------------------------------------------
+# edge cases and errors
+# ------------------------------------------------------------------------------------------------
+def test_empty_mesh_and_isolated_nodes():
+    for et in (0, 1, 2, 3):
+        k = meshgen.ARITY[et]
+        for N in (0, 1, 17):
+            c = torch.zeros((0, k), dtype=torch.int32).cuda()
+            (no, ni), (eo, ei) = mn().find_neighbors(c, et, N)
+            assert _np(no).tolist() == [0] * (N + 1) and ni.numel() == 0
+            assert _np(eo).tolist() == [0] * (N + 1) and ei.numel() == 0
+    conn = torch.tensor([[2, 5, 7]], dtype=torch.int32)
+    (no, ni), _ = mn().find_neighbors(conn.cuda(), 0, 100000)
+    _assert_csr((no, ni), oracle.node_csr(0, conn, 100000), "isolated")
+
+
+@pytest.mark.parametrize("conn,N,et", [
+    ([[0, 1, 3]], 3, 0), ([[0, 1, 1]], 3, 0), ([[0, 1, 2], [0, 1, 2], [4, 4, -1]], 5, 0),
+    ([[0, 1, 2, 3]] * 5000 + [[1, 2, 3, 1]] + [[0, 9, 2, 3]], 9, 2),
+    ([[0, 1, 2, 3, 4, 5, 6, 7]] * 3 + [[0, 1, 2, 3, 4, 5, 6, 6]], 8, 3),
+    ([[0, 1, 2]], 0, 0),
+])
+def test_invalid_input_reported_like_the_oracle(conn, N, et):
+    c = torch.tensor(conn, dtype=torch.int32)
+    code, elem, pos = oracle.validate(et, c, N)
+    assert code != 0
+    for fn in (mn().find_neighbors, mn().find_node_neighbors, mn().find_elem_neighbors):
+        with pytest.raises(mn().MeshError) as ei:
+            fn(c.cuda(), et, N)
+        assert (ei.value.code, ei.value.elem, ei.value.pos) == (code, elem, pos)
+
+
+def test_deterministic_repeats():
+    et = meshgen.HEX8
+    conn, N = _perm_hex(20, 3, 4)
+    conn = conn.cuda()
+    ref = mn().find_neighbors(conn, et, N)
+    for _ in range(5):
+        got = mn().find_neighbors(conn, et, N)
+        for a, b in zip(ref, got):
+            assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+# ------------------------------------------------------------------------------------------------
+# full-size configs 3-5: sampled vertices vs the oracle's one-vertex form + size-free properties
+# ------------------------------------------------------------------------------------------------
+def _sampled_check(et, conn_cpu, N, got_node, got_elem, nsample=48, seed=0):
+    rng = np.random.default_rng(seed)
+    sample = np.unique(np.concatenate([rng.integers(0, N, nsample), [0, N - 1, N // 2]]))
+    no, ni = (_np(x) for x in got_node)
+    eo, ei = (_np(x) for x in got_elem)
+    exp_n = stages.node_neighbors_sample(et, conn_cpu, N, sample)
+    exp_e = stages.elem_neighbors_sample(et, conn_cpu, N, sample)
+    for v in sample.tolist():
+        assert np.array_equal(ni[no[v]:no[v + 1]], exp_n[v]), f"node {v}"
+        assert np.array_equal(ei[eo[v]:eo[v + 1]], exp_e[v]), f"elem {v}"
+
+
+def _kuhn_counts(n, device):
+    """Closed-form valence and element count of every node of the Kuhn n^3 mesh (torch)."""
+    w = n + 1
+    idx = torch.arange(w ** 3, device=device, dtype=torch.int64)
+    i, j, k = idx % w, (idx // w) % w, idx // (w * w)
+    val = torch.zeros_like(idx)
+    for d in [(1, 0, 0), (0, 1, 0), (0, 0, 1), (1, 1, 0), (1, 0, 1), (0, 1, 1), (1, 1, 1)]:
+        for s in (1, -1):
+            x, y, z = i + s * d[0], j + s * d[1], k + s * d[2]
+            val += ((x >= 0) & (x <= n) & (y >= 0) & (y <= n) & (z >= 0) & (z <= n)).long()
+    ne = torch.zeros_like(idx)
+    # tets of cell (corner offset o) containing that corner: 6 for o in {000, 111}, else 2
+    for o in [(a, b, c) for a in (0, 1) for b in (0, 1) for c in (0, 1)]:
+        ok = (i - o[0] >= 0) & (i - o[0] < n) & (j - o[1] >= 0) & (j - o[1] < n) & (k - o[2] >= 0) & (k - o[2] < n)
+        ne += ok.long() * (6 if sum(o) in (0, 3) else 2)
+    return val, ne
+
+
+def _symmetric(off, idx):
+    rows = torch.repeat_interleave(torch.arange(off.numel() - 1, device=off.device), off[1:] - off[:-1])
+    cols = idx.long()
+    n = off.numel() - 1
+    a = torch.sort(rows * n + cols).values
+    b = torch.sort(cols * n + rows).values
+    return bool(torch.equal(a, b)) and bool((rows != cols).all())
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_full_size_config(cfg):
+    et, conn, N = meshgen.make_config(cfg, device="cuda")
+    (no, ni), (eo, ei) = mn().find_neighbors(conn, et, N)
+    M = conn.shape[0]
+    assert int(eo[-1]) == meshgen.ARITY[et] * M
+    if cfg == 3:
+        n = 128
+        val, ne = _kuhn_counts(n, "cuda")
+        assert torch.equal(no[1:] - no[:-1], val) and torch.equal(eo[1:] - eo[:-1], ne)
+        assert int(no[-1]) == 2 * (3 * n * (n + 1) ** 2 + 3 * n * n * (n + 1) + n ** 3)
+    else:
+        n = 256
+        assert int(no[-1]) == 2 * 3 * n * (n + 1) ** 2      # handshake, hex |E| = 3n(n+1)^2
+        pi = torch.from_numpy(meshgen.seeded_permutation(N, 1604)).cuda()
+        w = n + 1
+        idx = torch.arange(N, device="cuda")
+        i, j, k = idx % w, (idx // w) % w, idx // (w * w)
+        inner = lambda x: (x > 0).long() + (x < n).long()
+        val = inner(i) + inner(j) + inner(k)           # valence of the unpermuted node
+        cnt = torch.zeros_like(no[1:])
+        cnt[pi] = val
+        assert torch.equal(no[1:] - no[:-1], cnt)       # permutation equivariance of valences
+    assert _symmetric(no, ni)
+    _sampled_check(et, conn.cpu(), N, (no, ni), (eo, ei))
+
+
+@pytest.mark.slow
+def test_full_size_config5_single_gpu():
+    et, conn, N = meshgen.make_config(5, device="cuda")
+    (no, ni), (eo, ei) = mn().find_neighbors(conn, et, N)
+    n = 320
+    assert int(no[-1]) == 2 * (3 * n * (n + 1) ** 2 + 3 * n * n * (n + 1) + n ** 3)
+    assert int(eo[-1]) == 4 * conn.shape[0]
+    val, ne = _kuhn_counts(n, "cuda")
+    assert torch.equal(no[1:] - no[:-1], val) and torch.equal(eo[1:] - eo[:-1], ne)
+    del val, ne
+    _sampled_check(et, conn.cpu(), N, (no, ni), (eo, ei), nsample=24)
