@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark: mesh elements/s to CSR node + element one-ring neighbours (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step is one pass of the whole hot path (both modes) over the
+workload: at N=1 the whole of config 5 (Kuhn tets 320^3, 196,608,000 tets) on one GPU; at N>1
+config 5 sharded by elements over N ranks with the NCCL all-to-all (strong scaling: the same
+mesh).  Inputs are resident in HBM before the timed region and larger than L2 (3.15 GB of
+connectivity, 18.9 GB of node keys), so no explicit L2 flush is needed.  One JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "mesh elements/sec to CSR node+elem neighbors; achieved HBM GB/s vs peak, 1/2/4/8 GPU"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------------
+# helpers
+# ------------------------------------------------------------------------------------------------
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                rows.append((float(f[1]), float(f[2]), float(f[3]), f[4:8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        pmax = max(r[2] for r in rows)
+        load = [r for r in rows if r[2] >= 0.5 * pmax] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in load for i, v in enumerate(r[3]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(load), "power_w_max": pmax}
+
+
+def workload(cfg, rank, world, device):
+    """(etype, conn shard on device, global element base, total elements, num_nodes, desc)."""
+    import meshgen
+    info = meshgen.CONFIGS[cfg]
+    if cfg in (3, 5) and world > 1:
+        n = 128 if cfg == 3 else 320
+        ncell = n ** 3
+        c0, c1 = rank * ncell // world, (rank + 1) * ncell // world
+        conn, N = meshgen.kuhn_tets(n, device=device, cell_begin=c0, cell_end=c1)
+        return info["etype"], conn, 6 * c0, 6 * ncell, N, info
+    et, conn, N = meshgen.make_config(cfg, device=device)
+    M = conn.shape[0]
+    if world > 1:
+        s0, s1 = rank * M // world, (rank + 1) * M // world
+        return et, conn[s0:s1].contiguous(), s0, M, N, info
+    return et, conn, 0, M, N, info
+
+
+def oracle_sample(conn_full_dev, et, target_s, k_layers_hint=None):
+    """Time the oracle (std::set serial baseline, 1 thread) on a bounded prefix of the workload:
+    the first Ms elements with N trimmed to the largest node id + 1.  Returns (elements/s,
+    description, seconds)."""
+    import numpy as np
+
+    import oracle
+    M = conn_full_dev.shape[0]
+    ms = min(M, 200_000)
+    while True:
+        sub = conn_full_dev[:ms].cpu().numpy()
+        n_s = int(sub.max()) + 1 if sub.size else 0
+        t0 = time.perf_counter()
+        oracle.node_csr(et, sub, n_s)
+        oracle.elem_csr(et, sub, n_s)
+        dt = time.perf_counter() - t0
+        if dt >= 0.6 * target_s or ms >= M:
+            return ms / dt, (f"first {ms:,} of {M:,} elements (node ids < {n_s:,}), node + element CSR, "
+                             f"1 thread, {dt:.1f} s"), dt, ms
+        ms = min(M, int(ms * max(1.5, min(8.0, target_s / max(dt, 1e-3)))))
+
+
+# ------------------------------------------------------------------------------------------------
+# reference arm: the oracle, timed as it stands on the host cores
+# ------------------------------------------------------------------------------------------------
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import torch
+
+    import meshgen
+    import oracle
+    if args.config == 5:   # only the leading cell layers are ever sampled: build just those
+        et, conn = meshgen.TET4, meshgen.kuhn_tets(320, cell_begin=0, cell_end=320 * 320 * 48)[0]
+    else:
+        et, conn, _ = meshgen.make_config(args.config, device="cpu")
+    conn = conn.numpy()
+    # size the per-step sample for ~ (few minutes) / (steps + warmup)
+    per_step = max(1.0, min(20.0, 150.0 / (args.steps + args.warmup)))
+    ms = min(conn.shape[0], 100_000)
+    while True:
+        sub = conn[:ms]
+        n_s = int(sub.max()) + 1
+        t0 = time.perf_counter()
+        oracle.node_csr(et, sub, n_s)
+        oracle.elem_csr(et, sub, n_s)
+        dt = time.perf_counter() - t0
+        if dt >= 0.6 * per_step or ms >= conn.shape[0]:
+            break
+        ms = min(conn.shape[0], int(ms * max(1.5, min(8.0, per_step / max(dt, 1e-3)))))
+    sub = conn[:ms]
+    n_s = int(sub.max()) + 1
+    for _ in range(args.warmup):
+        oracle.node_csr(et, sub, n_s)
+        oracle.elem_csr(et, sub, n_s)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.node_csr(et, sub, n_s)
+        oracle.elem_csr(et, sub, n_s)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    v = ms / t
+    sample = (f"first {ms:,} elements of config {args.config} ({meshgen.CONFIGS[args.config]['name']}), "
+              f"node ids < {n_s:,}; std::set oracle, node + element CSR, 1 thread")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": meshgen.CONFIGS[args.config]["name"], "sample_elements": ms,
+                       "parallelism": "host, 1 thread"},
+            "cpu_baseline": {"value": v, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1604_04689_b200 as mn
+    from paper_1604_04689_b200 import build as mnbuild
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if rank == 0:
+        mnbuild.build()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+    mn.load()
+
+    et, conn, base, M_total, N, info = workload(args.config, rank, world, dev)
+    M_local = conn.shape[0]
+    torch.cuda.synchronize()
+
+    if world > 1:
+        from paper_1604_04689_b200.dist import find_neighbors_dist
+
+        def step():
+            return find_neighbors_dist(conn, et, base, N)
+    else:
+        def step():
+            return mn.find_neighbors(conn, et, N)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def maxover(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        r = step()
+        del r
+    torch.cuda.synchronize()
+
+    # ---- device-timed region ----
+    s = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    mn.profile_reset()
+    mn.profile_enable(True)
+    launches0 = mn.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(s)
+        for _ in range(args.steps):
+            r = step()
+            del r
+        ev1.record(s)
+        torch.cuda.synchronize()
+    barrier()
+    launches = mn.launch_count() - launches0
+    mn.profile_enable(False)
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms = maxover(ms_local)
+    prof = mn.profile_collect()
+    mn.profile_reset()
+    value = M_total / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (live CUDA events on the launching stream) ----
+    peak, peak_src = peaks()
+    prof = sorted(prof, key=lambda e: -e["ms"])
+    top = prof[0]
+    achieved = (top["alg_bytes"] / top["launches"]) / ((top["ms"] / top["launches"]) / 1e3) / 1e9
+    tot_ms = sum(e["ms"] for e in prof)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"config{args.config}/n{world}/{top['name']}")
+    step_bytes = sum(e["alg_bytes"] for e in prof) / args.steps
+    roofline = {"bound": "hbm", "kernel": top["name"], "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "alg_bytes_per_launch": top["alg_bytes"] / top["launches"],
+                "avg_launch_ms": top["ms"] / top["launches"],
+                "share_of_kernel_time": top["ms"] / tot_ms if tot_ms else None}
+    kernels = [{"name": e["name"], "launches_per_step": e["launches"] / args.steps,
+                "ms_per_step": e["ms"] / args.steps, "share": e["ms"] / tot_ms if tot_ms else None,
+                "GBps": (e["alg_bytes"] / (e["ms"] / 1e3) / 1e9) if e["ms"] > 0 else None} for e in prof]
+    step_roof = {"alg_bytes_per_step": step_bytes, "achieved_GBps": step_bytes / (ms_local / 1e3) / 1e9,
+                 "frac_of_peak": step_bytes / (ms_local / 1e3) / 1e9 / peak,
+                 "kernel_ms_per_step": tot_ms / args.steps}
+
+    # ---- end to end through the public host-buffer API ----
+    e2e = None
+    if not args.no_e2e:
+        host_conn = conn.cpu().pin_memory()
+        h2d = host_conn.numel() * 4
+
+        if world > 1:
+            from paper_1604_04689_b200.dist import find_neighbors_dist
+
+            def estep():
+                c = host_conn.to(dev, non_blocking=True)
+                res = find_neighbors_dist(c, et, base, N)
+                outs = [x.to("cpu") for x in (*res.node, *res.elem)]
+                return outs
+        else:
+            def estep():
+                (no, ni), (eo, ei) = mn.find_neighbors_host(host_conn, et, N, device=dev)
+                return [no, ni, eo, ei]
+
+        outs = estep()   # warm the pinned caching allocator
+        d2h = sum(x.numel() * x.element_size() for x in outs)
+        del outs
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        e0.record(s)
+        for _ in range(args.steps):
+            outs = estep()
+            del outs
+        e1.record(s)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - w0) / args.steps * 1e3
+        barrier()
+        ems = maxover(max(e0.elapsed_time(e1) / args.steps, wall))
+        e2e = {"value": M_total / (ems / 1e3), "unit": "elements/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems}
+        del host_conn
+
+    # ---- CPU baseline: the oracle on a bounded sample, rank 0 at N=1 only ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, desc, dt, ms_s = oracle_sample(conn, et, args.cpu_seconds)
+        cpu = {"value": v, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"config {args.config}: {info['desc']}", "elements": M_total, "nodes": N,
+                       "parallelism": "single GPU" if world == 1 else
+                       f"{world} GPUs: element shards + NCCL all-to-all by owner node range",
+                       "l2": "inputs larger than L2 (no flush needed)", "outputs": "node + element CSR"},
+            "roofline": roofline, "step_roofline": step_roof, "kernels": kernels,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

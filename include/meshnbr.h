@@ -91,6 +91,16 @@ mn_status mn_find_node_neighbors(mn_elem_type type, const int32_t* d_conn, int64
                                  int64_t num_nodes, const mn_allocator* alloc, mn_stream stream,
                                  mn_csr* out, mn_error_detail* err);
 
+/* Same result as mn_find_node_neighbors, computed by the paper's node pipeline verbatim: every
+ * node pair (a, v) of every element edge is created (§2.2.1), the packed keys
+ * (a << b | v) are LSD-radix-sorted over all 2b bits (L228-232), adjacent duplicates dropped and
+ * run lengths scanned into offsets (L234-245).  mn_find_node_neighbors reaches the identical CSR
+ * from the element-pair sort instead (DESIGN.md §"Node path"); this entry is kept for parity and
+ * measurement. */
+mn_status mn_find_node_neighbors_sortpairs(mn_elem_type type, const int32_t* d_conn, int64_t num_elems,
+                                           int64_t num_nodes, const mn_allocator* alloc, mn_stream stream,
+                                           mn_csr* out, mn_error_detail* err);
+
 /* One-ring neighbouring ELEMENTS of every vertex (§2.2.2: pairs (node, element
  * itself), sorted by node, segmented reduction and scan).  Slices list element ids ascending. */
 mn_status mn_find_elem_neighbors(mn_elem_type type, const int32_t* d_conn, int64_t num_elems,

@@ -64,6 +64,89 @@ __device__ __forceinline__ uint64_t lookback_wait(const uint64_t* p, uint32_t ep
   return w;
 }
 
+// Windowed decoupled look-back for BPT digits owned by this thread: W predecessor status words per
+// digit are requested at once, so a walk over k aggregate-only tiles costs ceil(k / W) round trips
+// to L2 instead of k.  status is [tiles][bins]; returns the exclusive prefix of each digit.
+template <int BPT, int W>
+__device__ __forceinline__ void lookback_bins(const uint64_t* status, int bins, uint32_t tile, int b0,
+                                              uint32_t epoch, uint64_t (&excl)[BPT]) {
+  const int64_t t0 = (int64_t)tile - 1;
+  uint64_t w[BPT][W];
+#pragma unroll
+  for (int j = 0; j < BPT; ++j) {
+    excl[j] = 0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const int64_t t = t0 - k;
+      w[j][k] = t >= 0 ? ld_relaxed_u64(status + (size_t)t * bins + b0 + j) : 0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < BPT; ++j) {
+    int64_t tb = t0;
+    bool done = false;
+    while (true) {
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        if (!done) {
+          const uint64_t* p = status + (size_t)(tb - k) * bins + b0 + j;
+          uint64_t x = w[j][k];
+          int spins = 0;
+          while ((uint32_t)(x >> 56) != epoch || ((x >> 54) & 3u) == 0) {
+            if (++spins > 2) __nanosleep(16);
+            x = ld_relaxed_u64(p);
+          }
+          excl[j] += x & ST_VMASK;
+          done = ((x >> 54) & 3u) == ST_INC;
+        }
+      }
+      if (done) break;
+      tb -= W;
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        const int64_t t = tb - k;
+        w[j][k] = t >= 0 ? ld_relaxed_u64(status + (size_t)t * bins + b0 + j) : 0;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Warp-cooperative look-back over one status word per tile (compaction / scan kernels): the 32
+// lanes read 32 predecessors per round trip.  Call with the whole warp; returns the exclusive
+// prefix in every lane.
+__device__ __forceinline__ uint64_t warp_lookback(const uint64_t* status, uint32_t tile, uint32_t epoch,
+                                                  int lane) {
+  uint64_t excl = 0;
+  int64_t tb = (int64_t)tile - 1;
+  while (true) {
+    const int64_t t = tb - lane;
+    uint64_t x = t >= 0 ? ld_relaxed_u64(status + t) : st_pack(epoch, ST_INC, 0);
+    while (true) {
+      const bool ready = (uint32_t)(x >> 56) == epoch && ((x >> 54) & 3u) != 0;
+      if (__all_sync(0xffffffffu, ready)) break;
+      if (!ready) {
+        __nanosleep(16);
+        x = ld_relaxed_u64(status + t);
+      }
+    }
+    const unsigned inc = __ballot_sync(0xffffffffu, ((x >> 54) & 3u) == ST_INC);
+    uint64_t v = x & ST_VMASK;
+    if (inc) {
+      const int first = __ffs(inc) - 1;   // nearest predecessor holding an inclusive prefix
+      if (lane > first) v = 0;
+      return excl + warp_sum_u64(v);
+    }
+    excl += warp_sum_u64(v);
+    tb -= 32;
+  }
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -116,6 +199,22 @@ __device__ __forceinline__ void slot_locals(int r, int& la, int& lb) {
     la = (int)((EL::A_HI >> (4 * (r - 16))) & 0xF);
     lb = (int)((EL::B_HI >> (4 * (r - 16))) & 0xF);
   }
+}
+
+// Edge-neighbours of each local node (derived from the same edge lists): local node p's C
+// neighbours are nibbles p*C .. p*C+C-1 of (NB_LO | NB_HI << 64).
+template <int T> struct Nbr;
+template <> struct Nbr<MN_TRI3> { static constexpr uint64_t LO = 0x102021ull, HI = 0; };           // {1,2} {0,2} {0,1}
+template <> struct Nbr<MN_QUAD4> { static constexpr uint64_t LO = 0x20312031ull, HI = 0; };        // {1,3} {0,2} {1,3} {0,2}
+template <> struct Nbr<MN_TET4> { static constexpr uint64_t LO = 0x210310320321ull, HI = 0; };     // all other three
+template <> struct Nbr<MN_HEX8> {   // {1,3,4} {0,2,5} {1,3,6} {0,2,7} {0,5,7} {1,4,6} {2,5,7} {3,4,6}
+  static constexpr uint64_t LO = 0x1750720631520431ull, HI = 0x64375264ull;
+};
+
+template <int T>
+__device__ __forceinline__ int nbr_local(int p, int c) {
+  const int i = p * Elem<T>::C + c;
+  return (int)(((i < 16) ? (Nbr<T>::LO >> (4 * i)) : (Nbr<T>::HI >> (4 * (i - 16)))) & 0xF);
 }
 
 inline int arity_of(int t) { return t == MN_TRI3 ? 3 : (t == MN_HEX8 ? 8 : 4); }

@@ -181,13 +181,15 @@ struct OnesweepSmem {
   uint32_t tile;
 };
 
-template <typename KeyT, int SRC, int T, bool PAYLOAD, bool OWNER, int BINS, int THREADS, int ITEMS>
-__global__ void __launch_bounds__(THREADS)
+template <typename KeyT, int SRC, int T, bool PAYLOAD, bool OWNER, int BINS, int THREADS, int ITEMS,
+          int W = 4, int MINB = 3>
+__global__ void __launch_bounds__(THREADS, MINB)
 k_onesweep(PassArgs pa) {
   constexpr int WARPS = THREADS / 32;
   constexpr int TILE = THREADS * ITEMS;
-  constexpr int BPT = BINS / THREADS;   // bins owned per thread (contiguous)
-  static_assert(BINS % THREADS == 0, "BINS must be a multiple of THREADS");
+  // digits owned per thread (contiguous); with BINS < THREADS only threads tid < BINS own one
+  constexpr int BPT = BINS >= THREADS ? BINS / THREADS : 1;
+  static_assert(BINS % THREADS == 0 || THREADS % BINS == 0, "BINS and THREADS must nest");
   using Sm = OnesweepSmem<THREADS, ITEMS, BINS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
@@ -196,6 +198,7 @@ k_onesweep(PassArgs pa) {
 
   if (*pa.err != ERR_NONE) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool own = BINS >= THREADS || tid < BINS;   // warp-uniform
   if (tid == 0) sm.tile = atomicAdd(pa.ticket, 1u);
   for (int i = tid; i < WARPS * BINS; i += THREADS) (&sm.whist[0][0])[i] = 0;
   __syncthreads();
@@ -237,14 +240,12 @@ k_onesweep(PassArgs pa) {
     }
   }
 
-  // ---- rank: per-warp running digit histogram, warp-match aggregated ----
-  uint32_t rank[ITEMS];
-  uint32_t dig[ITEMS];
+  // ---- rank: per-warp running digit histogram, warp-match aggregated; dr = digit | rank << 16 ----
+  uint32_t dr[ITEMS];
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int64_t idx = chunk + i * 32 + lane;
     const uint32_t d = idx < pa.n ? digit_of<KeyT, OWNER>(key[i], pa.pd, BINS - 1) : (uint32_t)(BINS - 1);
-    dig[i] = d;
     const unsigned peers = __match_any_sync(FULL, d);
     const int leader = __ffs(peers) - 1;
     uint32_t old = 0;
@@ -253,17 +254,19 @@ k_onesweep(PassArgs pa) {
       sm.whist[warp][d] = old + __popc(peers);
     }
     old = __shfl_sync(FULL, old, leader);
-    rank[i] = old + __popc(peers & lanemask_lt());
+    dr[i] = d | ((old + __popc(peers & lanemask_lt())) << 16);
   }
   __syncthreads();
 
-  // ---- tile digit counts, publish aggregates ----
+  // ---- tile digit counts; publish the aggregate (tile 0: the inclusive prefix) ----
   const int64_t nvalid64 = pa.n - base;
   const int nvalid = nvalid64 >= TILE ? TILE : (int)nvalid64;
   uint32_t cnt[BPT];
   uint32_t tsum = 0;
 #pragma unroll
   for (int j = 0; j < BPT; ++j) {
+    cnt[j] = 0;
+    if (!own) continue;
     const int b = tid * BPT + j;
     uint32_t run = 0;
 #pragma unroll
@@ -277,7 +280,7 @@ k_onesweep(PassArgs pa) {
     const uint32_t pub = (b == BINS - 1) ? run - (uint32_t)(TILE - nvalid) : run;
     st_relaxed_u64(pa.status + (size_t)tile * BINS + b, st_pack(pa.epoch, tile == 0 ? ST_INC : ST_AGG, pub));
   }
-  // ---- local exclusive scan of the tile counts over bins ----
+  // ---- local exclusive scan of the tile counts over digits ----
   uint32_t inc = tsum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -290,43 +293,45 @@ k_onesweep(PassArgs pa) {
 #pragma unroll
   for (int w = 0; w < WARPS; ++w)
     if (w < warp) pre += (uint32_t)sm.wsum[w];
-  uint32_t run = pre + inc - tsum;
+  uint32_t binst[BPT];
+  {
+    uint32_t run = pre + inc - tsum;
 #pragma unroll
-  for (int j = 0; j < BPT; ++j) {
-    sm.binstart[tid * BPT + j] = run;
-    run += cnt[j];
+    for (int j = 0; j < BPT; ++j) {
+      binst[j] = run;
+      if (own) sm.binstart[tid * BPT + j] = run;
+      run += cnt[j];
+    }
   }
   __syncthreads();
 
-  // ---- scatter keys (and values) into shared memory in local digit order ----
+  // ---- scatter keys (and values) into shared memory in local digit order (frees registers) ----
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    const uint32_t d = dig[i];
-    const uint32_t pos = sm.binstart[d] + sm.whist[warp][d] + rank[i];
+    const uint32_t d = dr[i] & 0xFFFFu;
+    const uint32_t pos = sm.binstart[d] + sm.whist[warp][d] + (dr[i] >> 16);
     if (pos < (uint32_t)nvalid) {
       skeys[pos] = key[i];
       if (PAYLOAD || SRC == 2) svals[pos] = val[i];
     }
   }
 
-  // ---- decoupled look-back over the previous tiles, per owned digit ----
+  // ---- windowed decoupled look-back, publish the inclusive prefix, global digit offsets ----
+  uint64_t excl[BPT];
 #pragma unroll
-  for (int j = 0; j < BPT; ++j) {
-    const int b = tid * BPT + j;
-    uint64_t excl = 0;
-    if (tile > 0) {
-      int64_t t = (int64_t)tile - 1;
-      while (true) {
-        const uint64_t w = lookback_wait(pa.status + (size_t)t * BINS + b, pa.epoch);
-        excl += w & ST_VMASK;
-        if (((w >> 54) & 3u) == ST_INC) break;
-        --t;
-      }
+  for (int j = 0; j < BPT; ++j) excl[j] = 0;
+  if (tile > 0 && own) {
+    lookback_bins<BPT, W>(pa.status, BINS, tile, tid * BPT, pa.epoch, excl);
+#pragma unroll
+    for (int j = 0; j < BPT; ++j) {
+      const int b = tid * BPT + j;
       const uint32_t mine = (b == BINS - 1) ? cnt[j] - (uint32_t)(TILE - nvalid) : cnt[j];
-      st_relaxed_u64(pa.status + (size_t)tile * BINS + b, st_pack(pa.epoch, ST_INC, excl + mine));
+      st_relaxed_u64(pa.status + (size_t)tile * BINS + b, st_pack(pa.epoch, ST_INC, excl[j] + mine));
     }
-    sm.gofs[b] = pa.bases[b] + excl - sm.binstart[b];
   }
+#pragma unroll
+  for (int j = 0; j < BPT; ++j)
+    if (own) sm.gofs[tid * BPT + j] = pa.bases[tid * BPT + j] + excl[j] - binst[j];
   __syncthreads();
 
   // ---- write out: consecutive local slots of a digit go to consecutive global slots ----
@@ -366,7 +371,7 @@ struct UniqueArgs {
 };
 
 template <typename KeyT, int THREADS, int ITEMS>
-__global__ void __launch_bounds__(THREADS)
+__global__ void __launch_bounds__(THREADS, 3)
 k_unique_node(UniqueArgs ua) {
   constexpr int WARPS = THREADS / 32;
   constexpr int TILE = THREADS * ITEMS;
@@ -391,44 +396,44 @@ k_unique_node(UniqueArgs ua) {
   if (lane == 0 && chunk > 0 && chunk < ua.n) before = keys[chunk - 1];
   before = __shfl_sync(FULL, before, 0);
 
+  // predecessor of item i in this lane (lane 0 takes lane 31 of item i-1, or `before`)
+  auto prev_of = [&](int i) -> KeyT {
+    const KeyT up = __shfl_up_sync(FULL, key[i], 1);
+    const KeyT last = __shfl_sync(FULL, i > 0 ? key[i > 0 ? i - 1 : 0] : before, 31);
+    return lane > 0 ? up : (i > 0 ? last : before);
+  };
+
   unsigned bal[ITEMS];
   uint32_t wcount = 0;
-  KeyT prevk[ITEMS];
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int64_t idx = chunk + i * 32 + lane;
-    const KeyT up = __shfl_up_sync(FULL, key[i], 1);
-    const KeyT last = __shfl_sync(FULL, i > 0 ? key[i > 0 ? i - 1 : 0] : before, 31);
-    const KeyT p = lane > 0 ? up : (i > 0 ? last : before);
-    prevk[i] = p;
+    const KeyT p = prev_of(i);
     const bool f = idx < ua.n && (idx == 0 || key[i] != p);
     bal[i] = __ballot_sync(FULL, f);
     wcount += __popc(bal[i]);
   }
   if (lane == 0) s_wcount[warp] = wcount;
   __syncthreads();
-  if (tid == 0) {
-    uint32_t tot = 0;
-    for (int w = 0; w < WARPS; ++w) {
-      const uint32_t c = s_wcount[w];
-      s_wcount[w] = tot;
-      tot += c;
+  if (warp == 0) {
+    uint32_t c = lane < WARPS ? s_wcount[lane] : 0;
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
     }
+    const uint32_t tot = __shfl_sync(FULL, incl, 31);
+    if (lane < WARPS) s_wcount[lane] = incl - c;
     uint64_t excl = 0;
     if (tile == 0) {
-      st_relaxed_u64(ua.status, st_pack(ua.epoch, ST_INC, tot));
+      if (lane == 0) st_relaxed_u64(ua.status, st_pack(ua.epoch, ST_INC, tot));
     } else {
-      st_relaxed_u64(ua.status + tile, st_pack(ua.epoch, ST_AGG, tot));
-      int64_t t = (int64_t)tile - 1;
-      while (true) {
-        const uint64_t w = lookback_wait(ua.status + t, ua.epoch);
-        excl += w & ST_VMASK;
-        if (((w >> 54) & 3u) == ST_INC) break;
-        --t;
-      }
-      st_relaxed_u64(ua.status + tile, st_pack(ua.epoch, ST_INC, excl + tot));
+      if (lane == 0) st_relaxed_u64(ua.status + tile, st_pack(ua.epoch, ST_AGG, tot));
+      excl = warp_lookback(ua.status, tile, ua.epoch, lane);
+      if (lane == 0) st_relaxed_u64(ua.status + tile, st_pack(ua.epoch, ST_INC, excl + tot));
     }
-    s_texcl = excl;
+    if (lane == 0) s_texcl = excl;
   }
   __syncthreads();
   uint64_t pos = s_texcl + s_wcount[warp];
@@ -438,10 +443,11 @@ k_unique_node(UniqueArgs ua) {
     const int64_t idx = chunk + i * 32 + lane;
     const bool f = (bal[i] >> lane) & 1u;
     const uint64_t mypos = pos + __popc(bal[i] & lanemask_lt());
+    const KeyT p = prev_of(i);
     if (f) {
       ua.indices[mypos] = (uint32_t)(key[i] & vmask);
       const int64_t a = (int64_t)(key[i] >> ua.b);
-      const int64_t pa = idx == 0 ? -1 : (int64_t)(prevk[i] >> ua.b);
+      const int64_t pa = idx == 0 ? -1 : (int64_t)(p >> ua.b);
       for (int64_t x = pa + 1; x <= a; ++x) ua.offsets[x] = (int64_t)mypos;
     }
     if (idx == ua.n - 1) {
@@ -450,6 +456,238 @@ k_unique_node(UniqueArgs ua) {
       *ua.nnz = total;
     }
     pos += __popc(bal[i]);
+  }
+}
+
+// ================================================================================================
+// Node neighbours from the element CSR (B200 restructure of rows a1/a3n/a4, DESIGN.md §"Node path").
+// The paper's node pairs sorted by their first node are exactly the expansion of the element CSR:
+// incidence (a, e) at element-CSR position i yields the C edge-neighbours of a inside e, so the
+// pairs of node a are {nbr_p(conn[e]) : e in inc(a)} and only a per-node sort + adjacent-difference
+// dedupe remains (segments of C*deg(a) entries: 12 tri, 72 Kuhn tet, 24 hex).  One warp per node:
+//   raw = C*deg <= 32 : one candidate per lane, warp bitonic sort, ballot dedupe;
+//   raw <= 256        : warp hash set in shared memory (tagged with the node id, never cleared),
+//                       the <= 32 uniques then bitonic-sorted;
+//   otherwise         : the node is queued for k_node_giant (block sort).
+// Sorted unique neighbours go to temp[C * elem_off[a]] (the node's own raw region), counts to cnt.
+// ================================================================================================
+__device__ __forceinline__ uint32_t bitonic32(uint32_t x, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t y = __shfl_xor_sync(FULL, x, j);
+      const bool asc = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      x = (lower == asc) ? min(x, y) : max(x, y);
+    }
+  }
+  return x;
+}
+
+// Insert v into a per-warp open-addressing set tagged with the node (entry = tag | v).  Entries
+// with another tag are free.  Returns true if v was not yet present for this node.
+__device__ __forceinline__ bool hash_insert(unsigned long long* tab, unsigned long long tag, uint32_t v) {
+  uint32_t h = (v * 0x9E3779B1u) >> 25;   // 128 slots
+  const unsigned long long want = tag | v;
+  for (int probe = 0; probe < 512; ++probe) {
+    const unsigned long long cur = *(volatile unsigned long long*)(tab + h);
+    if ((cur & 0xFFFFFFFF00000000ull) == tag) {
+      if ((uint32_t)cur == v) return false;
+      h = (h + 1) & 127;
+      continue;
+    }
+    if (atomicCAS(tab + h, cur, want) == cur) return true;
+  }
+  return false;
+}
+
+template <int T, bool ALIGNED>
+__device__ __forceinline__ void load_row(const int32_t* __restrict__ conn, int64_t e, int (&row)[Elem<T>::K]) {
+  constexpr int K = Elem<T>::K;
+  if (ALIGNED && (K == 4 || K == 8)) {
+    const int4* p = reinterpret_cast<const int4*>(conn + e * K);
+#pragma unroll
+    for (int q = 0; q < K / 4; ++q) {
+      const int4 x = __ldg(p + q);
+      row[4 * q] = x.x; row[4 * q + 1] = x.y; row[4 * q + 2] = x.z; row[4 * q + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < K; ++q) row[q] = __ldg(conn + e * K + q);
+  }
+}
+
+template <int T>
+__device__ __forceinline__ int local_of(const int (&row)[Elem<T>::K], int a) {
+  int p = 0;
+#pragma unroll
+  for (int q = 0; q < Elem<T>::K; ++q) p = (row[q] == a) ? q : p;
+  return p;
+}
+
+template <int T>
+__device__ __forceinline__ uint32_t pick(const int (&row)[Elem<T>::K], int idx) {
+  uint32_t v = 0;
+#pragma unroll
+  for (int q = 0; q < Elem<T>::K; ++q) v = (q == idx) ? (uint32_t)row[q] : v;
+  return v;
+}
+
+constexpr int kGatherWarps = 8;
+
+template <int T, bool ALIGNED>
+__global__ void __launch_bounds__(32 * kGatherWarps)
+k_node_gather(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, const int32_t* __restrict__ conn,
+              int64_t N, uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, uint32_t* __restrict__ giants,
+              unsigned int* __restrict__ ngiant, const unsigned long long* __restrict__ err) {
+  constexpr int C = Elem<T>::C, K = Elem<T>::K;
+  __shared__ unsigned long long htab[kGatherWarps][128];
+  __shared__ uint32_t ulist[kGatherWarps][64];
+  if (err && *err != ERR_NONE) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kGatherWarps * 128; i += blockDim.x) (&htab[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t a = (((int64_t)blockIdx.x * blockDim.x) >> 5) + wib; a < N; a += nw) {
+    const int64_t s = eoff[a];
+    const int64_t d = eoff[a + 1] - s;
+    const int64_t raw = (int64_t)C * d;
+    uint32_t* out = temp + (size_t)C * s;
+    if (raw <= 32) {
+      uint32_t v = 0xFFFFFFFFu;
+      if (lane < raw) {
+        const int inc = lane / C, c = lane - inc * C;
+        int row[K];
+        load_row<T, ALIGNED>(conn, eidx[s + inc], row);
+        v = pick<T>(row, nbr_local<T>(local_of<T>(row, (int)a), c));
+      }
+      v = bitonic32(v, lane);
+      const uint32_t up = __shfl_up_sync(FULL, v, 1);
+      const bool f = lane < raw && (lane == 0 || v != up);
+      const unsigned bal = __ballot_sync(FULL, f);
+      if (f) out[__popc(bal & lanemask_lt())] = v;
+      if (lane == 0) cnt[a] = __popc(bal);
+    } else if (raw <= 256) {
+      const unsigned long long tag = (unsigned long long)(a + 1) << 32;
+      int uc = 0;
+      bool overflow = false;
+      for (int64_t b0 = 0; b0 < d && !overflow; b0 += 32) {
+        const bool act = b0 + lane < d;
+        int row[K];
+        int p = 0;
+        if (act) {
+          load_row<T, ALIGNED>(conn, eidx[s + b0 + lane], row);
+          p = local_of<T>(row, (int)a);
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const uint32_t v = act ? pick<T>(row, nbr_local<T>(p, c)) : 0u;
+          const bool isnew = act && hash_insert(htab[wib], tag, v);
+          const unsigned bal = __ballot_sync(FULL, isnew);
+          const int pos = uc + __popc(bal & lanemask_lt());
+          if (isnew && pos < 64) ulist[wib][pos] = v;
+          uc += __popc(bal);
+        }
+        overflow = uc > 32;
+      }
+      __syncwarp();
+      if (!overflow) {
+        uint32_t x = lane < uc ? ulist[wib][lane] : 0xFFFFFFFFu;
+        x = bitonic32(x, lane);
+        if (lane < uc) out[lane] = x;
+        if (lane == 0) cnt[a] = uc;
+      } else if (lane == 0) {
+        giants[atomicAdd(ngiant, 1u)] = (uint32_t)a;
+      }
+      __syncwarp();
+    } else if (lane == 0) {
+      giants[atomicAdd(ngiant, 1u)] = (uint32_t)a;
+    }
+  }
+}
+
+// Nodes with more than 256 raw neighbour entries (or more than 32 distinct neighbours): one CTA per
+// node, the raw entries sorted with a block bitonic network (shared memory when they fit, else in
+// place in the node's global raw region), then adjacent-difference dedupe.
+template <int T, bool ALIGNED>
+__global__ void __launch_bounds__(1024)
+k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, const int32_t* __restrict__ conn,
+             uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, const uint32_t* __restrict__ giants,
+             const unsigned int* __restrict__ ngiant, int smem_cap, const unsigned long long* __restrict__ err) {
+  constexpr int C = Elem<T>::C, K = Elem<T>::K;
+  extern __shared__ uint32_t sv[];
+  __shared__ int s_u;
+  if (err && *err != ERR_NONE) return;
+  const unsigned ng = *ngiant;
+  for (unsigned g = blockIdx.x; g < ng; g += gridDim.x) {
+    const int64_t a = giants[g];
+    const int64_t s = eoff[a];
+    const int64_t d = eoff[a + 1] - s;
+    const int64_t raw = (int64_t)C * d;
+    uint32_t* out = temp + (size_t)C * s;
+    uint32_t* buf = raw <= smem_cap ? sv : out;
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+      int row[K];
+      load_row<T, ALIGNED>(conn, eidx[s + i], row);
+      const int p = local_of<T>(row, (int)a);
+#pragma unroll
+      for (int c = 0; c < C; ++c) buf[i * C + c] = pick<T>(row, nbr_local<T>(p, c));
+    }
+    __syncthreads();
+    int64_t n2 = 1;
+    while (n2 < raw) n2 <<= 1;
+    // ascending bitonic sort of raw entries, implicit +inf padding to n2 (pairs past raw skipped)
+    for (int64_t k = 2; k <= n2; k <<= 1) {
+      for (int64_t j = k >> 1; j > 0; j >>= 1) {
+        for (int64_t t = threadIdx.x; t < n2 / 2; t += blockDim.x) {
+          int64_t lo, hi;
+          if (j == (k >> 1)) {   // flip step: compare i with its mirror inside the k-block
+            const int64_t blk = t / j, off = t % j;
+            lo = blk * k + off;
+            hi = blk * k + k - 1 - off;
+          } else {
+            const int64_t blk = t / j, off = t % j;
+            lo = blk * 2 * j + off;
+            hi = lo + j;
+          }
+          if (hi < raw) {
+            const uint32_t x = buf[lo], y = buf[hi];
+            if (x > y) { buf[lo] = y; buf[hi] = x; }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (threadIdx.x == 0) {
+      int u = 0;
+      for (int64_t i = 0; i < raw; ++i)
+        if (i == 0 || buf[i] != buf[i - 1]) out[u++] = buf[i];
+      cnt[a] = u;
+      s_u = u;
+    }
+    __syncthreads();
+  }
+}
+
+// Node CSR indices: copy each node's sorted unique list to its final offset (warp per 32 nodes).
+__global__ void __launch_bounds__(256)
+k_node_compact(const int64_t* __restrict__ eoff, int C, const uint32_t* __restrict__ temp,
+               const int64_t* __restrict__ noff, int64_t N, int32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t a0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; a0 < N; a0 += nw * 32) {
+    const int64_t a = a0 + lane;
+    int64_t src = 0, dst = 0, u = 0;
+    if (a < N) {
+      src = (int64_t)C * eoff[a];
+      dst = noff[a];
+      u = noff[a + 1] - dst;
+    }
+    for (int j = 0; j < 32; ++j) {
+      const int64_t sj = __shfl_sync(FULL, src, j), dj = __shfl_sync(FULL, dst, j), uj = __shfl_sync(FULL, u, j);
+      for (int64_t i = lane; i < uj; i += 32) out[dj + i] = (int32_t)temp[sj + i];
+    }
   }
 }
 
@@ -505,28 +743,25 @@ k_scan_i32(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out,
   }
   if (lane == 0) s_w[warp] = wtot;
   __syncthreads();
-  if (tid == 0) {
-    uint64_t tot = 0;
-    for (int w = 0; w < WARPS; ++w) {
-      const uint64_t c = s_w[w];
-      s_w[w] = tot;
-      tot += c;
+  if (warp == 0) {
+    uint64_t c = lane < WARPS ? s_w[lane] : 0;
+    uint64_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
     }
+    const uint64_t tot = __shfl_sync(FULL, incl, 31);
+    if (lane < WARPS) s_w[lane] = incl - c;
     uint64_t excl = 0;
     if (tile == 0) {
-      st_relaxed_u64(status, st_pack(epoch, ST_INC, tot));
+      if (lane == 0) st_relaxed_u64(status, st_pack(epoch, ST_INC, tot));
     } else {
-      st_relaxed_u64(status + tile, st_pack(epoch, ST_AGG, tot));
-      int64_t t = (int64_t)tile - 1;
-      while (true) {
-        const uint64_t w = lookback_wait(status + t, epoch);
-        excl += w & ST_VMASK;
-        if (((w >> 54) & 3u) == ST_INC) break;
-        --t;
-      }
-      st_relaxed_u64(status + tile, st_pack(epoch, ST_INC, excl + tot));
+      if (lane == 0) st_relaxed_u64(status + tile, st_pack(epoch, ST_AGG, tot));
+      excl = warp_lookback(status, tile, epoch, lane);
+      if (lane == 0) st_relaxed_u64(status + tile, st_pack(epoch, ST_INC, excl + tot));
     }
-    s_texcl = excl;
+    if (lane == 0) s_texcl = excl;
   }
   __syncthreads();
   const int64_t add = (int64_t)(s_texcl + s_w[warp]);

@@ -110,9 +110,17 @@ static mn_status decode_err(uint64_t w, mn_error_detail* err) {
 // ================================================================================================
 // plans
 // ================================================================================================
+// onesweep pass tiles: 512 threads x 16 keys, 2 CTAs per SM, look-back window 4 (chosen with
+// tools/sweep_onesweep.cu on B200: per-tile look-back cost dominates, so larger tiles win)
+constexpr int kPassThreads = 512;
+constexpr int kPassItems = 16;
+constexpr int kPassMinBlocks = 2;
+constexpr int kPassWindow = 4;
+constexpr int kTile = kPassThreads * kPassItems;   // keys per onesweep tile
+// compaction / scan tiles
 constexpr int kThreads = 256;
 constexpr int kItems = 16;
-constexpr int kTile = kThreads * kItems;           // keys per onesweep / unique tile
+constexpr int kUTile = kThreads * kItems;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kThreads * kScanItems;
 
@@ -169,18 +177,18 @@ static int stream_grid(int64_t n) {
 // ================================================================================================
 template <typename KeyT, int SRC, int T, bool PAYLOAD, bool OWNER, int BINS>
 static cudaError_t run_pass(PassArgs pa, cudaStream_t s, const char* name, double bytes) {
-  using Sm = OnesweepSmem<kThreads, kItems, BINS>;
+  using Sm = OnesweepSmem<kPassThreads, kPassItems, BINS>;
   const int64_t tiles = tiles_of(pa.n, kTile);
   if (tiles == 0) return cudaSuccess;
   const size_t smem = ((sizeof(Sm) + 15) & ~size_t(15)) + (size_t)kTile * sizeof(KeyT) +
                       ((PAYLOAD || SRC == 2) ? (size_t)kTile * 4 : 0);
-  auto kern = k_onesweep<KeyT, SRC, T, PAYLOAD, OWNER, BINS, kThreads, kItems>;
+  auto kern = k_onesweep<KeyT, SRC, T, PAYLOAD, OWNER, BINS, kPassThreads, kPassItems, kPassWindow, kPassMinBlocks>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  return launch(name, bytes, s, [&] { kern<<<(unsigned)tiles, kThreads, smem, s>>>(pa); });
+  return launch(name, bytes, s, [&] { kern<<<(unsigned)tiles, kPassThreads, smem, s>>>(pa); });
 }
 
 static PassDigit mask_digit(int shift, int width) {
@@ -206,7 +214,7 @@ static mn_status pipeline(const Plan& P, const int32_t* conn, Mem& mem, bool wan
   const int npass = nnode_pass + nelem_pass;
   const int64_t node_tiles = tiles_of(P.Pn, kTile), elem_tiles = tiles_of(P.Pe, kTile);
   const int64_t st_tiles = std::max(want_node ? node_tiles : 0, want_elem ? elem_tiles : 0);
-  const int64_t uq_tiles = want_node ? node_tiles : 0;
+  const int64_t uq_tiles = want_node ? tiles_of(P.Pn, kUTile) : 0;
   const size_t w = sizeof(KeyT);
   // elem arrays alias the dead node key buffer when it is large enough
   const bool alias = want_node && want_elem && (size_t)P.Pn * w >= (size_t)16 * P.Pe;
@@ -332,7 +340,7 @@ static mn_status pipeline(const Plan& P, const int32_t* conn, Mem& mem, bool wan
       ua.nnz = nnz;
       ua.err = errw;
       MN_CUDA(launch("unique_node", (double)w * P.Pn + 8.0 * (P.N + 1), s, [&] {
-        k_unique_node<KeyT, kThreads, kItems><<<(unsigned)node_tiles, kThreads, 0, s>>>(ua);
+        k_unique_node<KeyT, kThreads, kItems><<<(unsigned)uq_tiles, kThreads, 0, s>>>(ua);
       }));
       node_idx = reinterpret_cast<int32_t*>(ua.indices);
     }
@@ -414,6 +422,204 @@ done:
   return st;
 }
 
+// ================================================================================================
+// the whole path, B200 restructure (DESIGN.md §"Node path"): element pairs are radix-sorted once
+// (stable, node digits); the element CSR falls out of it and the node CSR is the per-node
+// expansion of the element CSR (C edge-neighbours per incidence), sorted and deduplicated per
+// node, counted, scanned, and compacted into an exact-size output after the one host sync.
+// ================================================================================================
+template <int T, int BINS>
+static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool want_node, bool want_elem,
+                              mn_csr* node_out, mn_csr* elem_out, mn_error_detail* err) {
+  cudaStream_t s = mem.s;
+  mn_status st = MN_OK;
+  const int nd = P.dp.nd;
+  const int64_t elem_tiles = tiles_of(P.Pe, kTile);
+  const int64_t scan_tiles = tiles_of(P.N, kScanTile);
+  const int64_t giant_cap = P.N;   // any node may overflow the warp path (> 32 distinct neighbours)
+  const bool aligned = ((uintptr_t)conn & 15) == 0;
+  int64_t *node_off = nullptr, *elem_off = nullptr;
+  int32_t* elem_idx = nullptr;
+  void* ws = nullptr;
+  uint64_t* host = pinned_pair();
+  if (!host) return MN_ERR_CUDA;
+
+  // ---- outputs known in size up front ----
+  if (want_node) {
+    node_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
+    if (!node_off) { st = MN_ERR_OOM; goto done; }
+  }
+  if (want_elem) {
+    elem_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
+    elem_idx = P.Pe ? (int32_t*)mem.get((size_t)P.Pe * 4) : nullptr;
+    if (!elem_off || (P.Pe && !elem_idx)) { st = MN_ERR_OOM; goto done; }
+  }
+  if (P.M == 0) {
+    if (node_off) MN_CUDA(cudaMemsetAsync(node_off, 0, (size_t)(P.N + 1) * 8, s));
+    if (elem_off) MN_CUDA(cudaMemsetAsync(elem_off, 0, (size_t)(P.N + 1) * 8, s));
+    MN_CUDA(cudaStreamSynchronize(s));
+    if (want_node) { node_out->num_nodes = P.N; node_out->nnz = 0; node_out->offsets = node_off; node_out->indices = nullptr; node_out->owner = mem.a; }
+    if (want_elem) { elem_out->num_nodes = P.N; elem_out->nnz = 0; elem_out->offsets = elem_off; elem_out->indices = nullptr; elem_out->owner = mem.a; }
+    return MN_OK;
+  }
+  {
+    // ---- workspace ----
+    size_t head = 0;
+    unsigned long long *errw = nullptr, *hist = nullptr;
+    uint32_t *tickets = nullptr, *ekA = nullptr, *ekB = nullptr, *epA = nullptr, *epB = nullptr, *giants = nullptr;
+    unsigned int* ngiant = nullptr;
+    uint64_t *bases = nullptr, *status = nullptr, *sstatus = nullptr;
+    int32_t* cnt = nullptr;
+    int64_t* eoff = elem_off;
+    int32_t* eidx = elem_idx;
+    auto layout = [&](Arena& a) {
+      errw = a.take<unsigned long long>(2);
+      tickets = a.take<uint32_t>(32);
+      ngiant = a.take<unsigned int>(1);
+      hist = a.take<unsigned long long>((size_t)nd * BINS);
+      bases = a.take<uint64_t>((size_t)nd * BINS);
+      status = a.take<uint64_t>((size_t)elem_tiles * BINS);
+      sstatus = a.take<uint64_t>((size_t)(scan_tiles ? scan_tiles : 1));
+      head = a.off;
+      ekA = a.take<uint32_t>(4 * (size_t)P.Pe);   // ekA | ekB | epA | epB; later the node raw region
+      ekB = ekA + P.Pe;
+      epA = ekA + 2 * P.Pe;
+      epB = ekA + 3 * P.Pe;
+      if (want_node) {
+        cnt = a.take<int32_t>((size_t)P.N);
+        giants = a.take<uint32_t>((size_t)(giant_cap ? giant_cap : 1));
+        if (!want_elem) {
+          eoff = a.take<int64_t>((size_t)P.N + 1);
+          eidx = a.take<int32_t>((size_t)P.Pe);
+        }
+      }
+    };
+    Arena ar;
+    layout(ar);
+    ws = mem.get(ar.off);
+    if (!ws) { st = MN_ERR_OOM; goto done; }
+    ar = Arena{};
+    ar.base = (char*)ws;
+    eoff = elem_off;
+    eidx = elem_idx;
+    layout(ar);
+    MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
+    MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
+
+    // ---- a1/a2 validation + digit histograms of the node ids ----
+    MN_CUDA(launch("hist_validate", 4.0 * P.K * P.M, s, [&] {
+      k_hist_validate<T, BINS><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, 0, P.dp, 0, 1, hist, errw);
+    }));
+    BasesDesc bd{};
+    bd.npass = nd;
+    for (int q = 0; q < nd; ++q) { bd.hidx[q] = q; bd.mult[q] = 1; }
+    MN_CUDA(launch("bucket_bases", 0.0, s, [&] { k_bucket_bases<BINS><<<nd, BINS, 0, s>>>(hist, bd, bases, errw); }));
+
+    // ---- a2 + a3: element pairs (node, element) created from conn, stable LSD on the node digits ----
+    uint32_t* kb[2] = {ekA, ekB};
+    uint32_t* vb[2] = {epA, epB};
+    const uint32_t* kin = nullptr;
+    const uint32_t* vin = nullptr;
+    for (int q = 0; q < nd; ++q) {
+      PassArgs pa{};
+      pa.keys_in = kin;
+      pa.vals_in = vin;
+      pa.keys_out = kb[q & 1];
+      pa.vals_out = (q == nd - 1) ? reinterpret_cast<uint32_t*>(eidx) : vb[q & 1];
+      pa.conn = conn;
+      pa.n = P.Pe;
+      pa.pd = mask_digit(P.dp.shift[q], P.dp.width[q]);
+      pa.bases = bases + (size_t)q * BINS;
+      pa.status = status;
+      pa.ticket = tickets + q;
+      pa.epoch = (uint32_t)(q + 1);
+      pa.err = errw;
+      if (q == 0) {
+        MN_CUDA((run_pass<uint32_t, 2, T, false, false, BINS>(pa, s, "onesweep_elem_first", 4.0 * P.Pe + 8.0 * P.Pe)));
+      } else {
+        MN_CUDA((run_pass<uint32_t, 0, 0, true, false, BINS>(pa, s, "onesweep_elem", 16.0 * P.Pe)));
+      }
+      kin = kb[q & 1];
+      vin = vb[q & 1];
+    }
+    // ---- a4 + a5 (elements): run starts of the sorted node keys -> offsets ----
+    MN_CUDA(launch("elem_offsets", 4.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
+      k_elem_offsets<<<stream_grid(P.Pe), 256, 0, s>>>(kin, P.Pe, P.N, eoff, errw);
+    }));
+
+    int64_t U = 0;
+    if (want_node) {
+      // ---- a1 + a3n + a4 (nodes): expand the element CSR per node, sort + dedupe per node ----
+      uint32_t* temp = ekA;   // C * Pe <= 4 * Pe entries: the dead element-sort buffers
+      const double gb = 8.0 * (P.N + 1) + 4.0 * P.Pe + 4.0 * P.K * P.Pe;   // offsets, incidences, rows
+      if (aligned) {
+        MN_CUDA(launch("node_gather", gb, s, [&] {
+          k_node_gather<T, true><<<148 * 8, 32 * kGatherWarps, 0, s>>>(eoff, eidx, conn, P.N, temp, cnt, giants, ngiant, errw);
+        }));
+      } else {
+        MN_CUDA(launch("node_gather", gb, s, [&] {
+          k_node_gather<T, false><<<148 * 8, 32 * kGatherWarps, 0, s>>>(eoff, eidx, conn, P.N, temp, cnt, giants, ngiant, errw);
+        }));
+      }
+      const int cap = 48 * 1024;   // uint32 entries sorted in shared memory by k_node_giant (192 KB)
+      static bool giant_attr = false;
+      if (!giant_attr) {
+        cudaFuncSetAttribute(k_node_giant<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
+        cudaFuncSetAttribute(k_node_giant<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
+        giant_attr = true;
+      }
+      MN_CUDA(launch("node_giant", 0.0, s, [&] {
+        if (aligned) k_node_giant<T, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, conn, temp, cnt, giants, ngiant, cap, errw);
+        else k_node_giant<T, false><<<148, 1024, cap * 4, s>>>(eoff, eidx, conn, temp, cnt, giants, ngiant, cap, errw);
+      }));
+      // ---- a5 (nodes): exclusive scan of the unique counts -> offsets ----
+      if (P.N > 0)   // N == 0 with M > 0 always fails validation; nothing to scan
+      MN_CUDA(launch("scan_counts", 4.0 * P.N + 8.0 * (P.N + 1), s, [&] {
+        k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(cnt, P.N, node_off, sstatus,
+                                                                                 tickets + 31, 1);
+      }));
+      MN_CUDA(cudaMemcpyAsync(host + 1, node_off + P.N, 8, cudaMemcpyDeviceToHost, s));
+    }
+    // ---- a6: the one blocking read (validation word, node nnz) ----
+    MN_CUDA(cudaMemcpyAsync(host, errw, 8, cudaMemcpyDeviceToHost, s));
+    MN_CUDA(cudaStreamSynchronize(s));
+    st = decode_err(host[0], err);
+    if (st != MN_OK) goto done;
+    if (want_node) {
+      U = (int64_t)host[1];
+      int32_t* out = U ? (int32_t*)mem.get((size_t)U * 4) : nullptr;
+      if (U && !out) { st = MN_ERR_OOM; goto done; }
+      if (U) {
+        MN_CUDA(launch("node_compact", 8.0 * U + 24.0 * P.N, s, [&] {
+          k_node_compact<<<stream_grid(P.N / 8 + 1), 256, 0, s>>>(eoff, P.C, ekA, node_off, P.N, out);
+        }));
+      }
+      node_out->num_nodes = P.N;
+      node_out->nnz = U;
+      node_out->offsets = node_off;
+      node_out->indices = out;
+      node_out->owner = mem.a;
+    }
+    if (want_elem) {
+      elem_out->num_nodes = P.N;
+      elem_out->nnz = P.Pe;
+      elem_out->offsets = elem_off;
+      elem_out->indices = elem_idx;
+      elem_out->owner = mem.a;
+    }
+    mem.put(ws);
+    return MN_OK;
+  }
+done:
+  if (ws) { cudaStreamSynchronize(s); mem.put(ws); }
+  mem.put(node_off);
+  mem.put(elem_off);
+  mem.put(elem_idx);
+  if (want_node && node_out) std::memset(node_out, 0, sizeof(*node_out));
+  if (want_elem && elem_out) std::memset(elem_out, 0, sizeof(*elem_out));
+  return st;
+}
+
 template <int T>
 static mn_status dispatch_key(const Plan& P, const int32_t* conn, Mem& mem, bool wn, bool we,
                               mn_csr* no, mn_csr* eo, mn_error_detail* err) {
@@ -432,19 +638,37 @@ static mn_status check_args(int t, const void* conn, int64_t M, int64_t N) {
   return MN_OK;
 }
 
+template <int T>
+static mn_status dispatch_inc(const Plan& P, const int32_t* conn, Mem& mem, bool wn, bool we, mn_csr* no,
+                              mn_csr* eo, mn_error_detail* err) {
+  if (P.bins == 256) return pipeline_inc<T, 256>(P, conn, mem, wn, we, no, eo, err);
+  return pipeline_inc<T, 512>(P, conn, mem, wn, we, no, eo, err);
+}
+
+// sortpairs = the paper's node pipeline verbatim (node pairs -> global LSD sort -> unique);
+// otherwise the element-CSR expansion path (identical output).
 static mn_status find(int t, const int32_t* conn, int64_t M, int64_t N, const mn_allocator* a,
-                      mn_stream stream, bool wn, bool we, mn_csr* no, mn_csr* eo, mn_error_detail* err) {
+                      mn_stream stream, bool wn, bool we, mn_csr* no, mn_csr* eo, mn_error_detail* err,
+                      bool sortpairs = false) {
   if (err) { err->elem = -1; err->pos = -1; }
   mn_status st = check_args(t, conn, M, N);
   if (st != MN_OK) return st;
   if ((wn && !no) || (we && !eo)) return MN_ERR_INVALID_ARG;
   Mem mem(a, (cudaStream_t)stream);
   const Plan P = make_plan(t, M, N);
+  if (sortpairs) {
+    switch (t) {
+      case MN_TRI3: return dispatch_key<MN_TRI3>(P, conn, mem, wn, we, no, eo, err);
+      case MN_QUAD4: return dispatch_key<MN_QUAD4>(P, conn, mem, wn, we, no, eo, err);
+      case MN_TET4: return dispatch_key<MN_TET4>(P, conn, mem, wn, we, no, eo, err);
+      default: return dispatch_key<MN_HEX8>(P, conn, mem, wn, we, no, eo, err);
+    }
+  }
   switch (t) {
-    case MN_TRI3: return dispatch_key<MN_TRI3>(P, conn, mem, wn, we, no, eo, err);
-    case MN_QUAD4: return dispatch_key<MN_QUAD4>(P, conn, mem, wn, we, no, eo, err);
-    case MN_TET4: return dispatch_key<MN_TET4>(P, conn, mem, wn, we, no, eo, err);
-    default: return dispatch_key<MN_HEX8>(P, conn, mem, wn, we, no, eo, err);
+    case MN_TRI3: return dispatch_inc<MN_TRI3>(P, conn, mem, wn, we, no, eo, err);
+    case MN_QUAD4: return dispatch_inc<MN_QUAD4>(P, conn, mem, wn, we, no, eo, err);
+    case MN_TET4: return dispatch_inc<MN_TET4>(P, conn, mem, wn, we, no, eo, err);
+    default: return dispatch_inc<MN_HEX8>(P, conn, mem, wn, we, no, eo, err);
   }
 }
 
@@ -526,7 +750,7 @@ static mn_status unique_csr(const KeyT* keys, int64_t n, int b, int64_t N, int64
     *h_nnz = 0;
     return MN_OK;
   }
-  const int64_t tiles = tiles_of(n, kTile);
+  const int64_t tiles = tiles_of(n, kUTile);
   Arena ar;
   unsigned long long* errw = ar.take<unsigned long long>(2);
   uint32_t* ticket = ar.take<uint32_t>(1);
@@ -703,6 +927,11 @@ mn_status mn_find_node_neighbors(mn_elem_type t, const int32_t* d_conn, int64_t 
   return find(t, d_conn, M, N, a, s, true, false, out, nullptr, err);
 }
 
+mn_status mn_find_node_neighbors_sortpairs(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N,
+                                           const mn_allocator* a, mn_stream s, mn_csr* out, mn_error_detail* err) {
+  return find(t, d_conn, M, N, a, s, true, false, out, nullptr, err, true);
+}
+
 mn_status mn_find_elem_neighbors(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N,
                                  const mn_allocator* a, mn_stream s, mn_csr* out, mn_error_detail* err) {
   return find(t, d_conn, M, N, a, s, false, true, nullptr, out, err);
@@ -772,7 +1001,7 @@ mn_status mn_workspace_bytes(mn_elem_type t, int64_t M, int64_t N, int modes, si
   const bool wn = modes & 1, we = modes & 2;
   const size_t w = P.key64 ? 8 : 4;
   const int64_t st_tiles = std::max(wn ? tiles_of(P.Pn, kTile) : 0, we ? tiles_of(P.Pe, kTile) : 0);
-  size_t b = 4096 + (size_t)st_tiles * P.bins * 8 + (wn ? (size_t)tiles_of(P.Pn, kTile) * 8 : 0);
+  size_t b = 4096 + (size_t)st_tiles * P.bins * 8 + (wn ? (size_t)tiles_of(P.Pn, kUTile) * 8 : 0);
   if (wn) b += 2 * (size_t)P.Pn * w;
   const bool alias = wn && we && (size_t)P.Pn * w >= (size_t)16 * P.Pe;
   if (we && !alias) b += 16 * (size_t)P.Pe;

@@ -1,0 +1,120 @@
+"""Multi-GPU one-ring neighbours: one process per GPU, elements sharded.
+
+Each rank holds a contiguous element shard (global element base given).  Nodes are owned in
+contiguous ranges [r*ceil(N/G), (r+1)*ceil(N/G)).  Per call:
+
+  1. mn_dist_bucket   (CUDA)  validate the shard, create the node pairs and the (node, element)
+                              pairs and stably bucket both by owner rank — one onesweep pass each,
+                              the pair creation fused in (no emitted-pair round trip);
+  2. count exchange           all_to_all of the G x 2 pair counts (NCCL over NVLink);
+  3. payload exchange         all_to_all(v) of node keys and element pairs, received in source-rank
+                              order, so element ids stay ascending per node (stable by rank);
+  4. mn_dist_finish   (CUDA)  rebase onto the owned range, sort, dedupe, offsets -> CSR slices.
+
+The result on rank r is the CSR of nodes [lo_r, hi_r) with local offsets; concatenating the
+slices in rank order (offsets shifted by the preceding ranks' nnz, returned as ``base``) is
+bit-identical to the single-GPU CSR.
+
+``ops`` is the per-rank compute: the CUDA library by default.  The exchange logic is independent
+of it, which is what lets tests/test_dist_gloo.py drive this exact orchestration over the gloo
+backend on CPU with a test-side stand-in for the two CUDA calls.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass
+class DistResult:
+    lo: int
+    hi: int
+    node: tuple          # (offsets int64[hi-lo+1], indices int32[nnz]) — local offsets
+    elem: tuple
+    node_base: int       # global offset of this slice in the single-GPU node CSR
+    elem_base: int
+    sent_pairs: int      # pairs this rank sent to other ranks (exchange volume)
+
+
+def owner_range(num_nodes: int, world: int, rank: int):
+    chunk = max(1, -(-num_nodes // world))
+    lo = min(num_nodes, rank * chunk)
+    hi = min(num_nodes, (rank + 1) * chunk)
+    return lo, hi
+
+
+class CudaOps:
+    """The product compute: libmeshnbr's two dist entry points."""
+
+    @staticmethod
+    def bucket(conn_shard, etype, elem_base, num_nodes, world):
+        from . import dist_bucket
+        return dist_bucket(conn_shard, etype, elem_base, num_nodes, world)
+
+    @staticmethod
+    def finish(node_keys, elem_pairs, num_nodes, lo, hi):
+        from . import dist_finish
+        return dist_finish(node_keys, elem_pairs, num_nodes, lo, hi)
+
+
+def find_neighbors_dist(conn_shard: torch.Tensor, etype, global_elem_base: int, num_nodes: int,
+                        group=None, ops=None) -> DistResult:
+    ops = ops or CudaOps
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = conn_shard.device
+    nk, ncount, ep, ecount = ops.bucket(conn_shard, etype, int(global_elem_base), int(num_nodes), world)
+    # ---- count exchange: row g of `send` goes to rank g ----
+    send = torch.tensor([[ncount[g], ecount[g]] for g in range(world)], dtype=torch.int64, device=dev)
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send.reshape(-1), group=group)
+    recv = recv.reshape(world, 2).cpu()
+    rn = recv[:, 0].tolist()
+    re_ = recv[:, 1].tolist()
+    # ---- payload exchange, received in source-rank order ----
+    node_in = torch.empty(sum(rn), dtype=torch.int64, device=dev)
+    elem_in = torch.empty(sum(re_), dtype=torch.int64, device=dev)
+    dist.all_to_all_single(node_in, nk, output_split_sizes=rn, input_split_sizes=list(ncount), group=group)
+    dist.all_to_all_single(elem_in, ep, output_split_sizes=re_, input_split_sizes=list(ecount), group=group)
+    del nk, ep
+    lo, hi = owner_range(num_nodes, world, rank)
+    node, elem = ops.finish(node_in, elem_in, num_nodes, lo, hi)
+    # ---- global bases of the slices (exclusive scan of the per-rank nnz) ----
+    mine = torch.tensor([node[1].numel(), elem[1].numel()], dtype=torch.int64, device=dev)
+    allv = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(allv, mine, group=group)
+    allv = torch.stack(allv).cpu()
+    node_base = int(allv[:rank, 0].sum())
+    elem_base = int(allv[:rank, 1].sum())
+    sent = sum(int(ncount[g]) + int(ecount[g]) for g in range(world) if g != rank)
+    return DistResult(lo, hi, node, elem, node_base, elem_base, sent)
+
+
+def gather_global(res: DistResult, num_nodes: int, group=None):
+    """Assemble the global CSRs on every rank (verification helper; moves everything)."""
+    world = dist.get_world_size(group)
+    out = []
+    for which, base in ((res.node, res.node_base), (res.elem, res.elem_base)):
+        off, idx = which
+        glob_off = off[:-1] + base
+        sizes = torch.tensor([glob_off.numel(), idx.numel()], dtype=torch.int64, device=off.device)
+        allsz = [torch.empty_like(sizes) for _ in range(world)]
+        dist.all_gather(allsz, sizes, group=group)
+        allsz = torch.stack(allsz).cpu()
+        mo, mi = int(allsz[:, 0].max()), int(allsz[:, 1].max())
+        po = torch.zeros(mo, dtype=torch.int64, device=off.device)
+        po[: glob_off.numel()] = glob_off
+        pi = torch.zeros(mi, dtype=torch.int32, device=off.device)
+        pi[: idx.numel()] = idx
+        offs = [torch.empty_like(po) for _ in range(world)]
+        idxs = [torch.empty_like(pi) for _ in range(world)]
+        dist.all_gather(offs, po, group=group)      # padded to equal sizes (gloo needs that)
+        dist.all_gather(idxs, pi, group=group)
+        offs = [o[: int(s[0])] for o, s in zip(offs, allsz)]
+        idxs = [x[: int(s[1])] for x, s in zip(idxs, allsz)]
+        total = int(allsz[:, 1].sum())
+        full_off = torch.cat(offs + [torch.tensor([total], dtype=torch.int64, device=off.device)])
+        out.append((full_off, torch.cat(idxs)))
+    return out[0], out[1]

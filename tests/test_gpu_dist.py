@@ -1,0 +1,113 @@
+"""GPU tests of the multi-GPU building blocks (mn_dist_bucket / mn_dist_finish) on one B200:
+G "virtual ranks" run one after another on the same device, the all-to-all replaced by slicing
+and concatenating in source-rank order; the concatenated slices must equal the oracle CSR bit for
+bit.  Plus the real torch.distributed NCCL path at world size 1."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import meshgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1604_04689_b200 import build
+    build.build()
+
+
+def _virtual_ranks(conn, et, N, G):
+    import paper_1604_04689_b200 as mn
+    from paper_1604_04689_b200.dist import owner_range
+    M = conn.shape[0]
+    sent = []
+    for r in range(G):
+        s0, s1 = r * M // G, (r + 1) * M // G
+        nk, nc, ep, ec = mn.dist_bucket(conn[s0:s1].contiguous(), et, s0, N, G)
+        # bucket g must hold exactly the pairs owned by rank g
+        nsplit = list(torch.split(nk, nc))
+        esplit = list(torch.split(ep, ec))
+        sent.append((nsplit, esplit))
+    b = mn.node_key_bits(N)
+    node_parts, elem_parts = [], []
+    node_base = elem_base = 0
+    for g in range(G):
+        lo, hi = owner_range(N, G, g)
+        nin = torch.cat([sent[r][0][g] for r in range(G)])
+        ein = torch.cat([sent[r][1][g] for r in range(G)])
+        if nin.numel():
+            own = (nin >> b)
+            assert bool(((own >= lo) & (own < hi)).all())
+        (no, ni), (eo, ei) = mn.dist_finish(nin, ein, N, lo, hi)
+        node_parts.append((no[:-1] + node_base, ni))
+        elem_parts.append((eo[:-1] + elem_base, ei))
+        node_base += ni.numel()
+        elem_base += ei.numel()
+    no = torch.cat([p[0] for p in node_parts] + [torch.tensor([node_base], device="cuda")])
+    ni = torch.cat([p[1] for p in node_parts])
+    eo = torch.cat([p[0] for p in elem_parts] + [torch.tensor([elem_base], device="cuda")])
+    ei = torch.cat([p[1] for p in elem_parts])
+    return (no, ni), (eo, ei)
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 8])
+@pytest.mark.parametrize("name,et,make", [
+    ("kuhn_9", meshgen.TET4, lambda: meshgen.kuhn_tets(9)),
+    ("hex_9_perm", meshgen.HEX8, lambda: (meshgen.relabel(*meshgen.hex_grid(9), 5, 6), 1000)),
+    ("sphere", meshgen.TRI3, lambda: meshgen.uv_sphere(64, 33)),
+    ("quad", meshgen.QUAD4, lambda: meshgen.quad_grid(40, 50)),
+])
+def test_virtual_ranks_match_oracle(G, name, et, make):
+    conn, N = make()
+    (no, ni), (eo, ei) = _virtual_ranks(conn.cuda(), et, N, G)
+    ro, ri = oracle.node_csr(et, conn, N)
+    so, si = oracle.elem_csr(et, conn, N)
+    assert np.array_equal(no.cpu().numpy(), ro) and np.array_equal(ni.cpu().numpy(), ri)
+    assert np.array_equal(eo.cpu().numpy(), so) and np.array_equal(ei.cpu().numpy(), si)
+
+
+def test_virtual_ranks_config5_shape_small():
+    """Config 5's recipe (Kuhn, natural order) at 40^3, 8 ranks: equals the 1-GPU CSR."""
+    import paper_1604_04689_b200 as mn
+    conn, N = meshgen.kuhn_tets(40, device="cuda")
+    ref = mn.find_neighbors(conn, "tet4", N)
+    got = _virtual_ranks(conn, meshgen.TET4, N, 8)
+    for a, b in zip(ref, got):
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_bucket_reports_invalid_with_global_ids():
+    import paper_1604_04689_b200 as mn
+    conn = torch.tensor([[0, 1, 2], [1, 2, 9]], dtype=torch.int32).cuda()
+    with pytest.raises(mn.MeshError) as ei:
+        mn.dist_bucket(conn, "tri3", 1000, 5, 2)
+    assert (ei.value.code, ei.value.elem, ei.value.pos) == (2, 1001, 2)
+
+
+def test_nccl_world_size_one():
+    import torch.distributed as dist
+
+    import paper_1604_04689_b200 as mn
+    from paper_1604_04689_b200.dist import find_neighbors_dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        conn, N = meshgen.kuhn_tets(12, device="cuda")
+        res = find_neighbors_dist(conn, "tet4", 0, N)
+        ref = mn.find_neighbors(conn, "tet4", N)
+        assert (res.lo, res.hi) == (0, N)
+        assert torch.equal(res.node[0], ref[0][0]) and torch.equal(res.node[1], ref[0][1])
+        assert torch.equal(res.elem[0], ref[1][0]) and torch.equal(res.elem[1], ref[1][1])
+    finally:
+        dist.destroy_process_group()

@@ -45,6 +45,8 @@ SMALL = [
     ("fan5", meshgen.TRI3, lambda: meshgen.nonmanifold_fan(5)),
     ("single_tet", meshgen.TET4, lambda: (torch.tensor([[3, 1, 0, 2]], dtype=torch.int32), 4)),
     ("hex_big_ids", meshgen.HEX8, lambda: _perm_hex(9, 77, None)),
+    # > 32 distinct neighbours with <= 256 raw entries: hash-set overflow -> block path
+    ("rand_tet_dense", meshgen.TET4, lambda: meshgen.random_mesh(meshgen.TET4, 900, 120, seed=10)),
 ]
 
 
@@ -190,11 +192,23 @@ def test_whole_path_both(name, et, make):
     _assert_csr((eo, ei), oracle.elem_csr(et, conn, N), name + " elem")
 
 
-@pytest.mark.parametrize("name,et,make", SMALL[:6])
+@pytest.mark.parametrize("name,et,make", SMALL)
 def test_whole_path_single_modes(name, et, make):
     conn, N = make()
-    _assert_csr(mn().find_node_neighbors(conn.cuda(), et, N), oracle.node_csr(et, conn, N), name)
+    exp = oracle.node_csr(et, conn, N)
+    _assert_csr(mn().find_node_neighbors(conn.cuda(), et, N), exp, name)
+    _assert_csr(mn().find_node_neighbors_sortpairs(conn.cuda(), et, N), exp, name + " sortpairs")
     _assert_csr(mn().find_elem_neighbors(conn.cuda(), et, N), oracle.elem_csr(et, conn, N), name)
+
+
+@pytest.mark.parametrize("ntri", [40, 200, 20000, 30000])
+def test_high_valence_fans(ntri):
+    """Node 0 and 1 of a fan see 2*ntri raw pairs: 80 (hash), 400 (block sort in shared memory),
+    40000 (shared memory) and 60000 (in place in global memory) entries."""
+    conn, N = meshgen.nonmanifold_fan(ntri)
+    (no, ni), (eo, ei) = mn().find_neighbors(conn.cuda(), 0, N)
+    _assert_csr((no, ni), oracle.node_csr(0, conn, N), f"fan{ntri}")
+    _assert_csr((eo, ei), oracle.elem_csr(0, conn, N), f"fan{ntri} elem")
 
 
 def test_whole_path_host_buffers():
