@@ -607,6 +607,81 @@ k_node_gather(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx
   }
 }
 
+// Thread-per-node variant (the one the pipeline uses): each thread walks its node's incidences
+// (batched 4 at a time so the element-row gathers overlap), inserts the C neighbours of every
+// incidence into a private open-addressing set in shared memory (column-major, so the 32 lanes of
+// a warp always hit 32 different banks), insertion-sorts the <= kMaxUnique distinct values and
+// writes them to the node's raw region.  Nodes with more distinct neighbours go to k_node_giant.
+constexpr int kNodeThreads = 128;
+constexpr int kHashSlots = 32;
+constexpr int kMaxUnique = 24;
+
+template <int T, bool ALIGNED>
+__global__ void __launch_bounds__(kNodeThreads)
+k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, const int32_t* __restrict__ conn,
+                int64_t N, uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, uint32_t* __restrict__ giants,
+                unsigned int* __restrict__ ngiant, const unsigned long long* __restrict__ err) {
+  constexpr int C = Elem<T>::C, K = Elem<T>::K, B = 4;
+  constexpr uint32_t EMPTY = 0xFFFFFFFFu;
+  __shared__ uint32_t tab[kHashSlots][kNodeThreads];
+  __shared__ uint32_t lst[kMaxUnique + 1][kNodeThreads];
+  if (err && *err != ERR_NONE) return;
+  const int t = threadIdx.x;
+  const int64_t a = (int64_t)blockIdx.x * kNodeThreads + t;
+  if (a >= N) return;
+#pragma unroll
+  for (int i = 0; i < kHashSlots; ++i) tab[i][t] = EMPTY;
+  const int64_t s = eoff[a];
+  const int64_t d = eoff[a + 1] - s;
+  int L = 0;
+  for (int64_t i0 = 0; i0 < d && L <= kMaxUnique; i0 += B) {
+    int e[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) e[q] = (i0 + q < d) ? __ldg(eidx + s + i0 + q) : -1;
+    int row[B][K];
+#pragma unroll
+    for (int q = 0; q < B; ++q)
+      if (e[q] >= 0) load_row<T, ALIGNED>(conn, e[q], row[q]);
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      if (e[q] < 0) continue;
+      const int p = local_of<T>(row[q], (int)a);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const uint32_t v = pick<T>(row[q], nbr_local<T>(p, c));
+        uint32_t h = (v * 0x9E3779B1u) >> 27;
+        while (L <= kMaxUnique) {   // at most kMaxUnique + 1 entries: the set never fills
+          const uint32_t x = tab[h][t];
+          if (x == v) break;
+          if (x == EMPTY) {
+            tab[h][t] = v;
+            lst[L][t] = v;
+            ++L;
+            break;
+          }
+          h = (h + 1) & (kHashSlots - 1);
+        }
+      }
+    }
+  }
+  if (L > kMaxUnique) {
+    giants[atomicAdd(ngiant, 1u)] = (uint32_t)a;
+    return;
+  }
+  for (int i = 1; i < L; ++i) {
+    const uint32_t x = lst[i][t];
+    int j = i - 1;
+    while (j >= 0 && lst[j][t] > x) {
+      lst[j + 1][t] = lst[j][t];
+      --j;
+    }
+    lst[j + 1][t] = x;
+  }
+  uint32_t* out = temp + (size_t)C * s;
+  for (int i = 0; i < L; ++i) out[i] = lst[i][t];
+  cnt[a] = L;
+}
+
 // Nodes with more than 256 raw neighbour entries (or more than 32 distinct neighbours): one CTA per
 // node, the raw entries sorted with a block bitonic network (shared memory when they fit, else in
 // place in the node's global raw region), then adjacent-difference dedupe.

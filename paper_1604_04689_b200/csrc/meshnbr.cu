@@ -552,13 +552,17 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       // ---- a1 + a3n + a4 (nodes): expand the element CSR per node, sort + dedupe per node ----
       uint32_t* temp = ekA;   // C * Pe <= 4 * Pe entries: the dead element-sort buffers
       const double gb = 8.0 * (P.N + 1) + 4.0 * P.Pe + 4.0 * P.K * P.Pe;   // offsets, incidences, rows
-      if (aligned) {
+      if (P.N == 0) {
+        // M > 0 with N == 0 always fails validation: nothing to expand
+      } else if (aligned) {
         MN_CUDA(launch("node_gather", gb, s, [&] {
-          k_node_gather<T, true><<<148 * 8, 32 * kGatherWarps, 0, s>>>(eoff, eidx, conn, P.N, temp, cnt, giants, ngiant, errw);
+          k_node_gather_t<T, true><<<(unsigned)tiles_of(P.N, kNodeThreads), kNodeThreads, 0, s>>>(
+              eoff, eidx, conn, P.N, temp, cnt, giants, ngiant, errw);
         }));
       } else {
         MN_CUDA(launch("node_gather", gb, s, [&] {
-          k_node_gather<T, false><<<148 * 8, 32 * kGatherWarps, 0, s>>>(eoff, eidx, conn, P.N, temp, cnt, giants, ngiant, errw);
+          k_node_gather_t<T, false><<<(unsigned)tiles_of(P.N, kNodeThreads), kNodeThreads, 0, s>>>(
+              eoff, eidx, conn, P.N, temp, cnt, giants, ngiant, errw);
         }));
       }
       const int cap = 48 * 1024;   // uint32 entries sorted in shared memory by k_node_giant (192 KB)
