@@ -49,7 +49,13 @@ __device__ __forceinline__ uint32_t digit_of(KeyT key, const PassDigit& pd, uint
 // k_hist_validate: one thread per element.  Validation (reading R8) + per-digit histograms of the
 // node ids of valid elements.  Histograms are CTA-private in shared memory, flushed once.
 // ================================================================================================
-template <int T, int BINS>
+template <int T, bool ALIGNED>
+__device__ __forceinline__ void load_row(const int32_t* __restrict__ conn, int64_t e, int (&row)[Elem<T>::K]);
+
+// The warp walks 32 consecutive elements per step.  A digit that is the same in all 32 lanes
+// (typical for the high digits of a mesh numbered with spatial locality) is counted with one
+// shared-memory atomic instead of 32 (__reduce_min/max_sync test).
+template <int T, int BINS, bool ALIGNED>
 __global__ void __launch_bounds__(256)
 k_hist_validate(const int32_t* __restrict__ conn, int64_t M, int64_t N, int64_t elem_base,
                 DigitPlan dp, int owner_hist, uint64_t owner_div,
@@ -59,36 +65,62 @@ k_hist_validate(const int32_t* __restrict__ conn, int64_t M, int64_t N, int64_t 
   const int nh = owner_hist ? 1 : dp.nd;
   for (int i = threadIdx.x; i < nh * BINS; i += blockDim.x) sh[i] = 0;
   __syncthreads();
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < M;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < M; base += stride) {
+    const int64_t e = base + lane;
+    const bool in = e < M;
     int v[K];
+    if (in) {
+      load_row<T, ALIGNED>(conn, e, v);
+    } else {
 #pragma unroll
-    for (int p = 0; p < K; ++p) v[p] = __ldg(conn + e * K + p);
-    int bad = -1, kind = 0;
-#pragma unroll
-    for (int p = K - 1; p >= 0; --p)
-      if (v[p] < 0 || (int64_t)v[p] >= N) bad = p;
-    if (bad < 0) {
-#pragma unroll
-      for (int p = K - 1; p >= 1; --p) {
-        bool dup = false;
-#pragma unroll
-        for (int q = 0; q < p; ++q) dup |= (v[q] == v[p]);
-        if (dup) { bad = p; kind = 1; }
-      }
+      for (int p = 0; p < K; ++p) v[p] = 0;
     }
-    if (bad >= 0) {
-      atomicMin(err, (unsigned long long)err_encode((uint64_t)(elem_base + e), kind, bad));
+    int bad = -1, kind = 0;
+    if (in) {
+#pragma unroll
+      for (int p = K - 1; p >= 0; --p)
+        if (v[p] < 0 || (int64_t)v[p] >= N) bad = p;
+      if (bad < 0) {
+#pragma unroll
+        for (int p = K - 1; p >= 1; --p) {
+          bool dup = false;
+#pragma unroll
+          for (int q = 0; q < p; ++q) dup |= (v[q] == v[p]);
+          if (dup) { bad = p; kind = 1; }
+        }
+      }
+      if (bad >= 0) atomicMin(err, (unsigned long long)err_encode((uint64_t)(elem_base + e), kind, bad));
+    }
+    const bool ok = in && bad < 0;
+    const unsigned okm = __ballot_sync(FULL, ok);
+    if (owner_hist) {
+      if (ok) {
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          const uint64_t d = (uint64_t)v[p] / owner_div;
+          atomicAdd(&sh[d < BINS ? d : BINS - 1], 1u);
+        }
+      }
       continue;
     }
 #pragma unroll
-    for (int p = 0; p < K; ++p) {
-      if (owner_hist) {
-        uint64_t d = (uint64_t)v[p] / owner_div;
-        atomicAdd(&sh[d < BINS ? d : BINS - 1], 1u);
-      } else {
-        for (int j = 0; j < dp.nd; ++j)
-          atomicAdd(&sh[j * BINS + (((uint32_t)v[p] >> dp.shift[j]) & ((1u << dp.width[j]) - 1))], 1u);
+    for (int j = 0; j < 4; ++j) {
+      if (j >= dp.nd) break;
+      const int sh_j = dp.shift[j];
+      const uint32_t mk = (1u << dp.width[j]) - 1u;
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        const uint32_t dg = ((uint32_t)v[p] >> sh_j) & mk;
+        if (okm == FULL) {
+          const uint32_t lo = __reduce_min_sync(FULL, dg), hi = __reduce_max_sync(FULL, dg);
+          if (lo == hi) {
+            if (lane == 0) atomicAdd(&sh[j * BINS + lo], 32u);
+            continue;
+          }
+        }
+        if (ok) atomicAdd(&sh[j * BINS + dg], 1u);
       }
     }
   }
@@ -745,24 +777,31 @@ k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx,
   }
 }
 
-// Node CSR indices: copy each node's sorted unique list to its final offset (warp per 32 nodes).
+// Node CSR indices: a CTA per 256 consecutive nodes writes its contiguous output range
+// [noff[a0], noff[a0+256]) with consecutive threads on consecutive positions; the node of each
+// position is found by binary search over the CTA's 256 offsets in shared memory.
 __global__ void __launch_bounds__(256)
 k_node_compact(const int64_t* __restrict__ eoff, int C, const uint32_t* __restrict__ temp,
                const int64_t* __restrict__ noff, int64_t N, int32_t* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t a0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; a0 < N; a0 += nw * 32) {
-    const int64_t a = a0 + lane;
-    int64_t src = 0, dst = 0, u = 0;
-    if (a < N) {
-      src = (int64_t)C * eoff[a];
-      dst = noff[a];
-      u = noff[a + 1] - dst;
+  __shared__ int64_t s_src[256];
+  __shared__ int64_t s_dst[257];
+  const int64_t a0 = (int64_t)blockIdx.x * 256;
+  const int t = threadIdx.x;
+  const int nloc = (int)(N - a0 < 256 ? N - a0 : 256);
+  if (t < nloc) {
+    s_src[t] = (int64_t)C * eoff[a0 + t];
+    s_dst[t] = noff[a0 + t];
+  }
+  if (t == 0) s_dst[nloc] = noff[a0 + nloc];
+  __syncthreads();
+  const int64_t o0 = s_dst[0], o1 = s_dst[nloc];
+  for (int64_t o = o0 + t; o < o1; o += 256) {
+    int lo = 0, hi = nloc - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_dst[mid] <= o) lo = mid; else hi = mid - 1;
     }
-    for (int j = 0; j < 32; ++j) {
-      const int64_t sj = __shfl_sync(FULL, src, j), dj = __shfl_sync(FULL, dst, j), uj = __shfl_sync(FULL, u, j);
-      for (int64_t i = lane; i < uj; i += 32) out[dj + i] = (int32_t)temp[sj + i];
-    }
+    out[o] = (int32_t)temp[s_src[lo] + (o - s_dst[lo])];
   }
 }
 
@@ -770,17 +809,33 @@ k_node_compact(const int64_t* __restrict__ eoff, int C, const uint32_t* __restri
 // k_elem_offsets: offsets from the stably sorted element-pair keys (no dedupe needed: (node,
 // element) pairs are unique once the input is validated).
 // ================================================================================================
+template <bool ALIGNED>
 __global__ void __launch_bounds__(256)
 k_elem_offsets(const uint32_t* __restrict__ keys, int64_t n, int64_t N, int64_t* __restrict__ offsets,
                const unsigned long long* __restrict__ err) {
   if (err && *err != ERR_NONE) return;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = keys[i];
-    const int64_t pk = i == 0 ? -1 : (int64_t)keys[i - 1];
-    for (int64_t x = pk + 1; x <= k; ++x) offsets[x] = i;
-    if (i == n - 1)
-      for (int64_t x = k + 1; x <= N; ++x) offsets[x] = n;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 4 * q < n; q += stride) {
+    const int64_t i0 = 4 * q;
+    uint32_t k[4];
+    if (ALIGNED && i0 + 3 < n) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(keys) + q);
+      k[0] = x.x; k[1] = x.y; k[2] = x.z; k[3] = x.w;
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) k[r] = (i0 + r < n) ? __ldg(keys + i0 + r) : 0u;
+    }
+    int64_t prev = i0 == 0 ? -1 : (int64_t)__ldg(keys + i0 - 1);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t i = i0 + r;
+      if (i >= n) break;
+      const int64_t cur = k[r];
+      for (int64_t x = prev + 1; x <= cur; ++x) offsets[x] = i;
+      prev = cur;
+      if (i == n - 1)
+        for (int64_t x = cur + 1; x <= N; ++x) offsets[x] = n;
+    }
   }
 }
 

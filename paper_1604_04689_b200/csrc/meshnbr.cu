@@ -288,7 +288,10 @@ static mn_status pipeline(const Plan& P, const int32_t* conn, Mem& mem, bool wan
 
     // ---- a1/a2: validate + histograms ----
     MN_CUDA(launch("hist_validate", 4.0 * P.K * P.M, s, [&] {
-      k_hist_validate<T, BINS><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, 0, P.dp, 0, 1, hist, errw);
+      if (((uintptr_t)conn & 15) == 0)
+        k_hist_validate<T, BINS, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, 0, P.dp, 0, 1, hist, errw);
+      else
+        k_hist_validate<T, BINS, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, 0, P.dp, 0, 1, hist, errw);
     }));
     BasesDesc bd{};
     bd.npass = npass;
@@ -375,7 +378,7 @@ static mn_status pipeline(const Plan& P, const int32_t* conn, Mem& mem, bool wan
         vin = vb[q & 1];
       }
       MN_CUDA(launch("elem_offsets", 4.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
-        k_elem_offsets<<<stream_grid(P.Pe), 256, 0, s>>>(kin, P.Pe, P.N, elem_off, errw);
+        k_elem_offsets<false><<<stream_grid(P.Pe / 4 + 1), 256, 0, s>>>(kin, P.Pe, P.N, elem_off, errw);
       }));
     }
 
@@ -481,10 +484,11 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       status = a.take<uint64_t>((size_t)elem_tiles * BINS);
       sstatus = a.take<uint64_t>((size_t)(scan_tiles ? scan_tiles : 1));
       head = a.off;
-      ekA = a.take<uint32_t>(4 * (size_t)P.Pe);   // ekA | ekB | epA | epB; later the node raw region
-      ekB = ekA + P.Pe;
-      epA = ekA + 2 * P.Pe;
-      epB = ekA + 3 * P.Pe;
+      // ekA | ekB | epA | epB (each 256-byte aligned, contiguous); later the node raw region
+      ekA = a.take<uint32_t>((size_t)P.Pe);
+      ekB = a.take<uint32_t>((size_t)P.Pe);
+      epA = a.take<uint32_t>((size_t)P.Pe);
+      epB = a.take<uint32_t>((size_t)P.Pe);
       if (want_node) {
         cnt = a.take<int32_t>((size_t)P.N);
         giants = a.take<uint32_t>((size_t)(giant_cap ? giant_cap : 1));
@@ -508,7 +512,10 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
 
     // ---- a1/a2 validation + digit histograms of the node ids ----
     MN_CUDA(launch("hist_validate", 4.0 * P.K * P.M, s, [&] {
-      k_hist_validate<T, BINS><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, 0, P.dp, 0, 1, hist, errw);
+      if (((uintptr_t)conn & 15) == 0)
+        k_hist_validate<T, BINS, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, 0, P.dp, 0, 1, hist, errw);
+      else
+        k_hist_validate<T, BINS, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, 0, P.dp, 0, 1, hist, errw);
     }));
     BasesDesc bd{};
     bd.npass = nd;
@@ -544,7 +551,10 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     }
     // ---- a4 + a5 (elements): run starts of the sorted node keys -> offsets ----
     MN_CUDA(launch("elem_offsets", 4.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
-      k_elem_offsets<<<stream_grid(P.Pe), 256, 0, s>>>(kin, P.Pe, P.N, eoff, errw);
+      if (((uintptr_t)kin & 15) == 0)
+        k_elem_offsets<true><<<stream_grid(P.Pe / 4 + 1), 256, 0, s>>>(kin, P.Pe, P.N, eoff, errw);
+      else
+        k_elem_offsets<false><<<stream_grid(P.Pe / 4 + 1), 256, 0, s>>>(kin, P.Pe, P.N, eoff, errw);
     }));
 
     int64_t U = 0;
@@ -595,7 +605,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       if (U && !out) { st = MN_ERR_OOM; goto done; }
       if (U) {
         MN_CUDA(launch("node_compact", 8.0 * U + 24.0 * P.N, s, [&] {
-          k_node_compact<<<stream_grid(P.N / 8 + 1), 256, 0, s>>>(eoff, P.C, ekA, node_off, P.N, out);
+          k_node_compact<<<(unsigned)tiles_of(P.N, 256), 256, 0, s>>>(eoff, P.C, ekA, node_off, P.N, out);
         }));
       }
       node_out->num_nodes = P.N;
@@ -805,7 +815,7 @@ static mn_status emit_stage(const int32_t* conn, int64_t M, int64_t N, void* key
   MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
   if (M > 0) {
     MN_CUDA(launch("hist_validate", 4.0 * P.K * M, s, [&] {
-      k_hist_validate<T, 512><<<hist_grid(M), 256, 0, s>>>(conn, M, N, 0, P.dp, 0, 1, hist, errw);
+      k_hist_validate<T, 512, false><<<hist_grid(M), 256, 0, s>>>(conn, M, N, 0, P.dp, 0, 1, hist, errw);
     }));
     if (node) {
       if (P.key64) {
@@ -865,7 +875,7 @@ static mn_status dist_bucket_impl(const int32_t* conn, int64_t M, int64_t base, 
     MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
     if (M > 0) {
       MN_CUDA(launch("hist_validate", 4.0 * P.K * M, s, [&] {
-        k_hist_validate<T, BINS><<<hist_grid(M), 256, 0, s>>>(conn, M, N, base, P.dp, 1, chunk, hist, errw);
+        k_hist_validate<T, BINS, false><<<hist_grid(M), 256, 0, s>>>(conn, M, N, base, P.dp, 1, chunk, hist, errw);
       }));
       BasesDesc bd{};
       bd.npass = 2;
@@ -1078,7 +1088,7 @@ mn_status mn_elem_offsets(const uint32_t* d_sorted_keys, int64_t n, int64_t N, i
   cudaStream_t s = (cudaStream_t)stream;
   if (n == 0) return cudaMemsetAsync(d_offsets, 0, (size_t)(N + 1) * 8, s) == cudaSuccess ? MN_OK : MN_ERR_CUDA;
   cudaError_t e = launch("elem_offsets", 4.0 * n + 8.0 * (N + 1), s, [&] {
-    k_elem_offsets<<<stream_grid(n), 256, 0, s>>>(d_sorted_keys, n, N, d_offsets, nullptr);
+    k_elem_offsets<false><<<stream_grid(n / 4 + 1), 256, 0, s>>>(d_sorted_keys, n, N, d_offsets, nullptr);
   });
   return e == cudaSuccess ? MN_OK : MN_ERR_CUDA;
 }
