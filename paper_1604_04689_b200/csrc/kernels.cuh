@@ -213,8 +213,28 @@ struct OnesweepSmem {
   uint32_t tile;
 };
 
+// Peer mask of lanes holding the same digit.  RANK 0: __match_any_sync.  RANK 1: one ballot per
+// digit bit (vote unit only, no scoreboard wait).  RANK 2: RANK 1 behind a warp-uniform test.
+template <int RANK, int BINS>
+__device__ __forceinline__ unsigned digit_peers(uint32_t d) {
+  constexpr int RB = BINS >= 512 ? 9 : 8;
+  if (RANK == 0) return __match_any_sync(FULL, d);
+  if (RANK == 2) {
+    const uint32_t d0 = __shfl_sync(FULL, d, 0);
+    if (__all_sync(FULL, d == d0)) return FULL;
+  }
+  unsigned peers = FULL;
+#pragma unroll
+  for (int bit = 0; bit < RB; ++bit) {
+    const bool set = (d >> bit) & 1u;
+    const unsigned bal = __ballot_sync(FULL, set);
+    peers &= set ? bal : ~bal;
+  }
+  return peers;
+}
+
 template <typename KeyT, int SRC, int T, bool PAYLOAD, bool OWNER, int BINS, int THREADS, int ITEMS,
-          int W = 4, int MINB = 3>
+          int W = 4, int MINB = 3, int RANK = 0>
 __global__ void __launch_bounds__(THREADS, MINB)
 k_onesweep(PassArgs pa) {
   constexpr int WARPS = THREADS / 32;
@@ -274,19 +294,42 @@ k_onesweep(PassArgs pa) {
 
   // ---- rank: per-warp running digit histogram, warp-match aggregated; dr = digit | rank << 16 ----
   uint32_t dr[ITEMS];
+  if (RANK == 3) {
+    // all MATCHes first (independent, pipelined), then the per-warp histogram chain
+    unsigned pm[ITEMS];
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int64_t idx = chunk + i * 32 + lane;
-    const uint32_t d = idx < pa.n ? digit_of<KeyT, OWNER>(key[i], pa.pd, BINS - 1) : (uint32_t)(BINS - 1);
-    const unsigned peers = __match_any_sync(FULL, d);
-    const int leader = __ffs(peers) - 1;
-    uint32_t old = 0;
-    if (lane == leader) {
-      old = sm.whist[warp][d];
-      sm.whist[warp][d] = old + __popc(peers);
+    for (int i = 0; i < ITEMS; ++i) {
+      const int64_t idx = chunk + i * 32 + lane;
+      dr[i] = idx < pa.n ? digit_of<KeyT, OWNER>(key[i], pa.pd, BINS - 1) : (uint32_t)(BINS - 1);
+      pm[i] = __match_any_sync(FULL, dr[i]);
     }
-    old = __shfl_sync(FULL, old, leader);
-    dr[i] = d | ((old + __popc(peers & lanemask_lt())) << 16);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t d = dr[i];
+      const int leader = __ffs(pm[i]) - 1;
+      uint32_t old = 0;
+      if (lane == leader) {
+        old = sm.whist[warp][d];
+        sm.whist[warp][d] = old + __popc(pm[i]);
+      }
+      old = __shfl_sync(FULL, old, leader);
+      dr[i] = d | ((old + __popc(pm[i] & lanemask_lt())) << 16);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int64_t idx = chunk + i * 32 + lane;
+      const uint32_t d = idx < pa.n ? digit_of<KeyT, OWNER>(key[i], pa.pd, BINS - 1) : (uint32_t)(BINS - 1);
+      const unsigned peers = digit_peers<RANK, BINS>(d);
+      const int leader = __ffs(peers) - 1;
+      uint32_t old = 0;
+      if (lane == leader) {
+        old = sm.whist[warp][d];
+        sm.whist[warp][d] = old + __popc(peers);
+      }
+      old = __shfl_sync(FULL, old, leader);
+      dr[i] = d | ((old + __popc(peers & lanemask_lt())) << 16);
+    }
   }
   __syncthreads();
 
@@ -331,7 +374,10 @@ k_onesweep(PassArgs pa) {
 #pragma unroll
     for (int j = 0; j < BPT; ++j) {
       binst[j] = run;
-      if (own) sm.binstart[tid * BPT + j] = run;
+      if (own) {
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) sm.whist[w][tid * BPT + j] += run;   // fold the tile-local start
+      }
       run += cnt[j];
     }
   }
@@ -341,7 +387,7 @@ k_onesweep(PassArgs pa) {
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const uint32_t d = dr[i] & 0xFFFFu;
-    const uint32_t pos = sm.binstart[d] + sm.whist[warp][d] + (dr[i] >> 16);
+    const uint32_t pos = sm.whist[warp][d] + (dr[i] >> 16);
     if (pos < (uint32_t)nvalid) {
       skeys[pos] = key[i];
       if (PAYLOAD || SRC == 2) svals[pos] = val[i];
