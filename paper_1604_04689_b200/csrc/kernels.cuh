@@ -113,10 +113,10 @@ k_hist_validate(const int32_t* __restrict__ conn, int64_t M, int64_t N, int64_t 
 #pragma unroll
       for (int p = 0; p < K; ++p) {
         const uint32_t dg = ((uint32_t)v[p] >> sh_j) & mk;
-        if (okm == FULL) {
-          const uint32_t lo = __reduce_min_sync(FULL, dg), hi = __reduce_max_sync(FULL, dg);
-          if (lo == hi) {
-            if (lane == 0) atomicAdd(&sh[j * BINS + lo], 32u);
+        if (j > 0 && okm == FULL) {   // the lowest digit is practically never warp-uniform
+          const uint32_t d0 = __shfl_sync(FULL, dg, 0);
+          if (__all_sync(FULL, dg == d0)) {
+            if (lane == 0) atomicAdd(&sh[j * BINS + d0], 32u);
             continue;
           }
         }
@@ -201,6 +201,7 @@ struct PassArgs {
   uint32_t* ticket;
   uint32_t epoch;
   const unsigned long long* err;
+  int32_t* counts;         // COUNTS mode: per-key run lengths (last element pass)
 };
 
 template <int THREADS, int ITEMS, int BINS>
@@ -233,8 +234,12 @@ __device__ __forceinline__ unsigned digit_peers(uint32_t d) {
   return peers;
 }
 
+// COUNTS (last pass of the element sort): the sorted keys are not written; instead each run of
+// equal keys inside the tile adds its length to counts[key] with two atomics (+end+1 at the run's
+// last slot, -start at its first), so counts[] ends as the per-node incidence counts whose
+// exclusive scan is the element-CSR offsets.
 template <typename KeyT, int SRC, int T, bool PAYLOAD, bool OWNER, int BINS, int THREADS, int ITEMS,
-          int W = 4, int MINB = 3, int RANK = 0>
+          int W = 4, int MINB = 3, int RANK = 0, bool COUNTS = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 k_onesweep(PassArgs pa) {
   constexpr int WARPS = THREADS / 32;
@@ -420,8 +425,12 @@ k_onesweep(PassArgs pa) {
     if (li < nvalid) {
       const KeyT k = skeys[li];
       const uint64_t g = sm.gofs[digit_of<KeyT, OWNER>(k, pa.pd, BINS - 1)] + li;
-      kout[g] = k;
+      if (!COUNTS) kout[g] = k;
       if (PAYLOAD || SRC == 2) pa.vals_out[g] = svals[li];
+      if (COUNTS) {
+        if (li == 0 || skeys[li - 1] != k) atomicAdd(pa.counts + k, -li);
+        if (li == nvalid - 1 || skeys[li + 1] != k) atomicAdd(pa.counts + k, li + 1);
+      }
     }
   }
 }
@@ -697,52 +706,76 @@ constexpr int kMaxUnique = 24;
 template <int T, bool ALIGNED>
 __global__ void __launch_bounds__(kNodeThreads)
 k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, const int32_t* __restrict__ conn,
-                int64_t N, uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, uint32_t* __restrict__ giants,
-                unsigned int* __restrict__ ngiant, const unsigned long long* __restrict__ err) {
+                int64_t N, uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, int32_t* __restrict__ lofs,
+                uint32_t* __restrict__ giants, unsigned int* __restrict__ ngiant,
+                const unsigned long long* __restrict__ err) {
   constexpr int C = Elem<T>::C, K = Elem<T>::K, B = 4;
   constexpr uint32_t EMPTY = 0xFFFFFFFFu;
   __shared__ uint32_t tab[kHashSlots][kNodeThreads];
   __shared__ uint32_t lst[kMaxUnique + 1][kNodeThreads];
+  __shared__ uint32_t s_wsum[kNodeThreads / 32];
   if (err && *err != ERR_NONE) return;
-  const int t = threadIdx.x;
-  const int64_t a = (int64_t)blockIdx.x * kNodeThreads + t;
-  if (a >= N) return;
-#pragma unroll
-  for (int i = 0; i < kHashSlots; ++i) tab[i][t] = EMPTY;
-  const int64_t s = eoff[a];
-  const int64_t d = eoff[a + 1] - s;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t n0 = (int64_t)blockIdx.x * kNodeThreads;
+  const int64_t a = n0 + t;
+  const bool valid = a < N;
   int L = 0;
-  for (int64_t i0 = 0; i0 < d && L <= kMaxUnique; i0 += B) {
-    int e[B];
+  int64_t raw = 0;
+  if (valid) {
 #pragma unroll
-    for (int q = 0; q < B; ++q) e[q] = (i0 + q < d) ? __ldg(eidx + s + i0 + q) : -1;
-    int row[B][K];
+    for (int i = 0; i < kHashSlots; ++i) tab[i][t] = EMPTY;
+    const int64_t s = eoff[a];
+    const int64_t d = eoff[a + 1] - s;
+    raw = (int64_t)C * d;
+    for (int64_t i0 = 0; i0 < d && L <= kMaxUnique; i0 += B) {
+      int e[B];
 #pragma unroll
-    for (int q = 0; q < B; ++q)
-      if (e[q] >= 0) load_row<T, ALIGNED>(conn, e[q], row[q]);
+      for (int q = 0; q < B; ++q) e[q] = (i0 + q < d) ? __ldg(eidx + s + i0 + q) : -1;
+      int row[B][K];
 #pragma unroll
-    for (int q = 0; q < B; ++q) {
-      if (e[q] < 0) continue;
-      const int p = local_of<T>(row[q], (int)a);
+      for (int q = 0; q < B; ++q)
+        if (e[q] >= 0) load_row<T, ALIGNED>(conn, e[q], row[q]);
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const uint32_t v = pick<T>(row[q], nbr_local<T>(p, c));
-        uint32_t h = (v * 0x9E3779B1u) >> 27;
-        while (L <= kMaxUnique) {   // at most kMaxUnique + 1 entries: the set never fills
-          const uint32_t x = tab[h][t];
-          if (x == v) break;
-          if (x == EMPTY) {
-            tab[h][t] = v;
-            lst[L][t] = v;
-            ++L;
-            break;
+      for (int q = 0; q < B; ++q) {
+        if (e[q] < 0) continue;
+        const int p = local_of<T>(row[q], (int)a);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const uint32_t v = pick<T>(row[q], nbr_local<T>(p, c));
+          uint32_t h = (v * 0x9E3779B1u) >> 27;
+          while (L <= kMaxUnique) {   // at most kMaxUnique + 1 entries: the set never fills
+            const uint32_t x = tab[h][t];
+            if (x == v) break;
+            if (x == EMPTY) {
+              tab[h][t] = v;
+              lst[L][t] = v;
+              ++L;
+              break;
+            }
+            h = (h + 1) & (kHashSlots - 1);
           }
-          h = (h + 1) & (kHashSlots - 1);
         }
       }
     }
   }
-  if (L > kMaxUnique) {
+  const bool giant = valid && L > kMaxUnique;
+  // ---- dense per-CTA layout: node lists packed from C * eoff[n0]; a giant reserves raw slots ----
+  const uint32_t size = valid ? (giant ? (uint32_t)raw : (uint32_t)L) : 0u;
+  uint32_t incl = size;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  uint32_t excl = incl - size;
+#pragma unroll
+  for (int w = 0; w < kNodeThreads / 32; ++w)
+    if (w < warp) excl += s_wsum[w];
+  if (!valid) return;
+  lofs[a] = (int32_t)excl;
+  if (giant) {
     giants[atomicAdd(ngiant, 1u)] = (uint32_t)a;
     return;
   }
@@ -755,7 +788,7 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
     }
     lst[j + 1][t] = x;
   }
-  uint32_t* out = temp + (size_t)C * s;
+  uint32_t* out = temp + (size_t)C * eoff[n0] + excl;
   for (int i = 0; i < L; ++i) out[i] = lst[i][t];
   cnt[a] = L;
 }
@@ -766,8 +799,9 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
 template <int T, bool ALIGNED>
 __global__ void __launch_bounds__(1024)
 k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, const int32_t* __restrict__ conn,
-             uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, const uint32_t* __restrict__ giants,
-             const unsigned int* __restrict__ ngiant, int smem_cap, const unsigned long long* __restrict__ err) {
+             uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, const int32_t* __restrict__ lofs,
+             const uint32_t* __restrict__ giants, const unsigned int* __restrict__ ngiant, int smem_cap,
+             const unsigned long long* __restrict__ err) {
   constexpr int C = Elem<T>::C, K = Elem<T>::K;
   extern __shared__ uint32_t sv[];
   __shared__ int s_u;
@@ -778,7 +812,8 @@ k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx,
     const int64_t s = eoff[a];
     const int64_t d = eoff[a + 1] - s;
     const int64_t raw = (int64_t)C * d;
-    uint32_t* out = temp + (size_t)C * s;
+    // the slot reserved by k_node_gather_t: raw entries at chunk base + lofs[a]
+    uint32_t* out = temp + (size_t)C * eoff[(a / kNodeThreads) * kNodeThreads] + lofs[a];
     uint32_t* buf = raw <= smem_cap ? sv : out;
     for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
       int row[K];
@@ -823,25 +858,34 @@ k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx,
   }
 }
 
-// Node CSR indices: a CTA per 256 consecutive nodes writes its contiguous output range
-// [noff[a0], noff[a0+256]) with consecutive threads on consecutive positions; the node of each
-// position is found by binary search over the CTA's 256 offsets in shared memory.
-__global__ void __launch_bounds__(256)
+// Node CSR indices: a CTA per kNodeThreads-node chunk (the same chunks as k_node_gather_t, whose
+// lists are packed from C * eoff[n0]) writes its contiguous output range with consecutive threads
+// on consecutive positions; the node of each position is found by binary search in shared memory.
+__global__ void __launch_bounds__(kNodeThreads)
 k_node_compact(const int64_t* __restrict__ eoff, int C, const uint32_t* __restrict__ temp,
-               const int64_t* __restrict__ noff, int64_t N, int32_t* __restrict__ out) {
-  __shared__ int64_t s_src[256];
-  __shared__ int64_t s_dst[257];
-  const int64_t a0 = (int64_t)blockIdx.x * 256;
+               const int32_t* __restrict__ lofs, const int64_t* __restrict__ noff, int64_t N,
+               int32_t* __restrict__ out) {
+  __shared__ int64_t s_src[kNodeThreads];
+  __shared__ int64_t s_dst[kNodeThreads + 1];
+  const int64_t n0 = (int64_t)blockIdx.x * kNodeThreads;
   const int t = threadIdx.x;
-  const int nloc = (int)(N - a0 < 256 ? N - a0 : 256);
+  const int nloc = (int)(N - n0 < kNodeThreads ? N - n0 : kNodeThreads);
+  const int64_t base = (int64_t)C * eoff[n0];
   if (t < nloc) {
-    s_src[t] = (int64_t)C * eoff[a0 + t];
-    s_dst[t] = noff[a0 + t];
+    s_src[t] = base + lofs[n0 + t];
+    s_dst[t] = noff[n0 + t];
   }
-  if (t == 0) s_dst[nloc] = noff[a0 + nloc];
+  if (t == 0) s_dst[nloc] = noff[n0 + nloc];
   __syncthreads();
   const int64_t o0 = s_dst[0], o1 = s_dst[nloc];
-  for (int64_t o = o0 + t; o < o1; o += 256) {
+  // without a giant in the chunk the packed source layout equals the destination layout
+  const bool packed = __syncthreads_and(t >= nloc || s_src[t] - base == s_dst[t] - o0);
+  if (packed) {
+    const uint32_t* src = temp + base - o0;
+    for (int64_t o = o0 + t; o < o1; o += kNodeThreads) out[o] = (int32_t)src[o];
+    return;
+  }
+  for (int64_t o = o0 + t; o < o1; o += kNodeThreads) {
     int lo = 0, hi = nloc - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;

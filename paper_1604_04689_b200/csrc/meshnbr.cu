@@ -175,14 +175,15 @@ static int stream_grid(int64_t n) {
 // ================================================================================================
 // one onesweep pass
 // ================================================================================================
-template <typename KeyT, int SRC, int T, bool PAYLOAD, bool OWNER, int BINS>
+template <typename KeyT, int SRC, int T, bool PAYLOAD, bool OWNER, int BINS, bool COUNTS = false>
 static cudaError_t run_pass(PassArgs pa, cudaStream_t s, const char* name, double bytes) {
   using Sm = OnesweepSmem<kPassThreads, kPassItems, BINS>;
   const int64_t tiles = tiles_of(pa.n, kTile);
   if (tiles == 0) return cudaSuccess;
   const size_t smem = ((sizeof(Sm) + 15) & ~size_t(15)) + (size_t)kTile * sizeof(KeyT) +
                       ((PAYLOAD || SRC == 2) ? (size_t)kTile * 4 : 0);
-  auto kern = k_onesweep<KeyT, SRC, T, PAYLOAD, OWNER, BINS, kPassThreads, kPassItems, kPassWindow, kPassMinBlocks>;
+  auto kern = k_onesweep<KeyT, SRC, T, PAYLOAD, OWNER, BINS, kPassThreads, kPassItems, kPassWindow, kPassMinBlocks,
+                         0, COUNTS>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -472,7 +473,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     uint32_t *tickets = nullptr, *ekA = nullptr, *ekB = nullptr, *epA = nullptr, *epB = nullptr, *giants = nullptr;
     unsigned int* ngiant = nullptr;
     uint64_t *bases = nullptr, *status = nullptr, *sstatus = nullptr;
-    int32_t* cnt = nullptr;
+    int32_t *cnt = nullptr, *ecnt = nullptr, *lofs = nullptr;
     int64_t* eoff = elem_off;
     int32_t* eidx = elem_idx;
     auto layout = [&](Arena& a) {
@@ -483,6 +484,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       bases = a.take<uint64_t>((size_t)nd * BINS);
       status = a.take<uint64_t>((size_t)elem_tiles * BINS);
       sstatus = a.take<uint64_t>((size_t)(scan_tiles ? scan_tiles : 1));
+      ecnt = a.take<int32_t>((size_t)P.N + 1);   // per-node incidence counts (atomics in the last pass)
       head = a.off;
       // ekA | ekB | epA | epB (each 256-byte aligned, contiguous); later the node raw region
       ekA = a.take<uint32_t>((size_t)P.Pe);
@@ -491,6 +493,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       epB = a.take<uint32_t>((size_t)P.Pe);
       if (want_node) {
         cnt = a.take<int32_t>((size_t)P.N);
+        lofs = a.take<int32_t>((size_t)P.N);
         giants = a.take<uint32_t>((size_t)(giant_cap ? giant_cap : 1));
         if (!want_elem) {
           eoff = a.take<int64_t>((size_t)P.N + 1);
@@ -527,12 +530,15 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     uint32_t* vb[2] = {epA, epB};
     const uint32_t* kin = nullptr;
     const uint32_t* vin = nullptr;
+    // The last pass writes only the payloads (the element-CSR indices, in place) and adds each
+    // node's run lengths to ecnt (a4: reduction of the ones array).
     for (int q = 0; q < nd; ++q) {
+      const bool last = q == nd - 1;
       PassArgs pa{};
       pa.keys_in = kin;
       pa.vals_in = vin;
-      pa.keys_out = kb[q & 1];
-      pa.vals_out = (q == nd - 1) ? reinterpret_cast<uint32_t*>(eidx) : vb[q & 1];
+      pa.keys_out = last ? nullptr : kb[q & 1];
+      pa.vals_out = last ? reinterpret_cast<uint32_t*>(eidx) : vb[q & 1];
       pa.conn = conn;
       pa.n = P.Pe;
       pa.pd = mask_digit(P.dp.shift[q], P.dp.width[q]);
@@ -541,21 +547,25 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       pa.ticket = tickets + q;
       pa.epoch = (uint32_t)(q + 1);
       pa.err = errw;
-      if (q == 0) {
-        MN_CUDA((run_pass<uint32_t, 2, T, false, false, BINS>(pa, s, "onesweep_elem_first", 4.0 * P.Pe + 8.0 * P.Pe)));
-      } else {
+      pa.counts = ecnt;
+      if (q == 0 && !last) {
+        MN_CUDA((run_pass<uint32_t, 2, T, false, false, BINS>(pa, s, "onesweep_elem_first", 12.0 * P.Pe)));
+      } else if (q == 0) {
+        MN_CUDA((run_pass<uint32_t, 2, T, false, false, BINS, true>(pa, s, "onesweep_elem_first", 8.0 * P.Pe)));
+      } else if (!last) {
         MN_CUDA((run_pass<uint32_t, 0, 0, true, false, BINS>(pa, s, "onesweep_elem", 16.0 * P.Pe)));
+      } else {
+        MN_CUDA((run_pass<uint32_t, 0, 0, true, false, BINS, true>(pa, s, "onesweep_elem_last", 12.0 * P.Pe)));
       }
       kin = kb[q & 1];
       vin = vb[q & 1];
     }
-    // ---- a4 + a5 (elements): run starts of the sorted node keys -> offsets ----
-    MN_CUDA(launch("elem_offsets", 4.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
-      if (((uintptr_t)kin & 15) == 0)
-        k_elem_offsets<true><<<stream_grid(P.Pe / 4 + 1), 256, 0, s>>>(kin, P.Pe, P.N, eoff, errw);
-      else
-        k_elem_offsets<false><<<stream_grid(P.Pe / 4 + 1), 256, 0, s>>>(kin, P.Pe, P.N, eoff, errw);
-    }));
+    // ---- a5 (elements): exclusive scan of the per-node counts -> offsets ----
+    if (P.N > 0)
+      MN_CUDA(launch("scan_counts", 4.0 * P.N + 8.0 * (P.N + 1), s, [&] {
+        k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(ecnt, P.N, eoff, sstatus,
+                                                                                 tickets + 29, 1);
+      }));
 
     int64_t U = 0;
     if (want_node) {
@@ -567,12 +577,12 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       } else if (aligned) {
         MN_CUDA(launch("node_gather", gb, s, [&] {
           k_node_gather_t<T, true><<<(unsigned)tiles_of(P.N, kNodeThreads), kNodeThreads, 0, s>>>(
-              eoff, eidx, conn, P.N, temp, cnt, giants, ngiant, errw);
+              eoff, eidx, conn, P.N, temp, cnt, lofs, giants, ngiant, errw);
         }));
       } else {
         MN_CUDA(launch("node_gather", gb, s, [&] {
           k_node_gather_t<T, false><<<(unsigned)tiles_of(P.N, kNodeThreads), kNodeThreads, 0, s>>>(
-              eoff, eidx, conn, P.N, temp, cnt, giants, ngiant, errw);
+              eoff, eidx, conn, P.N, temp, cnt, lofs, giants, ngiant, errw);
         }));
       }
       const int cap = 48 * 1024;   // uint32 entries sorted in shared memory by k_node_giant (192 KB)
@@ -583,14 +593,14 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
         giant_attr = true;
       }
       MN_CUDA(launch("node_giant", 0.0, s, [&] {
-        if (aligned) k_node_giant<T, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, conn, temp, cnt, giants, ngiant, cap, errw);
-        else k_node_giant<T, false><<<148, 1024, cap * 4, s>>>(eoff, eidx, conn, temp, cnt, giants, ngiant, cap, errw);
+        if (aligned) k_node_giant<T, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, conn, temp, cnt, lofs, giants, ngiant, cap, errw);
+        else k_node_giant<T, false><<<148, 1024, cap * 4, s>>>(eoff, eidx, conn, temp, cnt, lofs, giants, ngiant, cap, errw);
       }));
       // ---- a5 (nodes): exclusive scan of the unique counts -> offsets ----
       if (P.N > 0)   // N == 0 with M > 0 always fails validation; nothing to scan
       MN_CUDA(launch("scan_counts", 4.0 * P.N + 8.0 * (P.N + 1), s, [&] {
         k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(cnt, P.N, node_off, sstatus,
-                                                                                 tickets + 31, 1);
+                                                                                 tickets + 31, 2);
       }));
       MN_CUDA(cudaMemcpyAsync(host + 1, node_off + P.N, 8, cudaMemcpyDeviceToHost, s));
     }
@@ -605,7 +615,8 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       if (U && !out) { st = MN_ERR_OOM; goto done; }
       if (U) {
         MN_CUDA(launch("node_compact", 8.0 * U + 24.0 * P.N, s, [&] {
-          k_node_compact<<<(unsigned)tiles_of(P.N, 256), 256, 0, s>>>(eoff, P.C, ekA, node_off, P.N, out);
+          k_node_compact<<<(unsigned)tiles_of(P.N, kNodeThreads), kNodeThreads, 0, s>>>(eoff, P.C, ekA, lofs,
+                                                                                         node_off, P.N, out);
         }));
       }
       node_out->num_nodes = P.N;
