@@ -216,12 +216,19 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    local = local % max(1, torch.cuda.device_count())   # several test ranks may share one GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if rank == 0:
         mnbuild.build()
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # MN_DIST_BACKEND=gloo stages the exchange through host memory: it lets several ranks share
+        # one GPU to exercise this path in tests; the product exchange is NCCL over NVLink
+        backend = os.environ.get("MN_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         dist.barrier()
     mn.load()
 
@@ -245,7 +252,7 @@ def run_ours(args):
     def maxover(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

@@ -214,7 +214,11 @@ template <> struct Nbr<MN_HEX8> {   // {1,3,4} {0,2,5} {1,3,6} {0,2,7} {0,5,7} {
 template <int T>
 __device__ __forceinline__ int nbr_local(int p, int c) {
   const int i = p * Elem<T>::C + c;
-  return (int)(((i < 16) ? (Nbr<T>::LO >> (4 * i)) : (Nbr<T>::HI >> (4 * (i - 16)))) & 0xF);
+  if constexpr (Nbr<T>::HI == 0) {
+    return (int)((Nbr<T>::LO >> (4 * i)) & 0xF);
+  } else {
+    return (int)(((i < 16) ? (Nbr<T>::LO >> (4 * i)) : (Nbr<T>::HI >> (4 * (i - 16)))) & 0xF);
+  }
 }
 
 inline int arity_of(int t) { return t == MN_TRI3 ? 3 : (t == MN_HEX8 ? 8 : 4); }

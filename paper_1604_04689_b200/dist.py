@@ -59,6 +59,27 @@ class CudaOps:
         return dist_finish(node_keys, elem_pairs, num_nodes, lo, hi)
 
 
+def _a2a(out, inp, out_splits, in_splits, group):
+    """all_to_all_single; with a gloo group and CUDA tensors the exchange is staged through host
+    memory (gloo has no CUDA all-to-all) — used to exercise the multi-rank path on one GPU."""
+    if inp.is_cuda and dist.get_backend(group) == "gloo":
+        host_out = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(host_out, inp.cpu(), out_splits, in_splits, group=group)
+        out.copy_(host_out)
+    else:
+        dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+
+
+def _all_gather(outs, inp, group):
+    if inp.is_cuda and dist.get_backend(group) == "gloo":
+        host = [torch.empty(o.shape, dtype=o.dtype) for o in outs]
+        dist.all_gather(host, inp.cpu(), group=group)
+        for o, h in zip(outs, host):
+            o.copy_(h)
+    else:
+        dist.all_gather(outs, inp, group=group)
+
+
 def find_neighbors_dist(conn_shard: torch.Tensor, etype, global_elem_base: int, num_nodes: int,
                         group=None, ops=None) -> DistResult:
     ops = ops or CudaOps
@@ -69,22 +90,22 @@ def find_neighbors_dist(conn_shard: torch.Tensor, etype, global_elem_base: int, 
     # ---- count exchange: row g of `send` goes to rank g ----
     send = torch.tensor([[ncount[g], ecount[g]] for g in range(world)], dtype=torch.int64, device=dev)
     recv = torch.empty_like(send)
-    dist.all_to_all_single(recv, send.reshape(-1), group=group)
+    _a2a(recv.view(-1), send.reshape(-1), None, None, group)
     recv = recv.reshape(world, 2).cpu()
     rn = recv[:, 0].tolist()
     re_ = recv[:, 1].tolist()
     # ---- payload exchange, received in source-rank order ----
     node_in = torch.empty(sum(rn), dtype=torch.int64, device=dev)
     elem_in = torch.empty(sum(re_), dtype=torch.int64, device=dev)
-    dist.all_to_all_single(node_in, nk, output_split_sizes=rn, input_split_sizes=list(ncount), group=group)
-    dist.all_to_all_single(elem_in, ep, output_split_sizes=re_, input_split_sizes=list(ecount), group=group)
+    _a2a(node_in, nk, rn, list(ncount), group)
+    _a2a(elem_in, ep, re_, list(ecount), group)
     del nk, ep
     lo, hi = owner_range(num_nodes, world, rank)
     node, elem = ops.finish(node_in, elem_in, num_nodes, lo, hi)
     # ---- global bases of the slices (exclusive scan of the per-rank nnz) ----
     mine = torch.tensor([node[1].numel(), elem[1].numel()], dtype=torch.int64, device=dev)
     allv = [torch.empty_like(mine) for _ in range(world)]
-    dist.all_gather(allv, mine, group=group)
+    _all_gather(allv, mine, group)
     allv = torch.stack(allv).cpu()
     node_base = int(allv[:rank, 0].sum())
     elem_base = int(allv[:rank, 1].sum())
@@ -101,7 +122,7 @@ def gather_global(res: DistResult, num_nodes: int, group=None):
         glob_off = off[:-1] + base
         sizes = torch.tensor([glob_off.numel(), idx.numel()], dtype=torch.int64, device=off.device)
         allsz = [torch.empty_like(sizes) for _ in range(world)]
-        dist.all_gather(allsz, sizes, group=group)
+        _all_gather(allsz, sizes, group)
         allsz = torch.stack(allsz).cpu()
         mo, mi = int(allsz[:, 0].max()), int(allsz[:, 1].max())
         po = torch.zeros(mo, dtype=torch.int64, device=off.device)
@@ -110,8 +131,8 @@ def gather_global(res: DistResult, num_nodes: int, group=None):
         pi[: idx.numel()] = idx
         offs = [torch.empty_like(po) for _ in range(world)]
         idxs = [torch.empty_like(pi) for _ in range(world)]
-        dist.all_gather(offs, po, group=group)      # padded to equal sizes (gloo needs that)
-        dist.all_gather(idxs, pi, group=group)
+        _all_gather(offs, po, group)      # padded to equal sizes (gloo needs that)
+        _all_gather(idxs, pi, group)
         offs = [o[: int(s[0])] for o, s in zip(offs, allsz)]
         idxs = [x[: int(s[1])] for x, s in zip(idxs, allsz)]
         total = int(allsz[:, 1].sum())
