@@ -68,21 +68,25 @@ __device__ __forceinline__ uint64_t lookback_wait(const uint64_t* p, uint32_t ep
 // digit are requested at once, so a walk over k aggregate-only tiles costs ceil(k / W) round trips
 // to L2 instead of k.  status is [tiles][bins]; returns the exclusive prefix of each digit.
 template <int BPT, int W>
-__device__ __forceinline__ void lookback_bins(const uint64_t* status, int bins, uint32_t tile, int b0,
-                                              uint32_t epoch, uint64_t (&excl)[BPT]) {
+__device__ __forceinline__ void lookback_issue(const uint64_t* status, int bins, uint32_t tile, int b0,
+                                               uint64_t (&w)[BPT][W]) {
   const int64_t t0 = (int64_t)tile - 1;
-  uint64_t w[BPT][W];
 #pragma unroll
-  for (int j = 0; j < BPT; ++j) {
-    excl[j] = 0;
+  for (int j = 0; j < BPT; ++j)
 #pragma unroll
     for (int k = 0; k < W; ++k) {
       const int64_t t = t0 - k;
       w[j][k] = t >= 0 ? ld_relaxed_u64(status + (size_t)t * bins + b0 + j) : 0;
     }
-  }
+}
+
+template <int BPT, int W>
+__device__ __forceinline__ void lookback_finish(const uint64_t* status, int bins, uint32_t tile, int b0,
+                                                uint32_t epoch, uint64_t (&w)[BPT][W], uint64_t (&excl)[BPT]) {
+  const int64_t t0 = (int64_t)tile - 1;
 #pragma unroll
   for (int j = 0; j < BPT; ++j) {
+    excl[j] = 0;
     int64_t tb = t0;
     bool done = false;
     while (true) {
@@ -109,6 +113,17 @@ __device__ __forceinline__ void lookback_bins(const uint64_t* status, int bins, 
       }
     }
   }
+}
+
+// Windowed decoupled look-back for BPT digits owned by this thread: W predecessor status words per
+// digit are requested at once, so a walk over k aggregate-only tiles costs ceil(k / W) round trips
+// to L2 instead of k.  status is [tiles][bins]; returns the exclusive prefix of each digit.
+template <int BPT, int W>
+__device__ __forceinline__ void lookback_bins(const uint64_t* status, int bins, uint32_t tile, int b0,
+                                              uint32_t epoch, uint64_t (&excl)[BPT]) {
+  uint64_t w[BPT][W];
+  lookback_issue<BPT, W>(status, bins, tile, b0, w);
+  lookback_finish<BPT, W>(status, bins, tile, b0, epoch, w, excl);
 }
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {

@@ -208,6 +208,7 @@ template <int THREADS, int ITEMS, int BINS>
 struct OnesweepSmem {
   static constexpr int WARPS = THREADS / 32;
   uint32_t whist[WARPS][BINS];
+  uint32_t ecnt[BINS];   // EARLY: tile digit counts from shared-memory atomics, before ranking
   uint32_t binstart[BINS];
   uint64_t gofs[BINS];
   uint64_t wsum[WARPS];
@@ -238,8 +239,11 @@ __device__ __forceinline__ unsigned digit_peers(uint32_t d) {
 // equal keys inside the tile adds its length to counts[key] with two atomics (+end+1 at the run's
 // last slot, -start at its first), so counts[] ends as the per-node incidence counts whose
 // exclusive scan is the element-CSR offsets.
+// EARLY: the tile histogram is built first with shared-memory atomics, the aggregate published and
+// the first look-back window requested before the (slower) stable ranking, so the look-back round
+// trip overlaps the ranking instead of following it (the "early counts" of onesweep).
 template <typename KeyT, int SRC, int T, bool PAYLOAD, bool OWNER, int BINS, int THREADS, int ITEMS,
-          int W = 4, int MINB = 3, int RANK = 0, bool COUNTS = false>
+          int W = 4, int MINB = 3, int RANK = 0, bool COUNTS = false, bool EARLY = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 k_onesweep(PassArgs pa) {
   constexpr int WARPS = THREADS / 32;
@@ -258,6 +262,8 @@ k_onesweep(PassArgs pa) {
   const bool own = BINS >= THREADS || tid < BINS;   // warp-uniform
   if (tid == 0) sm.tile = atomicAdd(pa.ticket, 1u);
   for (int i = tid; i < WARPS * BINS; i += THREADS) (&sm.whist[0][0])[i] = 0;
+  if (EARLY)
+    for (int i = tid; i < BINS; i += THREADS) sm.ecnt[i] = 0;
   __syncthreads();
   const uint32_t tile = sm.tile;
   const int64_t base = (int64_t)tile * TILE;
@@ -294,6 +300,26 @@ k_onesweep(PassArgs pa) {
       }
     } else {
       key[i] = (KeyT)~(KeyT)0;
+    }
+  }
+
+  // ---- EARLY: tile histogram, aggregate published, first look-back window in flight ----
+  uint64_t lbw[BPT][W];
+  if (EARLY) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int64_t idx = chunk + i * 32 + lane;
+      if (idx < pa.n) atomicAdd(&sm.ecnt[digit_of<KeyT, OWNER>(key[i], pa.pd, BINS - 1)], 1u);
+    }
+    __syncthreads();
+    if (own) {
+#pragma unroll
+      for (int j = 0; j < BPT; ++j) {
+        const int b = tid * BPT + j;
+        st_relaxed_u64(pa.status + (size_t)tile * BINS + b,
+                       st_pack(pa.epoch, tile == 0 ? ST_INC : ST_AGG, sm.ecnt[b]));
+      }
+      if (tile > 0) lookback_issue<BPT, W>(pa.status, BINS, tile, tid * BPT, lbw);
     }
   }
 
@@ -357,8 +383,10 @@ k_onesweep(PassArgs pa) {
     }
     cnt[j] = run;
     tsum += run;
-    const uint32_t pub = (b == BINS - 1) ? run - (uint32_t)(TILE - nvalid) : run;
-    st_relaxed_u64(pa.status + (size_t)tile * BINS + b, st_pack(pa.epoch, tile == 0 ? ST_INC : ST_AGG, pub));
+    if (!EARLY) {
+      const uint32_t pub = (b == BINS - 1) ? run - (uint32_t)(TILE - nvalid) : run;
+      st_relaxed_u64(pa.status + (size_t)tile * BINS + b, st_pack(pa.epoch, tile == 0 ? ST_INC : ST_AGG, pub));
+    }
   }
   // ---- local exclusive scan of the tile counts over digits ----
   uint32_t inc = tsum;
@@ -404,7 +432,10 @@ k_onesweep(PassArgs pa) {
 #pragma unroll
   for (int j = 0; j < BPT; ++j) excl[j] = 0;
   if (tile > 0 && own) {
-    lookback_bins<BPT, W>(pa.status, BINS, tile, tid * BPT, pa.epoch, excl);
+    if (EARLY)
+      lookback_finish<BPT, W>(pa.status, BINS, tile, tid * BPT, pa.epoch, lbw, excl);
+    else
+      lookback_bins<BPT, W>(pa.status, BINS, tile, tid * BPT, pa.epoch, excl);
 #pragma unroll
     for (int j = 0; j < BPT; ++j) {
       const int b = tid * BPT + j;

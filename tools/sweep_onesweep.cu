@@ -70,13 +70,14 @@ struct Bufs {
   const int32_t* conn;
 };
 
-template <typename KeyT, int SRC, int T, bool PAYLOAD, int BINS, int THREADS, int ITEMS, int W, int MINB, int RANK>
+template <typename KeyT, int SRC, int T, bool PAYLOAD, int BINS, int THREADS, int ITEMS, int W, int MINB, int RANK,
+          bool EARLY = false>
 unsigned long long run(Bufs& c, int shift, int width, const char* label, unsigned long long ref) {
   using Sm = OnesweepSmem<THREADS, ITEMS, BINS>;
   constexpr int TILE = THREADS * ITEMS;
   const int64_t tiles = (c.n + TILE - 1) / TILE;
   const size_t smem = ((sizeof(Sm) + 15) & ~size_t(15)) + (size_t)TILE * sizeof(KeyT) + ((PAYLOAD || SRC == 2) ? (size_t)TILE * 4 : 0);
-  auto kern = k_onesweep<KeyT, SRC, T, PAYLOAD, false, BINS, THREADS, ITEMS, W, MINB, RANK>;
+  auto kern = k_onesweep<KeyT, SRC, T, PAYLOAD, false, BINS, THREADS, ITEMS, W, MINB, RANK, false, EARLY>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, smem));
@@ -145,28 +146,22 @@ int main(int argc, char** argv) {
   CK(cudaMemset(c.err, 0xFF, 8));
   c.conn = conn;
   const int w0 = (b + 2) / 3, w1 = (b - w0 + 1) / 2;
-  for (int scr = 0; scr < 2; ++scr) {
+  for (int scr = 0; scr < 1; ++scr) {
     gen_kuhn<<<148 * 8, 256>>>(n, conn);
     if (scr) scramble<<<148 * 8, 256>>>(conn, P, b);
     CK(cudaDeviceSynchronize());
     printf("---- %s node numbering ----\n", scr ? "random" : "natural (coherent)");
     // pass 0 from conn
     unsigned long long r0 = run<uint32_t, 2, MN_TET4, false, 512, 512, 16, 4, 2, 0>(c, 0, w0, "pass0 match", 0);
-    run<uint32_t, 2, MN_TET4, false, 512, 512, 16, 4, 2, 1>(c, 0, w0, "pass0 ballot", r0);
-    run<uint32_t, 2, MN_TET4, false, 512, 512, 16, 4, 2, 2>(c, 0, w0, "pass0 uniform+ballot", r0);
-    run<uint32_t, 2, MN_TET4, false, 512, 512, 16, 4, 1, 3>(c, 0, w0, "pass0 batched minB1", r0);
-    run<uint32_t, 2, MN_TET4, false, 512, 512, 16, 4, 2, 3>(c, 0, w0, "pass0 batched match", r0);
+    run<uint32_t, 2, MN_TET4, false, 512, 512, 16, 4, 2, 0, true>(c, 0, w0, "pass0 early", r0);
+    run<uint32_t, 2, MN_TET4, false, 512, 512, 16, 8, 2, 0, true>(c, 0, w0, "pass0 early W8", r0);
     // make the pass-0 output the input of the timed pass 1
     std::swap(c.kA, c.kB);
     std::swap(c.vA, c.vB);
     unsigned long long r1 = run<uint32_t, 0, 0, true, 512, 512, 16, 4, 2, 0>(c, w0, w1, "pass1 match", 0);
-    run<uint32_t, 0, 0, true, 512, 512, 16, 4, 2, 1>(c, w0, w1, "pass1 ballot", r1);
-    run<uint32_t, 0, 0, true, 512, 512, 16, 4, 2, 2>(c, w0, w1, "pass1 uniform+ballot", r1);
-
-    run<uint32_t, 0, 0, true, 512, 512, 16, 4, 2, 3>(c, w0, w1, "pass1 batched match", r1);
-    run<uint32_t, 0, 0, true, 512, 512, 16, 4, 1, 3>(c, w0, w1, "pass1 batched minB1", r1);
-    run<uint32_t, 0, 0, true, 512, 512, 16, 8, 2, 2>(c, w0, w1, "pass1 u+b W8", r1);
-    run<uint32_t, 0, 0, true, 512, 512, 16, 2, 2, 2>(c, w0, w1, "pass1 u+b W2", r1);
+    run<uint32_t, 0, 0, true, 512, 512, 16, 4, 2, 0, true>(c, w0, w1, "pass1 early", r1);
+    run<uint32_t, 0, 0, true, 512, 512, 16, 8, 2, 0, true>(c, w0, w1, "pass1 early W8", r1);
+    run<uint32_t, 0, 0, true, 512, 512, 16, 2, 2, 0, true>(c, w0, w1, "pass1 early W2", r1);
     std::swap(c.kA, c.kB);
     std::swap(c.vA, c.vB);
   }
