@@ -215,6 +215,19 @@ mn_status mn_dist_finish(const uint64_t* d_node_keys, int64_t n_node_keys,
                          mn_csr* node_slice, mn_csr* elem_slice);
 
 /* ---------------------------------------------------------------------------------------------
+ * Algorithm selection for the element CSR (process-wide; results are identical either way).
+ *   0 = auto: meshes of >= 2^20 elements whose consecutive elements share nodes (sampled: fewer
+ *       than 0.5 distinct (slot, node) groups per incidence in windows of 32 elements) use the
+ *       counting-sort transpose, all others the LSD radix sort.  Costs one extra blocking read.
+ *   1 = LSD radix sort of (node, element) pairs (§2.2.2, "sort according to the
+ *       first array of integers").
+ *   2 = counting-sort transpose: per-node counts, scan, scatter, per-node sort of element ids
+ *       (element CSR = transpose of the incidence matrix).
+ * ------------------------------------------------------------------------------------------- */
+mn_status mn_set_elem_path(int mode);
+int mn_get_elem_path(void);
+
+/* ---------------------------------------------------------------------------------------------
  * Instrumentation (bench only; not thread-safe)
  * ------------------------------------------------------------------------------------------- */
 /* Count of kernels this library has launched since load. */

@@ -22,7 +22,7 @@ __all__ = [
     "emit_node_pairs", "emit_elem_pairs", "radix_sort_keys", "radix_sort_pairs_u32",
     "unique_node_csr", "elem_offsets", "exclusive_scan",
     "dist_bucket", "dist_finish",
-    "launch_count", "profile_enable", "profile_reset", "profile_collect",
+    "launch_count", "profile_enable", "profile_reset", "profile_collect", "set_elem_path", "get_elem_path",
 ]
 
 TRI3, QUAD4, TET4, HEX8 = 0, 1, 2, 3
@@ -102,6 +102,8 @@ def _declare(lib):
         "mn_dist_finish": (S, [_VP, _I64, _VP, _I64, _I64, _I64, _I64, _P(_Allocator), _VP, _P(_Csr),
                                _P(_Csr)]),
         "mn_launch_count": (_I64, []),
+        "mn_set_elem_path": (S, [_INT]),
+        "mn_get_elem_path": (_INT, []),
         "mn_profile_enable": (None, [_INT]),
         "mn_profile_reset": (None, []),
         "mn_profile_collect": (_INT, []),
@@ -452,6 +454,19 @@ def dist_finish(node_keys: torch.Tensor, elem_pairs: torch.Tensor, num_nodes: in
 # ------------------------------------------------------------------------------------------------
 # instrumentation
 # ------------------------------------------------------------------------------------------------
+ELEM_PATHS = {"auto": 0, "radix": 1, "transpose": 2}
+
+
+def set_elem_path(mode="auto"):
+    """Element-CSR algorithm (process-wide): "auto" | "radix" | "transpose" (include/meshnbr.h)."""
+    _check(load().mn_set_elem_path(ELEM_PATHS[mode] if isinstance(mode, str) else int(mode)))
+
+
+def get_elem_path() -> str:
+    v = int(load().mn_get_elem_path())
+    return {b: a for a, b in ELEM_PATHS.items()}[v]
+
+
 def launch_count() -> int:
     return int(load().mn_launch_count())
 

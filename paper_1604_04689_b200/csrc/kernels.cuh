@@ -927,6 +927,222 @@ k_node_compact(const int64_t* __restrict__ eoff, int C, const uint32_t* __restri
 }
 
 // ================================================================================================
+// Element CSR as a counting-sort transpose, used when the mesh numbering has
+// locality: the element CSR is the transpose of the incidence matrix B.
+//   k_locality_sample  distinct (slot, node) groups per warp window of 32 consecutive elements
+//   k_elem_count       validation + per-node incidence counts, one atomic per group of lanes that
+//                      hold the same node in the same local slot (__match_any_sync aggregation)
+//   k_elem_scatter     each group reserves its slots with one returning atomic, lanes write their
+//                      element ids (order inside a node is arbitrary here)
+//   k_elem_segsort     per-node insertion sort restores ascending element ids (canonical, R3)
+//   k_segsort_giant    block bitonic sort for segments longer than kSegMax
+// ================================================================================================
+template <int T, bool ALIGNED>
+__global__ void __launch_bounds__(256)
+k_locality_sample(const int32_t* __restrict__ conn, int64_t M, unsigned long long* __restrict__ out) {
+  constexpr int K = Elem<T>::K;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t e0 = (int64_t)((double)M * (double)gw / (double)nw);
+  const int64_t e = e0 + lane;
+  const bool in = e < M;
+  int row[K];
+  if (in) load_row<T, ALIGNED>(conn, e, row);
+  unsigned groups = 0;
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    const int x = in ? row[p] : -1 - lane;
+    const unsigned peers = __match_any_sync(FULL, x);
+    groups += (in && lane == __ffs(peers) - 1) ? 1u : 0u;
+  }
+  const unsigned act = __popc(__ballot_sync(FULL, in));
+  groups = __reduce_add_sync(FULL, groups);
+  if (lane == 0) {
+    atomicAdd(out, (unsigned long long)groups);
+    atomicAdd(out + 1, (unsigned long long)act * K);
+  }
+}
+
+template <int T, bool ALIGNED>
+__global__ void __launch_bounds__(256)
+k_elem_count(const int32_t* __restrict__ conn, int64_t M, int64_t N, int32_t* __restrict__ cnt,
+             unsigned long long* __restrict__ err) {
+  constexpr int K = Elem<T>::K;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < M; base += stride) {
+    const int64_t e = base + lane;
+    const bool in = e < M;
+    int v[K];
+    if (in) load_row<T, ALIGNED>(conn, e, v);
+    int bad = -1, kind = 0;
+    if (in) {
+#pragma unroll
+      for (int p = K - 1; p >= 0; --p)
+        if (v[p] < 0 || (int64_t)v[p] >= N) bad = p;
+      if (bad < 0) {
+#pragma unroll
+        for (int p = K - 1; p >= 1; --p) {
+          bool dup = false;
+#pragma unroll
+          for (int q = 0; q < p; ++q) dup |= (v[q] == v[p]);
+          if (dup) { bad = p; kind = 1; }
+        }
+      }
+      if (bad >= 0) atomicMin(err, (unsigned long long)err_encode((uint64_t)e, kind, bad));
+    }
+    const bool ok = in && bad < 0;
+    if (ok) {
+#pragma unroll
+      for (int p = 0; p < K; ++p) atomicAdd(cnt + v[p], 1);   // fire-and-forget RED
+    }
+  }
+}
+
+template <int T, bool ALIGNED>
+__global__ void __launch_bounds__(256)
+k_elem_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __restrict__ eoff,
+               int32_t* __restrict__ cursor, int32_t* __restrict__ eidx, const unsigned long long* __restrict__ err) {
+  constexpr int K = Elem<T>::K;
+  if (*err != ERR_NONE) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < M; base += stride) {
+    const int64_t e = base + lane;
+    const bool in = e < M;
+    int v[K];
+    if (in) load_row<T, ALIGNED>(conn, e, v);
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      const int x = in ? v[p] : -1 - lane;
+      const unsigned peers = __match_any_sync(FULL, x);
+      const int leader = __ffs(peers) - 1;
+      int b = 0;
+      if (in && lane == leader) b = atomicAdd(cursor + x, (int)__popc(peers));
+      b = __shfl_sync(FULL, b, leader);
+      if (in) eidx[eoff[x] + b + __popc(peers & lanemask_lt())] = (int32_t)e;
+    }
+  }
+}
+
+constexpr int kSegThreads = 128;
+constexpr int kSegMax = 32;
+
+constexpr int kSegSmem = 8192;   // elements of a 128-node chunk staged in shared memory
+
+// Bitonic sorting network on NET registers (ascending); every index is a compile-time constant
+// after unrolling, so v[] stays in registers.
+template <int NET>
+__device__ __forceinline__ void oddeven_sort(int32_t (&v)[NET]) {
+#pragma unroll
+  for (int k = 2; k <= NET; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < NET; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const int32_t a = v[i], b = v[l];
+          const bool asc = (i & k) == 0;
+          v[i] = asc ? min(a, b) : max(a, b);
+          v[l] = asc ? max(a, b) : min(a, b);
+        }
+      }
+    }
+  }
+}
+
+template <int NET>
+__device__ __forceinline__ void sort_segment(int32_t* seg, int d) {
+  int32_t v[NET];
+#pragma unroll
+  for (int i = 0; i < NET; ++i) v[i] = i < d ? seg[i] : INT32_MAX;
+  oddeven_sort<NET>(v);
+#pragma unroll
+  for (int i = 0; i < NET; ++i)
+    if (i < d) seg[i] = v[i];
+}
+
+// A CTA per kSegThreads consecutive nodes: their segments form one contiguous range, staged
+// through shared memory with coalesced loads/stores; each thread sorts its own segment with a
+// register sorting network sized by the largest segment of its warp (warp-uniform choice).
+__global__ void __launch_bounds__(kSegThreads)
+k_elem_segsort(const int64_t* __restrict__ eoff, int64_t N, int32_t* __restrict__ eidx,
+               uint32_t* __restrict__ giants, unsigned int* __restrict__ ngiant,
+               const unsigned long long* __restrict__ err) {
+  __shared__ int32_t buf[kSegSmem];
+  if (err && *err != ERR_NONE) return;
+  const int t = threadIdx.x;
+  const int64_t n0 = (int64_t)blockIdx.x * kSegThreads;
+  const int64_t n1 = n0 + kSegThreads < N ? n0 + kSegThreads : N;
+  const int64_t c0 = eoff[n0], c1 = eoff[n1];
+  const int64_t a = n0 + t;
+  const bool valid = a < N;
+  const int64_t s = valid ? eoff[a] : c1;
+  const int d = valid ? (int)(eoff[a + 1] - s) : 0;
+  const bool big = d > kSegMax;
+  if (valid && big) giants[atomicAdd(ngiant, 1u)] = (uint32_t)a;
+  const bool staged = c1 - c0 <= kSegSmem;   // CTA-uniform
+  if (staged) {
+    for (int64_t i = c0 + t; i < c1; i += kSegThreads) buf[i - c0] = eidx[i];
+    __syncthreads();
+  }
+  int32_t* seg = staged ? buf + (s - c0) : eidx + s;
+  const int dd = (valid && !big) ? d : 0;
+  const int wmax = __reduce_max_sync(0xffffffffu, (unsigned)dd);
+  if (wmax > 1) {
+    if (wmax <= 8) sort_segment<8>(seg, dd);
+    else if (wmax <= 16) sort_segment<16>(seg, dd);
+    else sort_segment<32>(seg, dd);
+  }
+  if (staged) {
+    __syncthreads();
+    // giants keep their (unsorted) values here and are sorted by k_segsort_giant afterwards
+    for (int64_t i = c0 + t; i < c1; i += kSegThreads) eidx[i] = buf[i - c0];
+  }
+}
+
+// In-place ascending bitonic sort of each queued segment [off[a], off[a+1]) (shared memory when it
+// fits, else directly in global memory), one CTA per segment.
+__global__ void __launch_bounds__(1024)
+k_segsort_giant(const int64_t* __restrict__ off, int32_t* __restrict__ vals, const uint32_t* __restrict__ giants,
+                const unsigned int* __restrict__ ngiant, int smem_cap, const unsigned long long* __restrict__ err) {
+  extern __shared__ int32_t sbuf[];
+  if (err && *err != ERR_NONE) return;
+  const unsigned ng = *ngiant;
+  for (unsigned g = blockIdx.x; g < ng; g += gridDim.x) {
+    const int64_t a = giants[g];
+    const int64_t s = off[a];
+    const int64_t n = off[a + 1] - s;
+    int32_t* buf = n <= smem_cap ? sbuf : vals + s;
+    if (n <= smem_cap)
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) sbuf[i] = vals[s + i];
+    __syncthreads();
+    int64_t n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (int64_t k = 2; k <= n2; k <<= 1) {
+      for (int64_t j = k >> 1; j > 0; j >>= 1) {
+        for (int64_t t = threadIdx.x; t < n2 / 2; t += blockDim.x) {
+          const int64_t blk = t / j, o = t % j;
+          int64_t lo, hi;
+          if (j == (k >> 1)) { lo = blk * k + o; hi = blk * k + k - 1 - o; }
+          else { lo = blk * 2 * j + o; hi = lo + j; }
+          if (hi < n) {
+            const int32_t x = buf[lo], y = buf[hi];
+            if (x > y) { buf[lo] = y; buf[hi] = x; }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (n <= smem_cap)
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) vals[s + i] = sbuf[i];
+    __syncthreads();
+  }
+}
+
+// ================================================================================================
 // k_elem_offsets: offsets from the stably sorted element-pair keys (no dedupe needed: (node,
 // element) pairs are unique once the input is validated).
 // ================================================================================================

@@ -26,6 +26,10 @@ namespace mn {
 // instrumentation
 // ================================================================================================
 static std::atomic<int64_t> g_launches{0};
+// element-CSR algorithm: 0 = auto (locality test), 1 = LSD radix sort, 2 = counting-sort transpose
+static std::atomic<int> g_elem_path{0};
+constexpr int64_t kTransposeMinElems = 1 << 20;
+constexpr double kTransposeMaxGroupRatio = 0.5;
 static bool g_prof = false;
 struct ProfRec { const char* name; cudaEvent_t a, b; double bytes; };
 static std::vector<ProfRec> g_recs;
@@ -442,6 +446,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
   const int64_t scan_tiles = tiles_of(P.N, kScanTile);
   const int64_t giant_cap = P.N;   // any node may overflow the warp path (> 32 distinct neighbours)
   const bool aligned = ((uintptr_t)conn & 15) == 0;
+  bool transpose = false;
   int64_t *node_off = nullptr, *elem_off = nullptr;
   int32_t* elem_idx = nullptr;
   void* ws = nullptr;
@@ -466,6 +471,25 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     if (want_elem) { elem_out->num_nodes = P.N; elem_out->nnz = 0; elem_out->offsets = elem_off; elem_out->indices = nullptr; elem_out->owner = mem.a; }
     return MN_OK;
   }
+  // ---- element-CSR algorithm: transpose when consecutive elements share nodes (locality) ----
+  {
+    const int mode = g_elem_path.load();
+    if (mode == 2) {
+      transpose = true;
+    } else if (mode == 0 && P.M >= kTransposeMinElems) {
+      unsigned long long* smp = (unsigned long long*)mem.get(16);
+      if (!smp) { st = MN_ERR_OOM; goto done; }
+      MN_CUDA(cudaMemsetAsync(smp, 0, 16, s));
+      MN_CUDA(launch("locality_sample", 0.0, s, [&] {
+        if (aligned) k_locality_sample<T, true><<<64, 256, 0, s>>>(conn, P.M, smp);
+        else k_locality_sample<T, false><<<64, 256, 0, s>>>(conn, P.M, smp);
+      }));
+      MN_CUDA(cudaMemcpyAsync(host + 2, smp, 16, cudaMemcpyDeviceToHost, s));
+      MN_CUDA(cudaStreamSynchronize(s));
+      mem.put(smp);
+      transpose = host[3] > 0 && (double)host[2] < kTransposeMaxGroupRatio * (double)host[3];
+    }
+  }
   {
     // ---- workspace ----
     size_t head = 0;
@@ -473,7 +497,9 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     uint32_t *tickets = nullptr, *ekA = nullptr, *ekB = nullptr, *epA = nullptr, *epB = nullptr, *giants = nullptr;
     unsigned int* ngiant = nullptr;
     uint64_t *bases = nullptr, *status = nullptr, *sstatus = nullptr;
-    int32_t *cnt = nullptr, *ecnt = nullptr, *lofs = nullptr;
+    int32_t *cnt = nullptr, *ecnt = nullptr, *lofs = nullptr, *cursor = nullptr;
+    uint32_t* sgiants = nullptr;
+    unsigned int* nsgiant = nullptr;
     int64_t* eoff = elem_off;
     int32_t* eidx = elem_idx;
     auto layout = [&](Arena& a) {
@@ -485,7 +511,10 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       status = a.take<uint64_t>((size_t)elem_tiles * BINS);
       sstatus = a.take<uint64_t>((size_t)(scan_tiles ? scan_tiles : 1));
       ecnt = a.take<int32_t>((size_t)P.N + 1);   // per-node incidence counts (atomics in the last pass)
+      nsgiant = a.take<unsigned int>(1);
+      if (transpose) cursor = a.take<int32_t>((size_t)P.N + 1);
       head = a.off;
+      if (transpose) sgiants = a.take<uint32_t>((size_t)P.N + 1);
       // ekA | ekB | epA | epB (each 256-byte aligned, contiguous); later the node raw region
       ekA = a.take<uint32_t>((size_t)P.Pe);
       ekB = a.take<uint32_t>((size_t)P.Pe);
@@ -513,6 +542,36 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
     MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
 
+    if (transpose) {
+      // ---- a2 + a3e + a4 + a5 (elements) as a counting-sort transpose ----
+      MN_CUDA(launch("elem_count", 4.0 * P.K * P.M, s, [&] {
+        if (aligned) k_elem_count<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw);
+        else k_elem_count<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw);
+      }));
+      if (P.N > 0)
+        MN_CUDA(launch("scan_counts", 4.0 * P.N + 8.0 * (P.N + 1), s, [&] {
+          k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(ecnt, P.N, eoff, sstatus,
+                                                                                   tickets + 29, 1);
+        }));
+      MN_CUDA(launch("elem_scatter", 4.0 * P.K * P.M + 12.0 * P.Pe, s, [&] {
+        if (aligned) k_elem_scatter<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, eoff, cursor, eidx, errw);
+        else k_elem_scatter<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, eoff, cursor, eidx, errw);
+      }));
+      if (P.N > 0)
+        MN_CUDA(launch("elem_segsort", 8.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
+          k_elem_segsort<<<(unsigned)tiles_of(P.N, kSegThreads), kSegThreads, 0, s>>>(eoff, P.N, eidx, sgiants,
+                                                                                   nsgiant, errw);
+        }));
+      const int scap = 48 * 1024;
+      static bool seg_attr = false;
+      if (!seg_attr) {
+        cudaFuncSetAttribute(k_segsort_giant, cudaFuncAttributeMaxDynamicSharedMemorySize, scap * 4);
+        seg_attr = true;
+      }
+      MN_CUDA(launch("segsort_giant", 0.0, s, [&] {
+        k_segsort_giant<<<148, 1024, scap * 4, s>>>(eoff, eidx, sgiants, nsgiant, scap, errw);
+      }));
+    } else {
     // ---- a1/a2 validation + digit histograms of the node ids ----
     MN_CUDA(launch("hist_validate", 4.0 * P.K * P.M, s, [&] {
       if (((uintptr_t)conn & 15) == 0)
@@ -566,6 +625,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
         k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(ecnt, P.N, eoff, sstatus,
                                                                                  tickets + 29, 1);
       }));
+    }   // LSD element path
 
     int64_t U = 0;
     if (want_node) {
@@ -1223,6 +1283,14 @@ fail:
 }
 
 int64_t mn_launch_count(void) { return g_launches.load(); }
+
+mn_status mn_set_elem_path(int mode) {
+  if (mode < 0 || mode > 2) return MN_ERR_INVALID_ARG;
+  g_elem_path.store(mode);
+  return MN_OK;
+}
+
+int mn_get_elem_path(void) { return g_elem_path.load(); }
 
 void mn_profile_enable(int on) { g_prof = on != 0; }
 

@@ -184,16 +184,23 @@ def test_row_a5_exclusive_scan(n):
 # ------------------------------------------------------------------------------------------------
 # whole path vs the std::set oracle
 # ------------------------------------------------------------------------------------------------
+@pytest.fixture(params=["radix", "transpose"])
+def elem_path(request):
+    mn().set_elem_path(request.param)
+    yield request.param
+    mn().set_elem_path("auto")
+
+
 @pytest.mark.parametrize("name,et,make", SMALL)
-def test_whole_path_both(name, et, make):
+def test_whole_path_both(name, et, make, elem_path):
     conn, N = make()
     (no, ni), (eo, ei) = mn().find_neighbors(conn.cuda(), et, N)
-    _assert_csr((no, ni), oracle.node_csr(et, conn, N), name + " node")
-    _assert_csr((eo, ei), oracle.elem_csr(et, conn, N), name + " elem")
+    _assert_csr((no, ni), oracle.node_csr(et, conn, N), name + " node " + elem_path)
+    _assert_csr((eo, ei), oracle.elem_csr(et, conn, N), name + " elem " + elem_path)
 
 
 @pytest.mark.parametrize("name,et,make", SMALL)
-def test_whole_path_single_modes(name, et, make):
+def test_whole_path_single_modes(name, et, make, elem_path):
     conn, N = make()
     exp = oracle.node_csr(et, conn, N)
     _assert_csr(mn().find_node_neighbors(conn.cuda(), et, N), exp, name)
@@ -201,8 +208,8 @@ def test_whole_path_single_modes(name, et, make):
     _assert_csr(mn().find_elem_neighbors(conn.cuda(), et, N), oracle.elem_csr(et, conn, N), name)
 
 
-@pytest.mark.parametrize("ntri", [40, 200, 20000, 30000])
-def test_high_valence_fans(ntri):
+@pytest.mark.parametrize("ntri", [40, 200, 20000, 30000, 60000])
+def test_high_valence_fans(ntri, elem_path):
     """Node 0 and 1 of a fan see 2*ntri raw pairs: 80 (hash), 400 (block sort in shared memory),
     40000 (shared memory) and 60000 (in place in global memory) entries."""
     conn, N = meshgen.nonmanifold_fan(ntri)
@@ -219,7 +226,7 @@ def test_whole_path_host_buffers():
     _assert_csr((eo, ei), oracle.elem_csr(meshgen.TET4, conn, N), "host elem")
 
 
-def test_config2_sphere_full():
+def test_config2_sphere_full(elem_path):
     et, conn, N = meshgen.make_config(2)
     (no, ni), (eo, ei) = mn().find_neighbors(conn.cuda(), et, N)
     _assert_csr((no, ni), oracle.node_csr(et, conn, N), "cfg2 node")
@@ -250,7 +257,7 @@ def test_empty_mesh_and_isolated_nodes():
     ([[0, 1, 2, 3, 4, 5, 6, 7]] * 3 + [[0, 1, 2, 3, 4, 5, 6, 6]], 8, 3),
     ([[0, 1, 2]], 0, 0),
 ])
-def test_invalid_input_reported_like_the_oracle(conn, N, et):
+def test_invalid_input_reported_like_the_oracle(conn, N, et, elem_path):
     c = torch.tensor(conn, dtype=torch.int32)
     code, elem, pos = oracle.validate(et, c, N)
     assert code != 0
@@ -260,7 +267,20 @@ def test_invalid_input_reported_like_the_oracle(conn, N, et):
         assert (ei.value.code, ei.value.elem, ei.value.pos) == (code, elem, pos)
 
 
-def test_deterministic_repeats():
+def test_auto_elem_path_choice():
+    """Config-5-like natural numbering takes the transpose, a relabelled hex the radix sort; both
+    give the same CSR."""
+    conn, N = meshgen.kuhn_tets(60, device="cuda")            # 1.3 M tets, coherent ids
+    mn().set_elem_path("auto")
+    a = mn().find_neighbors(conn, "tet4", N)
+    mn().set_elem_path("radix")
+    b = mn().find_neighbors(conn, "tet4", N)
+    mn().set_elem_path("auto")
+    for x, y in zip(a, b):
+        assert torch.equal(x[0], y[0]) and torch.equal(x[1], y[1])
+
+
+def test_deterministic_repeats(elem_path):
     et = meshgen.HEX8
     conn, N = _perm_hex(20, 3, 4)
     conn = conn.cuda()
@@ -314,7 +334,7 @@ def _symmetric(off, idx):
 
 
 @pytest.mark.parametrize("cfg", [3, 4])
-def test_full_size_config(cfg):
+def test_full_size_config(cfg, elem_path):
     et, conn, N = meshgen.make_config(cfg, device="cuda")
     (no, ni), (eo, ei) = mn().find_neighbors(conn, et, N)
     M = conn.shape[0]
