@@ -582,12 +582,10 @@ k_unique_node(UniqueArgs ua) {
 // The paper's node pairs sorted by their first node are exactly the expansion of the element CSR:
 // incidence (a, e) at element-CSR position i yields the C edge-neighbours of a inside e, so the
 // pairs of node a are {nbr_p(conn[e]) : e in inc(a)} and only a per-node sort + adjacent-difference
-// dedupe remains (segments of C*deg(a) entries: 12 tri, 72 Kuhn tet, 24 hex).  One warp per node:
-//   raw = C*deg <= 32 : one candidate per lane, warp bitonic sort, ballot dedupe;
-//   raw <= 256        : warp hash set in shared memory (tagged with the node id, never cleared),
-//                       the <= 32 uniques then bitonic-sorted;
-//   otherwise         : the node is queued for k_node_giant (block sort).
-// Sorted unique neighbours go to temp[C * elem_off[a]] (the node's own raw region), counts to cnt.
+// dedupe remains (segments of C*deg(a) entries: 12 tri, 72 Kuhn tet, 24 hex).  One thread per
+// node (k_node_gather_t): private shared-memory hash set, insertion sort of the <= kMaxUnique
+// distinct values, lists packed per CTA chunk; nodes with more distinct neighbours are queued for
+// k_node_giant (block sort).  (A warp-per-node variant was 4x slower on B200 and was removed.)
 // ================================================================================================
 __device__ __forceinline__ uint32_t bitonic32(uint32_t x, int lane) {
 #pragma unroll
@@ -652,77 +650,40 @@ __device__ __forceinline__ uint32_t pick(const int (&row)[Elem<T>::K], int idx) 
   return v;
 }
 
-constexpr int kGatherWarps = 8;
+constexpr int kSegThreads = 128;
+constexpr int kSegMax = 32;   // longer element lists are sorted by k_segsort_giant
 
-template <int T, bool ALIGNED>
-__global__ void __launch_bounds__(32 * kGatherWarps)
-k_node_gather(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, const int32_t* __restrict__ conn,
-              int64_t N, uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, uint32_t* __restrict__ giants,
-              unsigned int* __restrict__ ngiant, const unsigned long long* __restrict__ err) {
-  constexpr int C = Elem<T>::C, K = Elem<T>::K;
-  __shared__ unsigned long long htab[kGatherWarps][128];
-  __shared__ uint32_t ulist[kGatherWarps][64];
-  if (err && *err != ERR_NONE) return;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kGatherWarps * 128; i += blockDim.x) (&htab[0][0])[i] = 0;
-  __syncthreads();
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t a = (((int64_t)blockIdx.x * blockDim.x) >> 5) + wib; a < N; a += nw) {
-    const int64_t s = eoff[a];
-    const int64_t d = eoff[a + 1] - s;
-    const int64_t raw = (int64_t)C * d;
-    uint32_t* out = temp + (size_t)C * s;
-    if (raw <= 32) {
-      uint32_t v = 0xFFFFFFFFu;
-      if (lane < raw) {
-        const int inc = lane / C, c = lane - inc * C;
-        int row[K];
-        load_row<T, ALIGNED>(conn, eidx[s + inc], row);
-        v = pick<T>(row, nbr_local<T>(local_of<T>(row, (int)a), c));
-      }
-      v = bitonic32(v, lane);
-      const uint32_t up = __shfl_up_sync(FULL, v, 1);
-      const bool f = lane < raw && (lane == 0 || v != up);
-      const unsigned bal = __ballot_sync(FULL, f);
-      if (f) out[__popc(bal & lanemask_lt())] = v;
-      if (lane == 0) cnt[a] = __popc(bal);
-    } else if (raw <= 256) {
-      const unsigned long long tag = (unsigned long long)(a + 1) << 32;
-      int uc = 0;
-      bool overflow = false;
-      for (int64_t b0 = 0; b0 < d && !overflow; b0 += 32) {
-        const bool act = b0 + lane < d;
-        int row[K];
-        int p = 0;
-        if (act) {
-          load_row<T, ALIGNED>(conn, eidx[s + b0 + lane], row);
-          p = local_of<T>(row, (int)a);
-        }
+// Bitonic sorting network on NET registers (ascending); every index is a compile-time constant
+// after unrolling, so v[] stays in registers.
+template <int NET>
+__device__ __forceinline__ void oddeven_sort(int32_t (&v)[NET]) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-          const uint32_t v = act ? pick<T>(row, nbr_local<T>(p, c)) : 0u;
-          const bool isnew = act && hash_insert(htab[wib], tag, v);
-          const unsigned bal = __ballot_sync(FULL, isnew);
-          const int pos = uc + __popc(bal & lanemask_lt());
-          if (isnew && pos < 64) ulist[wib][pos] = v;
-          uc += __popc(bal);
+  for (int k = 2; k <= NET; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < NET; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const int32_t a = v[i], b = v[l];
+          const bool asc = (i & k) == 0;
+          v[i] = asc ? min(a, b) : max(a, b);
+          v[l] = asc ? max(a, b) : min(a, b);
         }
-        overflow = uc > 32;
       }
-      __syncwarp();
-      if (!overflow) {
-        uint32_t x = lane < uc ? ulist[wib][lane] : 0xFFFFFFFFu;
-        x = bitonic32(x, lane);
-        if (lane < uc) out[lane] = x;
-        if (lane == 0) cnt[a] = uc;
-      } else if (lane == 0) {
-        giants[atomicAdd(ngiant, 1u)] = (uint32_t)a;
-      }
-      __syncwarp();
-    } else if (lane == 0) {
-      giants[atomicAdd(ngiant, 1u)] = (uint32_t)a;
     }
   }
+}
+
+template <int NET>
+__device__ __forceinline__ void sort_segment(int32_t* seg, int d) {
+  int32_t v[NET];
+#pragma unroll
+  for (int i = 0; i < NET; ++i) v[i] = i < d ? seg[i] : INT32_MAX;
+  oddeven_sort<NET>(v);
+#pragma unroll
+  for (int i = 0; i < NET; ++i)
+    if (i < d) seg[i] = v[i];
 }
 
 // Thread-per-node variant (the one the pipeline uses): each thread walks its node's incidences
@@ -734,6 +695,9 @@ constexpr int kNodeThreads = 128;
 constexpr int kHashSlots = 32;
 constexpr int kMaxUnique = 24;
 
+// (Fusing the element-list sort of the transpose path into this kernel, with the CTA's incidence
+// range staged in shared memory, was measured slower on B200: the extra registers / shared memory
+// cost more occupancy than the saved pass.)
 template <int T, bool ALIGNED>
 __global__ void __launch_bounds__(kNodeThreads)
 k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, const int32_t* __restrict__ conn,
@@ -750,18 +714,20 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
   const int64_t n0 = (int64_t)blockIdx.x * kNodeThreads;
   const int64_t a = n0 + t;
   const bool valid = a < N;
+  const int64_t s0 = valid ? eoff[a] : 0;
+  const int64_t d0 = valid ? eoff[a + 1] - s0 : 0;
+  const int32_t* inc = eidx + s0;
   int L = 0;
   int64_t raw = 0;
   if (valid) {
 #pragma unroll
     for (int i = 0; i < kHashSlots; ++i) tab[i][t] = EMPTY;
-    const int64_t s = eoff[a];
-    const int64_t d = eoff[a + 1] - s;
+    const int64_t d = d0;
     raw = (int64_t)C * d;
     for (int64_t i0 = 0; i0 < d && L <= kMaxUnique; i0 += B) {
       int e[B];
 #pragma unroll
-      for (int q = 0; q < B; ++q) e[q] = (i0 + q < d) ? __ldg(eidx + s + i0 + q) : -1;
+      for (int q = 0; q < B; ++q) e[q] = (i0 + q < d) ? inc[i0 + q] : -1;
       int row[B][K];
 #pragma unroll
       for (int q = 0; q < B; ++q)
@@ -1026,43 +992,8 @@ k_elem_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __res
   }
 }
 
-constexpr int kSegThreads = 128;
-constexpr int kSegMax = 32;
 
 constexpr int kSegSmem = 8192;   // elements of a 128-node chunk staged in shared memory
-
-// Bitonic sorting network on NET registers (ascending); every index is a compile-time constant
-// after unrolling, so v[] stays in registers.
-template <int NET>
-__device__ __forceinline__ void oddeven_sort(int32_t (&v)[NET]) {
-#pragma unroll
-  for (int k = 2; k <= NET; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-#pragma unroll
-      for (int i = 0; i < NET; ++i) {
-        const int l = i ^ j;
-        if (l > i) {
-          const int32_t a = v[i], b = v[l];
-          const bool asc = (i & k) == 0;
-          v[i] = asc ? min(a, b) : max(a, b);
-          v[l] = asc ? max(a, b) : min(a, b);
-        }
-      }
-    }
-  }
-}
-
-template <int NET>
-__device__ __forceinline__ void sort_segment(int32_t* seg, int d) {
-  int32_t v[NET];
-#pragma unroll
-  for (int i = 0; i < NET; ++i) v[i] = i < d ? seg[i] : INT32_MAX;
-  oddeven_sort<NET>(v);
-#pragma unroll
-  for (int i = 0; i < NET; ++i)
-    if (i < d) seg[i] = v[i];
-}
 
 // A CTA per kSegThreads consecutive nodes: their segments form one contiguous range, staged
 // through shared memory with coalesced loads/stores; each thread sorts its own segment with a

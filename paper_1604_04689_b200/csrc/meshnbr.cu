@@ -557,20 +557,22 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
         if (aligned) k_elem_scatter<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, eoff, cursor, eidx, errw);
         else k_elem_scatter<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, eoff, cursor, eidx, errw);
       }));
-      if (P.N > 0)
-        MN_CUDA(launch("elem_segsort", 8.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
-          k_elem_segsort<<<(unsigned)tiles_of(P.N, kSegThreads), kSegThreads, 0, s>>>(eoff, P.N, eidx, sgiants,
-                                                                                   nsgiant, errw);
-        }));
       const int scap = 48 * 1024;
       static bool seg_attr = false;
       if (!seg_attr) {
         cudaFuncSetAttribute(k_segsort_giant, cudaFuncAttributeMaxDynamicSharedMemorySize, scap * 4);
         seg_attr = true;
       }
-      MN_CUDA(launch("segsort_giant", 0.0, s, [&] {
-        k_segsort_giant<<<148, 1024, scap * 4, s>>>(eoff, eidx, sgiants, nsgiant, scap, errw);
-      }));
+      if (want_elem) {
+        if (P.N > 0)
+          MN_CUDA(launch("elem_segsort", 8.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
+            k_elem_segsort<<<(unsigned)tiles_of(P.N, kSegThreads), kSegThreads, 0, s>>>(eoff, P.N, eidx, sgiants,
+                                                                                     nsgiant, errw);
+          }));
+        MN_CUDA(launch("segsort_giant", 0.0, s, [&] {
+          k_segsort_giant<<<148, 1024, scap * 4, s>>>(eoff, eidx, sgiants, nsgiant, scap, errw);
+        }));
+      }
     } else {
     // ---- a1/a2 validation + digit histograms of the node ids ----
     MN_CUDA(launch("hist_validate", 4.0 * P.K * P.M, s, [&] {
@@ -632,17 +634,15 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       // ---- a1 + a3n + a4 (nodes): expand the element CSR per node, sort + dedupe per node ----
       uint32_t* temp = ekA;   // C * Pe <= 4 * Pe entries: the dead element-sort buffers
       const double gb = 8.0 * (P.N + 1) + 4.0 * P.Pe + 4.0 * P.K * P.Pe;   // offsets, incidences, rows
-      if (P.N == 0) {
-        // M > 0 with N == 0 always fails validation: nothing to expand
-      } else if (aligned) {
+      const unsigned ng = (unsigned)tiles_of(P.N, kNodeThreads);
+      if (P.N > 0) {   // (M > 0 with N == 0 always fails validation: nothing to expand)
         MN_CUDA(launch("node_gather", gb, s, [&] {
-          k_node_gather_t<T, true><<<(unsigned)tiles_of(P.N, kNodeThreads), kNodeThreads, 0, s>>>(
-              eoff, eidx, conn, P.N, temp, cnt, lofs, giants, ngiant, errw);
-        }));
-      } else {
-        MN_CUDA(launch("node_gather", gb, s, [&] {
-          k_node_gather_t<T, false><<<(unsigned)tiles_of(P.N, kNodeThreads), kNodeThreads, 0, s>>>(
-              eoff, eidx, conn, P.N, temp, cnt, lofs, giants, ngiant, errw);
+          if (aligned)
+            k_node_gather_t<T, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, conn, P.N, temp, cnt, lofs, giants,
+                                                                 ngiant, errw);
+          else
+            k_node_gather_t<T, false><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, conn, P.N, temp, cnt, lofs, giants,
+                                                                  ngiant, errw);
         }));
       }
       const int cap = 48 * 1024;   // uint32 entries sorted in shared memory by k_node_giant (192 KB)
