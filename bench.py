@@ -30,7 +30,7 @@ FALLBACK_HBM_GBS = 6650.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -60,22 +60,24 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []          # (host time, csv line)
+        self.window = None       # (t0, t1) of the timed region, host clock
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.3)      # let the sampler start before the timed region
         except OSError:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *a):
         if self.proc:
@@ -87,18 +89,25 @@ class ClockSampler:
 
     def summary(self):
         rows = []
-        for ln in self.lines:
+        for ts, ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
             try:
-                rows.append((float(f[1]), float(f[2]), float(f[3]), f[4:8]))
+                rows.append((float(f[1]), float(f[2]), float(f[3]), f[4:8], ts))
             except ValueError:
                 continue
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        if self.window:
+            t0, t1 = self.window
+            inside = [r for r in rows if t0 <= r[4] <= t1]
+            if len(inside) < 3:   # a short timed region: the samples nearest to it
+                mid = 0.5 * (t0 + t1)
+                inside = sorted(rows, key=lambda r: abs(r[4] - mid))[:3]
+            rows = inside
         pmax = max(r[2] for r in rows)
-        load = [r for r in rows if r[2] >= 0.5 * pmax] or rows
+        load = rows
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in load for i, v in enumerate(r[3]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": max(r[1] for r in rows),
@@ -270,12 +279,14 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        t_host0 = time.time()
         ev0.record(s)
         for _ in range(args.steps):
             r = step()
             del r
         ev1.record(s)
         torch.cuda.synchronize()
+        clk.window = (t_host0, time.time())
     barrier()
     launches = mn.launch_count() - launches0
     mn.profile_enable(False)

@@ -735,10 +735,14 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
 #pragma unroll
       for (int q = 0; q < B; ++q) {
         if (e[q] < 0) continue;
-        const int p = local_of<T>(row[q], (int)a);
+        // simplices (TRI3, TET4): every other node of the element is an edge neighbour, so the
+        // candidates are the row values != a; otherwise the local neighbour table is used
+        constexpr bool simplex = (C == K - 1);
+        const int p = simplex ? 0 : local_of<T>(row[q], (int)a);
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-          const uint32_t v = pick<T>(row[q], nbr_local<T>(p, c));
+        for (int c = 0; c < (simplex ? K : C); ++c) {
+          const uint32_t v = simplex ? (uint32_t)row[q][c] : pick<T>(row[q], nbr_local<T>(p, c));
+          if (simplex && v == (uint32_t)a) continue;
           uint32_t h = (v * 0x9E3779B1u) >> 27;
           while (L <= kMaxUnique) {   // at most kMaxUnique + 1 entries: the set never fills
             const uint32_t x = tab[h][t];
