@@ -187,32 +187,37 @@ mn_status mn_exclusive_scan_i32(const int32_t* d_counts, int64_t n, int64_t* d_o
 
 /* ---------------------------------------------------------------------------------------------
  * Multi-GPU building blocks: nodes are owned in contiguous ranges
- * [r*ceil(N/G), (r+1)*ceil(N/G)); each rank holds an element shard with global element base.
- * The exchange between the two calls is done by the caller (torch.distributed all_to_all over
- * NCCL / NVLink); see paper_1604_04689_b200/dist.py.
+ * [r*ceil(N/G), (r+1)*ceil(N/G)); each rank holds an element shard with a global element base.
+ * Only incidences travel: the owner of node a receives every (a, e) pair together with e's row,
+ * which is all it needs for both CSR slices (the node pairs of a are the expansion of a's element
+ * list).  The exchange between the two calls is done by the caller
+ * (torch.distributed all_to_all over NCCL / NVLink); see paper_1604_04689_b200/dist.py.
  * ------------------------------------------------------------------------------------------- */
 
-/* Validate the shard and bucket its node pairs and element pairs by owner rank.  Writes, for
- * each destination rank g (0 <= g < world), the pairs it owns, contiguously in rank order:
- *   d_node_keys: packed (a << b | v) uint64 keys, b = mn_node_key_bits(num_nodes), sorted by
- *                owner, creation order kept inside each bucket;
- *   d_elem_pairs: uint64 (node << 32 | global element id), same bucketing, creation order kept
- *                (element-major, so each bucket is ascending in element id per node);
- *   h_node_counts[g], h_elem_counts[g]: pair counts per destination (host, world entries).
- * Buffers hold 2*E*shard_elems and arity*shard_elems entries.  Blocks once. */
+/* Validate the shard (error element ids are global) and bucket its incidences by owner rank,
+ * stably, so each bucket stays element-major:
+ *   d_pairs[i]        uint64 (node << 32 | global element id), arity*shard_elems entries (caller);
+ *   h_counts[g]       incidences destined to rank g (host, world entries);
+ *   *d_row_elems, *d_rows  (allocated here from `alloc`, released by the caller): one row per
+ *                     distinct (destination g != self_rank, element) pair, grouped by destination,
+ *                     element ids ascending within a group — the remote rows the owners need;
+ *   h_row_counts[g]   rows destined to rank g (0 for self_rank).  Blocks once. */
 mn_status mn_dist_bucket(mn_elem_type type, const int32_t* d_conn_shard, int64_t shard_elems,
-                         int64_t global_elem_base, int64_t num_nodes, int world,
-                         uint64_t* d_node_keys, uint64_t* d_elem_pairs, int64_t* h_node_counts,
-                         int64_t* h_elem_counts, const mn_allocator* alloc, mn_stream stream,
+                         int64_t global_elem_base, int64_t num_nodes, int world, int self_rank,
+                         uint64_t* d_pairs, int64_t* h_counts, int32_t** d_row_elems, int32_t** d_rows,
+                         int64_t* h_row_counts, const mn_allocator* alloc, mn_stream stream,
                          mn_error_detail* err);
 
-/* Finish on the owner: from the received node keys (any order) and element pairs (concatenated
- * in source-rank order, so element ids ascend per node), build the CSR slice of nodes [lo, hi):
- * offsets are local (slice offsets[0] = 0), indices global node / element ids. */
-mn_status mn_dist_finish(const uint64_t* d_node_keys, int64_t n_node_keys,
-                         const uint64_t* d_elem_pairs, int64_t n_elem_pairs, int64_t num_nodes,
-                         int64_t lo, int64_t hi, const mn_allocator* alloc, mn_stream stream,
-                         mn_csr* node_slice, mn_csr* elem_slice);
+/* Owner side: from the n received incidences (concatenated in source-rank order, so element ids
+ * ascend per node) and the n_rows received remote rows (element ids ascending), build the CSR
+ * slices of nodes [lo, hi): local offsets (slice offsets[0] = 0), global node / element ids as
+ * indices.  Rows of local elements are read from the own shard (d_conn_shard, shard_elems,
+ * global_elem_base).  Blocks once (node nnz). */
+mn_status mn_dist_finish(mn_elem_type type, const uint64_t* d_pairs, int64_t n, const int32_t* d_row_elems,
+                         const int32_t* d_rows, int64_t n_rows, const int32_t* d_conn_shard,
+                         int64_t shard_elems, int64_t global_elem_base, int64_t num_nodes, int64_t lo,
+                         int64_t hi, const mn_allocator* alloc, mn_stream stream, mn_csr* node_slice,
+                         mn_csr* elem_slice);
 
 /* ---------------------------------------------------------------------------------------------
  * Algorithm selection for the element CSR (process-wide; results are identical either way).

@@ -97,10 +97,10 @@ def _declare(lib):
         "mn_unique_node_csr": (S, [_VP, _INT, _I64, _I64, _VP, _VP, _P(_I64), _P(_Allocator), _VP]),
         "mn_elem_offsets": (S, [_VP, _I64, _I64, _VP, _VP]),
         "mn_exclusive_scan_i32": (S, [_VP, _I64, _VP, _P(_Allocator), _VP]),
-        "mn_dist_bucket": (S, [_INT, _VP, _I64, _I64, _I64, _INT, _VP, _VP, _P(_I64), _P(_I64),
-                               _P(_Allocator), _VP, _P(_ErrDetail)]),
-        "mn_dist_finish": (S, [_VP, _I64, _VP, _I64, _I64, _I64, _I64, _P(_Allocator), _VP, _P(_Csr),
-                               _P(_Csr)]),
+        "mn_dist_bucket": (S, [_INT, _VP, _I64, _I64, _I64, _INT, _INT, _VP, _P(_I64), _P(_VP), _P(_VP),
+                               _P(_I64), _P(_Allocator), _VP, _P(_ErrDetail)]),
+        "mn_dist_finish": (S, [_INT, _VP, _I64, _VP, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _I64,
+                               _P(_Allocator), _VP, _P(_Csr), _P(_Csr)]),
         "mn_launch_count": (_I64, []),
         "mn_set_elem_path": (S, [_INT]),
         "mn_get_elem_path": (_INT, []),
@@ -417,35 +417,46 @@ def exclusive_scan(counts: torch.Tensor, stream=None) -> torch.Tensor:
 # ------------------------------------------------------------------------------------------------
 # multi-GPU building blocks (orchestrated by paper_1604_04689_b200.dist)
 # ------------------------------------------------------------------------------------------------
-def dist_bucket(conn_shard: torch.Tensor, etype, global_elem_base: int, num_nodes: int, world: int, stream=None):
-    """Bucket this shard's node pairs and element pairs by owner rank.
-    Returns (node_keys int64, node_counts[world], elem_pairs int64, elem_counts[world])."""
+def dist_bucket(conn_shard: torch.Tensor, etype, global_elem_base: int, num_nodes: int, world: int,
+                self_rank: int, stream=None):
+    """Bucket this shard's incidences by owner rank.  Returns (pairs int64[k*M] = node << 32 |
+    element, counts[world], row_elems int32[R], rows int32[R, k], row_counts[world]): the remote
+    rows, one per (destination != self_rank, element), grouped by destination."""
     et = _etype(etype)
     c, M = _conn_arg(conn_shard, et)
-    E = {TRI3: 3, QUAD4: 4, TET4: 6, HEX8: 12}[et]
-    nk = torch.empty(2 * E * M, dtype=torch.int64, device=c.device)
-    ep = torch.empty(ARITY[et] * M, dtype=torch.int64, device=c.device)
-    hn = (ctypes.c_int64 * world)()
-    he = (ctypes.c_int64 * world)()
+    k = ARITY[et]
+    pairs = torch.empty(k * M, dtype=torch.int64, device=c.device)
+    hc = (ctypes.c_int64 * world)()
+    hrc = (ctypes.c_int64 * world)()
+    pe, pr = ctypes.c_void_p(), ctypes.c_void_p()
     al = _TorchAllocator(c.device)
     err = _ErrDetail()
     with torch.cuda.device(c.device):
         rc = load().mn_dist_bucket(et, c.data_ptr(), M, int(global_elem_base), int(num_nodes), int(world),
-                                   nk.data_ptr(), ep.data_ptr(), hn, he, ctypes.byref(al.struct),
-                                   _stream_ptr(stream), ctypes.byref(err))
+                                   int(self_rank), pairs.data_ptr(), hc, ctypes.byref(pe), ctypes.byref(pr), hrc,
+                                   ctypes.byref(al.struct), _stream_ptr(stream), ctypes.byref(err))
     _check(rc, err)
-    return nk, list(hn), ep, list(he)
+    R = sum(hrc)
+    relems = al.adopt(pe.value, R, torch.int32)
+    rows = al.adopt(pr.value, R * k, torch.int32).view(R, k)
+    return pairs, list(hc), relems, rows, list(hrc)
 
 
-def dist_finish(node_keys: torch.Tensor, elem_pairs: torch.Tensor, num_nodes: int, lo: int, hi: int, stream=None):
-    """CSR slices of the owned node range [lo, hi) from the received pairs."""
-    dev = node_keys.device
+def dist_finish(etype, pairs: torch.Tensor, row_elems: torch.Tensor, rows: torch.Tensor, conn_shard: torch.Tensor,
+                global_elem_base: int, num_nodes: int, lo: int, hi: int, stream=None):
+    """CSR slices (node, element) of the owned node range [lo, hi) from the received incidences,
+    the received remote rows and the own shard."""
+    et = _etype(etype)
+    dev = pairs.device
     al = _TorchAllocator(dev)
     ns, es = _Csr(), _Csr()
+    rows = rows.contiguous()
+    shard = conn_shard.contiguous()
+    ptr = lambda t: t.data_ptr() if t.numel() else None  # noqa: E731
     with torch.cuda.device(dev):
-        rc = load().mn_dist_finish(node_keys.data_ptr() if node_keys.numel() else None, node_keys.numel(),
-                                   elem_pairs.data_ptr() if elem_pairs.numel() else None, elem_pairs.numel(),
-                                   int(num_nodes), int(lo), int(hi), ctypes.byref(al.struct), _stream_ptr(stream),
+        rc = load().mn_dist_finish(et, ptr(pairs), pairs.numel(), ptr(row_elems), ptr(rows), row_elems.numel(),
+                                   ptr(shard), shard.numel() // ARITY[et], int(global_elem_base), int(num_nodes),
+                                   int(lo), int(hi), ctypes.byref(al.struct), _stream_ptr(stream),
                                    ctypes.byref(ns), ctypes.byref(es))
     _check(rc)
     return _take(al, ns), _take(al, es)

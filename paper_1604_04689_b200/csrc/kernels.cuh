@@ -634,6 +634,31 @@ __device__ __forceinline__ void load_row(const int32_t* __restrict__ conn, int64
   }
 }
 
+// Where element rows come from: the whole connectivity (1 GPU: base 0, M = all elements), or for
+// a multi-GPU owner its own shard [base, base + M) plus a table of received remote rows whose
+// element ids `relems` ascend (binary search).
+struct RowSrc {
+  const int32_t* conn;
+  int64_t base, M;
+  const int32_t* relems;
+  const int32_t* rrows;
+  int64_t nr;
+};
+
+template <int T, bool ALIGNED, bool DIST>
+__device__ __forceinline__ void fetch_row(const RowSrc& rs, int64_t e, int (&row)[Elem<T>::K]) {
+  if (!DIST || (e >= rs.base && e < rs.base + rs.M)) {
+    load_row<T, ALIGNED>(rs.conn, e - rs.base, row);
+    return;
+  }
+  int64_t lo = 0, hi = rs.nr - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)rs.relems[mid] < e) lo = mid + 1; else hi = mid;
+  }
+  load_row<T, ALIGNED>(rs.rrows, lo, row);
+}
+
 template <int T>
 __device__ __forceinline__ int local_of(const int (&row)[Elem<T>::K], int a) {
   int p = 0;
@@ -698,13 +723,13 @@ constexpr int kMaxUnique = 24;
 // (Fusing the element-list sort of the transpose path into this kernel, with the CTA's incidence
 // range staged in shared memory, was measured slower on B200: the extra registers / shared memory
 // cost more occupancy than the saved pass.)
-template <int T, bool ALIGNED>
+template <int T, bool ALIGNED, bool DIST = false>
 __global__ void __launch_bounds__(kNodeThreads)
-k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, const int32_t* __restrict__ conn,
+k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, RowSrc rs,
                 int64_t N, uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, int32_t* __restrict__ lofs,
                 uint32_t* __restrict__ giants, unsigned int* __restrict__ ngiant,
-                const unsigned long long* __restrict__ err) {
-  constexpr int C = Elem<T>::C, K = Elem<T>::K, B = 4;
+                const unsigned long long* __restrict__ err, int64_t a_base = 0) {
+  constexpr int C = Elem<T>::C, K = Elem<T>::K, B = 4;   // incidences in flight per thread
   constexpr uint32_t EMPTY = 0xFFFFFFFFu;
   __shared__ uint32_t tab[kHashSlots][kNodeThreads];
   __shared__ uint32_t lst[kMaxUnique + 1][kNodeThreads];
@@ -731,18 +756,18 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
       int row[B][K];
 #pragma unroll
       for (int q = 0; q < B; ++q)
-        if (e[q] >= 0) load_row<T, ALIGNED>(conn, e[q], row[q]);
+        if (e[q] >= 0) fetch_row<T, ALIGNED, DIST>(rs, e[q], row[q]);
 #pragma unroll
       for (int q = 0; q < B; ++q) {
         if (e[q] < 0) continue;
         // simplices (TRI3, TET4): every other node of the element is an edge neighbour, so the
         // candidates are the row values != a; otherwise the local neighbour table is used
         constexpr bool simplex = (C == K - 1);
-        const int p = simplex ? 0 : local_of<T>(row[q], (int)a);
+        const int p = simplex ? 0 : local_of<T>(row[q], (int)(a + a_base));
 #pragma unroll
         for (int c = 0; c < (simplex ? K : C); ++c) {
           const uint32_t v = simplex ? (uint32_t)row[q][c] : pick<T>(row[q], nbr_local<T>(p, c));
-          if (simplex && v == (uint32_t)a) continue;
+          if (simplex && v == (uint32_t)(a + a_base)) continue;
           uint32_t h = (v * 0x9E3779B1u) >> 27;
           while (L <= kMaxUnique) {   // at most kMaxUnique + 1 entries: the set never fills
             const uint32_t x = tab[h][t];
@@ -797,12 +822,12 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
 // Nodes with more than 256 raw neighbour entries (or more than 32 distinct neighbours): one CTA per
 // node, the raw entries sorted with a block bitonic network (shared memory when they fit, else in
 // place in the node's global raw region), then adjacent-difference dedupe.
-template <int T, bool ALIGNED>
+template <int T, bool ALIGNED, bool DIST = false>
 __global__ void __launch_bounds__(1024)
-k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, const int32_t* __restrict__ conn,
+k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, RowSrc rs,
              uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, const int32_t* __restrict__ lofs,
              const uint32_t* __restrict__ giants, const unsigned int* __restrict__ ngiant, int smem_cap,
-             const unsigned long long* __restrict__ err) {
+             const unsigned long long* __restrict__ err, int64_t a_base = 0) {
   constexpr int C = Elem<T>::C, K = Elem<T>::K;
   extern __shared__ uint32_t sv[];
   __shared__ int s_u;
@@ -818,8 +843,8 @@ k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx,
     uint32_t* buf = raw <= smem_cap ? sv : out;
     for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
       int row[K];
-      load_row<T, ALIGNED>(conn, eidx[s + i], row);
-      const int p = local_of<T>(row, (int)a);
+      fetch_row<T, ALIGNED, DIST>(rs, eidx[s + i], row);
+      const int p = local_of<T>(row, (int)(a + a_base));
 #pragma unroll
       for (int c = 0; c < C; ++c) buf[i * C + c] = pick<T>(row, nbr_local<T>(p, c));
     }
@@ -1209,25 +1234,108 @@ k_emit_elem(const int32_t* __restrict__ conn, int64_t P, uint32_t* __restrict__ 
   }
 }
 
-// Multi-GPU finish: rebase received pairs onto the local node range.
+// Multi-GPU bucketing: mark, in bucket order, the first incidence of each element inside a bucket
+// destined to another rank (flags[j] = 1): those elements' rows travel with the pairs.
 __global__ void __launch_bounds__(256)
-k_rebase_node(const uint64_t* __restrict__ in, int64_t n, int b, int64_t lo, uint64_t* __restrict__ out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = in[i];
-    const uint64_t a = (k >> b) - (uint64_t)lo;
-    out[i] = (a << b) | (k & ((1ull << b) - 1));
+k_mark_remote_rows(const uint64_t* __restrict__ pairs, int64_t n, uint64_t chunk, int world, int self,
+                   int32_t* __restrict__ flags, const unsigned long long* __restrict__ err) {
+  if (*err != ERR_NONE) return;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = pairs[j];
+    uint64_t g = (p >> 32) / chunk;
+    g = g < (uint64_t)world ? g : (uint64_t)world - 1;
+    bool f = (int)g != self;
+    if (f && j > 0) {
+      const uint64_t q = pairs[j - 1];
+      uint64_t gq = (q >> 32) / chunk;
+      gq = gq < (uint64_t)world ? gq : (uint64_t)world - 1;
+      f = !(gq == g && (q & 0xffffffffull) == (p & 0xffffffffull));
+    }
+    flags[j] = f ? 1 : 0;
+  }
+}
+
+// Rows per destination: differences of the flag scan at the bucket boundaries (bases[g] = first
+// incidence of bucket g).
+__global__ void k_row_counts(const int64_t* __restrict__ pos, const uint64_t* __restrict__ bases, int world,
+                             int64_t n, unsigned long long* __restrict__ rcnt) {
+  const int g = threadIdx.x;
+  if (g < world) {
+    const int64_t b0 = (int64_t)bases[g], b1 = g + 1 < world ? (int64_t)bases[g + 1] : n;
+    rcnt[g] = (unsigned long long)(pos[b1] - pos[b0]);
+  }
+}
+
+template <int T>
+__global__ void __launch_bounds__(256)
+k_emit_remote_rows(const uint64_t* __restrict__ pairs, const int32_t* __restrict__ flags,
+                   const int64_t* __restrict__ pos, int64_t n, const int32_t* __restrict__ conn, int64_t elem_base,
+                   int32_t* __restrict__ relems, int32_t* __restrict__ rrows, const unsigned long long* __restrict__ err) {
+  constexpr int K = Elem<T>::K;
+  if (*err != ERR_NONE) return;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    if (!flags[j]) continue;
+    const int64_t o = pos[j];
+    const int64_t e = (int64_t)(pairs[j] & 0xffffffffull);
+    relems[o] = (int32_t)e;
+#pragma unroll
+    for (int q = 0; q < K; ++q) rrows[o * K + q] = __ldg(conn + (e - elem_base) * K + q);
+  }
+}
+
+// Multi-GPU finish, transpose form (received pairs are element-major, i.e. as coherent as conn):
+// distinct nodes per window of 32 consecutive pairs (locality sample), per-node counts, and the
+// warp-aggregated scatter of element ids (sorted per node afterwards by k_elem_segsort).
+__global__ void __launch_bounds__(256)
+k_pairs_locality(const uint64_t* __restrict__ pairs, int64_t n, unsigned long long* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t j = (int64_t)((double)n * (double)gw / (double)nw) + lane;
+  const bool in = j < n;
+  const int64_t x = in ? (int64_t)(pairs[j] >> 32) : -1 - lane;
+  const unsigned peers = __match_any_sync(FULL, (unsigned long long)x);
+  const unsigned g = __reduce_add_sync(FULL, (in && lane == __ffs(peers) - 1) ? 1u : 0u);
+  const unsigned act = __popc(__ballot_sync(FULL, in));
+  if (lane == 0) {
+    atomicAdd(out, (unsigned long long)g);
+    atomicAdd(out + 1, (unsigned long long)act);
   }
 }
 
 __global__ void __launch_bounds__(256)
-k_split_elem(const uint64_t* __restrict__ in, int64_t n, int64_t lo, uint32_t* __restrict__ keys,
-             uint32_t* __restrict__ vals) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = in[i];
-    keys[i] = (uint32_t)((int64_t)(k >> 32) - lo);
-    vals[i] = (uint32_t)(k & 0xffffffffull);
+k_pairs_count(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, int32_t* __restrict__ cnt) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + ((int64_t)(pairs[j] >> 32) - lo), 1);
+}
+
+__global__ void __launch_bounds__(256)
+k_pairs_scatter(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, const int64_t* __restrict__ eoff,
+                int32_t* __restrict__ cursor, int32_t* __restrict__ eidx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
+    const int64_t j = base + lane;
+    const bool in = j < n;
+    const uint64_t p = in ? pairs[j] : 0;
+    const int64_t a = in ? (int64_t)(p >> 32) - lo : -1 - lane;
+    const unsigned peers = __match_any_sync(FULL, (unsigned long long)a);
+    const int leader = __ffs(peers) - 1;
+    int b = 0;
+    if (in && lane == leader) b = atomicAdd(cursor + a, (int)__popc(peers));
+    b = __shfl_sync(FULL, b, leader);
+    if (in) eidx[eoff[a] + b + __popc(peers & lanemask_lt())] = (int32_t)(p & 0xffffffffull);
+  }
+}
+
+// Multi-GPU finish: local node key and element-id payload of every received pair.
+__global__ void __launch_bounds__(256)
+k_local_keys(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, uint32_t* __restrict__ keys,
+             uint32_t* __restrict__ elems) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = pairs[i];
+    keys[i] = (uint32_t)((int64_t)(p >> 32) - lo);
+    elems[i] = (uint32_t)(p & 0xffffffffull);
   }
 }
 

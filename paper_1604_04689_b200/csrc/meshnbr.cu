@@ -637,11 +637,12 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       const unsigned ng = (unsigned)tiles_of(P.N, kNodeThreads);
       if (P.N > 0) {   // (M > 0 with N == 0 always fails validation: nothing to expand)
         MN_CUDA(launch("node_gather", gb, s, [&] {
+          const RowSrc rs{conn, 0, P.M, nullptr, nullptr, 0};
           if (aligned)
-            k_node_gather_t<T, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, conn, P.N, temp, cnt, lofs, giants,
+            k_node_gather_t<T, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs, giants,
                                                                  ngiant, errw);
           else
-            k_node_gather_t<T, false><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, conn, P.N, temp, cnt, lofs, giants,
+            k_node_gather_t<T, false><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs, giants,
                                                                   ngiant, errw);
         }));
       }
@@ -653,8 +654,9 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
         giant_attr = true;
       }
       MN_CUDA(launch("node_giant", 0.0, s, [&] {
-        if (aligned) k_node_giant<T, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, conn, temp, cnt, lofs, giants, ngiant, cap, errw);
-        else k_node_giant<T, false><<<148, 1024, cap * 4, s>>>(eoff, eidx, conn, temp, cnt, lofs, giants, ngiant, cap, errw);
+        const RowSrc rs{conn, 0, P.M, nullptr, nullptr, 0};
+        if (aligned) k_node_giant<T, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw);
+        else k_node_giant<T, false><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw);
       }));
       // ---- a5 (nodes): exclusive scan of the unique counts -> offsets ----
       if (P.N > 0)   // N == 0 with M > 0 always fails validation; nothing to scan
@@ -916,67 +918,259 @@ done:
 // multi-GPU bucketing: stable owner partition fused with pair creation (one onesweep pass each)
 // ================================================================================================
 template <int T, int BINS>
-static mn_status dist_bucket_impl(const int32_t* conn, int64_t M, int64_t base, int64_t N, int world,
-                                  uint64_t* nkeys, uint64_t* epairs, int64_t* hn, int64_t* he,
-                                  Mem& mem, mn_error_detail* err) {
+static mn_status dist_bucket_impl(const int32_t* conn, int64_t M, int64_t base, int64_t N, int world, int self,
+                                  uint64_t* pairs, int64_t* hc, int32_t** relems_out, int32_t** rrows_out,
+                                  int64_t* hrc, Mem& mem, mn_error_detail* err) {
   cudaStream_t s = mem.s;
   mn_status st = MN_OK;
   uint64_t* host = pinned_pair();
   if (!host) return MN_ERR_CUDA;
   const Plan P = make_plan(T, M, N);
   const uint64_t chunk = (uint64_t)((N + world - 1) / world > 0 ? (N + world - 1) / world : 1);
-  const int64_t tiles = std::max(tiles_of(P.Pn, kTile), tiles_of(P.Pe, kTile));
-  std::vector<unsigned long long> hh(BINS);
+  const int64_t tiles = tiles_of(P.Pe, kTile);
+  std::vector<unsigned long long> hh(BINS), hr(BINS);
+  int32_t *relems = nullptr, *rrows = nullptr;
+  int64_t R = 0;
   Arena ar;
-  unsigned long long* errw = ar.take<unsigned long long>(1);
+  unsigned long long* errw = ar.take<unsigned long long>(2);
   uint32_t* tickets = ar.take<uint32_t>(8);
   unsigned long long* hist = ar.take<unsigned long long>(BINS);
-  uint64_t* bases = ar.take<uint64_t>(2 * BINS);
+  unsigned long long* rcnt = ar.take<unsigned long long>(BINS);
+  uint64_t* bases = ar.take<uint64_t>(BINS);
   uint64_t* status = ar.take<uint64_t>((size_t)(tiles ? tiles : 1) * BINS);
+  uint64_t* sstatus = ar.take<uint64_t>((size_t)tiles_of(P.Pe, kScanTile) + 1);
+  const size_t head = ar.off;
+  int32_t* flags = ar.take<int32_t>((size_t)P.Pe + 1);
+  int64_t* pos = ar.take<int64_t>((size_t)P.Pe + 1);
   void* ws = mem.get(ar.off);
   if (!ws) return MN_ERR_OOM;
   {
     char* bb = (char*)ws;
-    errw = (unsigned long long*)(bb + (size_t)errw);
-    tickets = (uint32_t*)(bb + (size_t)tickets);
-    hist = (unsigned long long*)(bb + (size_t)hist);
-    bases = (uint64_t*)(bb + (size_t)bases);
-    status = (uint64_t*)(bb + (size_t)status);
-    MN_CUDA(cudaMemsetAsync(ws, 0, ar.off, s));
+    auto fix = [&](auto* q) { return (decltype(q))(bb + (size_t)q); };
+    errw = fix(errw); tickets = fix(tickets); hist = fix(hist); rcnt = fix(rcnt); bases = fix(bases);
+    status = fix(status); sstatus = fix(sstatus); flags = fix(flags); pos = fix(pos);
+    MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
     MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
     if (M > 0) {
+      // validation + incidence counts per owner rank
       MN_CUDA(launch("hist_validate", 4.0 * P.K * M, s, [&] {
         k_hist_validate<T, BINS, false><<<hist_grid(M), 256, 0, s>>>(conn, M, N, base, P.dp, 1, chunk, hist, errw);
       }));
       BasesDesc bd{};
-      bd.npass = 2;
-      bd.hidx[0] = 0; bd.mult[0] = P.C;
-      bd.hidx[1] = 0; bd.mult[1] = 1;
-      MN_CUDA(launch("bucket_bases", 0.0, s, [&] { k_bucket_bases<BINS><<<2, BINS, 0, s>>>(hist, bd, bases, errw); }));
-      PassArgs pa{};
-      pa.keys_out = nkeys; pa.conn = conn; pa.node_bits = P.b; pa.n = P.Pn;
-      pa.pd.shift = P.b; pa.pd.div = chunk; pa.pd.mask = 0;
-      pa.bases = bases; pa.status = status; pa.ticket = tickets; pa.epoch = 1; pa.err = errw;
-      MN_CUDA((run_pass<uint64_t, 1, T, false, true, BINS>(pa, s, "bucket_node", 4.0 * P.K * M + 8.0 * P.Pn)));
+      bd.npass = 1;
+      bd.hidx[0] = 0;
+      bd.mult[0] = 1;
+      MN_CUDA(launch("bucket_bases", 0.0, s, [&] { k_bucket_bases<BINS><<<1, BINS, 0, s>>>(hist, bd, bases, errw); }));
+      // (node << 32 | global element) pairs created from conn, stably bucketed by owner
       PassArgs pe{};
-      pe.keys_out = epairs; pe.conn = conn; pe.elem_base = base; pe.n = P.Pe;
+      pe.keys_out = pairs; pe.conn = conn; pe.elem_base = base; pe.n = P.Pe;
       pe.pd.shift = 32; pe.pd.div = chunk; pe.pd.mask = 0;
-      pe.bases = bases + BINS; pe.status = status; pe.ticket = tickets + 1; pe.epoch = 2; pe.err = errw;
-      MN_CUDA((run_pass<uint64_t, 3, T, false, true, BINS>(pe, s, "bucket_elem", 4.0 * P.Pe + 8.0 * P.Pe)));
+      pe.bases = bases; pe.status = status; pe.ticket = tickets; pe.epoch = 1; pe.err = errw;
+      MN_CUDA((run_pass<uint64_t, 3, T, false, true, BINS>(pe, s, "bucket_incidences", 4.0 * P.Pe + 8.0 * P.Pe)));
+      // one row per (remote destination, element): the owner reads local rows from its own shard
+      MN_CUDA(launch("mark_remote_rows", 16.0 * P.Pe, s, [&] {
+        k_mark_remote_rows<<<stream_grid(P.Pe), 256, 0, s>>>(pairs, P.Pe, chunk, world, self, flags, errw);
+      }));
+      MN_CUDA(launch("scan_counts", 12.0 * P.Pe, s, [&] {
+        k_scan_i32<kThreads, kScanItems><<<(unsigned)tiles_of(P.Pe, kScanTile), kThreads, 0, s>>>(
+            flags, P.Pe, pos, sstatus, tickets + 1, 1);
+      }));
+      MN_CUDA(launch("row_counts", 0.0, s, [&] { k_row_counts<<<1, 512, 0, s>>>(pos, bases, world, P.Pe, rcnt); }));
+      MN_CUDA(cudaMemcpyAsync(host + 1, pos + P.Pe, 8, cudaMemcpyDeviceToHost, s));
     }
     MN_CUDA(cudaMemcpyAsync(hh.data(), hist, BINS * 8, cudaMemcpyDeviceToHost, s));
+    MN_CUDA(cudaMemcpyAsync(hr.data(), rcnt, BINS * 8, cudaMemcpyDeviceToHost, s));
     MN_CUDA(cudaMemcpyAsync(host, errw, 8, cudaMemcpyDeviceToHost, s));
     MN_CUDA(cudaStreamSynchronize(s));
     st = decode_err(host[0], err);
-    if (st == MN_OK) {
-      for (int g = 0; g < world; ++g) {
-        hn[g] = (int64_t)hh[g] * P.C;
-        he[g] = (int64_t)hh[g];
-      }
+    if (st != MN_OK) goto done;
+    R = M > 0 ? (int64_t)host[1] : 0;
+    for (int g = 0; g < world; ++g) {
+      hc[g] = (int64_t)hh[g];
+      hrc[g] = (int64_t)hr[g];
     }
+    if (R > 0) {
+      relems = (int32_t*)mem.get((size_t)R * 4);
+      rrows = (int32_t*)mem.get((size_t)R * P.K * 4);
+      if (!relems || !rrows) { st = MN_ERR_OOM; goto done; }
+      MN_CUDA(launch("emit_remote_rows", 8.0 * P.Pe + 4.0 * (P.K + 1) * R, s, [&] {
+        k_emit_remote_rows<T><<<stream_grid(P.Pe), 256, 0, s>>>(pairs, flags, pos, P.Pe, conn, base, relems, rrows,
+                                                               errw);
+      }));
+    }
+    *relems_out = relems;
+    *rrows_out = rrows;
+    relems = rrows = nullptr;
   }
 done:
+  mem.put(relems);
+  mem.put(rrows);
   mem.put(ws);
+  return st;
+}
+
+// Owner-side finish: element CSR slice by a stable sort of the received incidences on the local
+// node id (source-rank order keeps element ids ascending; the element ids are the sort payload and
+// become the indices in place), node CSR slice by the same per-node expansion + dedupe as the
+// single-GPU path, rows read from the own shard or, for remote elements, the received row table.
+template <int T>
+static mn_status dist_finish_impl(const uint64_t* pairs, int64_t n, const int32_t* relems, const int32_t* rrows,
+                                  int64_t nr, const int32_t* shard, int64_t shard_base, int64_t shard_m, int64_t N,
+                                  int64_t lo, int64_t hi, Mem& mem, mn_csr* node_slice, mn_csr* elem_slice) {
+  cudaStream_t s = mem.s;
+  mn_status st = MN_OK;
+  constexpr int K = Elem<T>::K, C = Elem<T>::C;
+  uint64_t* host = pinned_pair();
+  if (!host) return MN_ERR_CUDA;
+  const int64_t nloc = hi - lo;
+  const int bl = node_bits(nloc);
+  std::memset(node_slice, 0, sizeof(*node_slice));
+  std::memset(elem_slice, 0, sizeof(*elem_slice));
+  int64_t* noff = (int64_t*)mem.get((size_t)(nloc + 1) * 8);
+  int64_t* eoff = (int64_t*)mem.get((size_t)(nloc + 1) * 8);
+  int32_t* eidx = n ? (int32_t*)mem.get((size_t)n * 4) : nullptr;
+  void* ws = nullptr;
+  if (!noff || !eoff || (n && !eidx)) { st = MN_ERR_OOM; goto done; }
+  if (n == 0) {
+    MN_CUDA(cudaMemsetAsync(noff, 0, (size_t)(nloc + 1) * 8, s));
+    MN_CUDA(cudaMemsetAsync(eoff, 0, (size_t)(nloc + 1) * 8, s));
+    MN_CUDA(cudaStreamSynchronize(s));
+  } else {
+    Arena ar;
+    unsigned long long* errw = ar.take<unsigned long long>(2);
+    unsigned long long* smp = ar.take<unsigned long long>(2);
+    uint32_t* tickets = ar.take<uint32_t>(8);
+    unsigned int* ngiant = ar.take<unsigned int>(1);
+    uint64_t* sstatus = ar.take<uint64_t>((size_t)tiles_of(nloc, kScanTile) + 1);
+    int32_t* cnt = ar.take<int32_t>((size_t)nloc + 1);    // zeroed: counts of the transpose
+    int32_t* lofs = ar.take<int32_t>((size_t)nloc + 1);   // zeroed: cursors of the transpose
+    const size_t head = ar.off;
+    uint32_t* keys = ar.take<uint32_t>((size_t)n);
+    uint32_t* temp = ar.take<uint32_t>((size_t)C * n);
+    uint32_t* giants = ar.take<uint32_t>((size_t)nloc + 1);
+    ws = mem.get(ar.off);
+    if (!ws) { st = MN_ERR_OOM; goto done; }
+    {
+      char* bb = (char*)ws;
+      auto fix = [&](auto* q) { return (decltype(q))(bb + (size_t)q); };
+      errw = fix(errw); smp = fix(smp); tickets = fix(tickets); ngiant = fix(ngiant); sstatus = fix(sstatus);
+      keys = fix(keys); temp = fix(temp); cnt = fix(cnt); lofs = fix(lofs); giants = fix(giants);
+      uint32_t* elems = reinterpret_cast<uint32_t*>(eidx);
+      MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
+      MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
+      // element CSR slice: counting-sort transpose when the received pairs have locality (same rule
+      // as the 1-GPU path), else a stable LSD sort on the local node id
+      bool transpose = g_elem_path.load() == 2;
+      if (g_elem_path.load() == 0 && n >= kTransposeMinElems) {
+        MN_CUDA(launch("locality_sample", 0.0, s, [&] { k_pairs_locality<<<64, 256, 0, s>>>(pairs, n, smp); }));
+        MN_CUDA(cudaMemcpyAsync(host + 2, smp, 16, cudaMemcpyDeviceToHost, s));
+        MN_CUDA(cudaStreamSynchronize(s));
+        transpose = host[3] > 0 && (double)host[2] < kTransposeMaxGroupRatio * (double)host[3];
+      }
+      if (transpose) {
+        if (nloc > 0) {
+          MN_CUDA(launch("elem_count", 8.0 * n, s, [&] { k_pairs_count<<<stream_grid(n), 256, 0, s>>>(pairs, n, lo, cnt); }));
+          MN_CUDA(launch("scan_counts", 12.0 * nloc, s, [&] {
+            k_scan_i32<kThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kThreads, 0, s>>>(
+                cnt, nloc, eoff, sstatus, tickets + 2, 1);
+          }));
+          MN_CUDA(launch("elem_scatter", 16.0 * n, s, [&] {
+            k_pairs_scatter<<<stream_grid(n), 256, 0, s>>>(pairs, n, lo, eoff, lofs, eidx);
+          }));
+          MN_CUDA(launch("elem_segsort", 8.0 * n + 8.0 * (nloc + 1), s, [&] {
+            k_elem_segsort<<<(unsigned)tiles_of(nloc, kSegThreads), kSegThreads, 0, s>>>(eoff, nloc, eidx, giants,
+                                                                                      ngiant, errw);
+          }));
+          const int scap = 48 * 1024;
+          cudaFuncSetAttribute(k_segsort_giant, cudaFuncAttributeMaxDynamicSharedMemorySize, scap * 4);
+          MN_CUDA(launch("segsort_giant", 0.0, s, [&] {
+            k_segsort_giant<<<148, 1024, scap * 4, s>>>(eoff, eidx, giants, ngiant, scap, errw);
+          }));
+          // reset the buffers the node pass reuses (counts, cursors, giant queue)
+          MN_CUDA(cudaMemsetAsync(cnt, 0, (size_t)(nloc + 1) * 4, s));
+          MN_CUDA(cudaMemsetAsync(lofs, 0, (size_t)(nloc + 1) * 4, s));
+          MN_CUDA(cudaMemsetAsync(ngiant, 0, 4, s));
+        } else {
+          MN_CUDA(cudaMemsetAsync(eoff, 0, 8, s));
+        }
+      } else {
+        MN_CUDA(launch("local_keys", 16.0 * n, s, [&] {
+          k_local_keys<<<stream_grid(n), 256, 0, s>>>(pairs, n, lo, keys, elems);
+        }));
+        st = lsd_sort<uint32_t, true>(keys, elems, n, bl, mem);
+        if (st != MN_OK) goto done;
+        MN_CUDA(launch("elem_offsets", 4.0 * n + 8.0 * (nloc + 1), s, [&] {
+          k_elem_offsets<false><<<stream_grid(n / 4 + 1), 256, 0, s>>>(keys, n, nloc, eoff, nullptr);
+        }));
+      }
+      if (nloc > 0) {
+        const bool aligned = ((uintptr_t)shard & 15) == 0 && ((uintptr_t)rrows & 15) == 0;
+        const RowSrc rs{shard, shard_base, shard_m, relems, rrows, nr};
+        const unsigned ng = (unsigned)tiles_of(nloc, kNodeThreads);
+        MN_CUDA(launch("node_gather", 8.0 * (nloc + 1) + 4.0 * n + 4.0 * K * n, s, [&] {
+          if (aligned)
+            k_node_gather_t<T, true, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, nloc, temp, cnt, lofs,
+                                                                       giants, ngiant, errw, lo);
+          else
+            k_node_gather_t<T, false, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, nloc, temp, cnt, lofs,
+                                                                        giants, ngiant, errw, lo);
+        }));
+        const int cap = 48 * 1024;
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(k_node_giant<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
+          cudaFuncSetAttribute(k_node_giant<T, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
+          attr = true;
+        }
+        MN_CUDA(launch("node_giant", 0.0, s, [&] {
+          if (aligned)
+            k_node_giant<T, true, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant,
+                                                                  cap, errw, lo);
+          else
+            k_node_giant<T, false, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant,
+                                                                   cap, errw, lo);
+        }));
+        MN_CUDA(launch("scan_counts", 12.0 * nloc, s, [&] {   // epoch 2: the element scan may have used 1
+          k_scan_i32<kThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kThreads, 0, s>>>(
+              cnt, nloc, noff, sstatus, tickets + 1, 2);
+        }));
+      } else {
+        MN_CUDA(cudaMemsetAsync(noff, 0, 8, s));
+      }
+      MN_CUDA(cudaMemcpyAsync(host + 1, noff + nloc, 8, cudaMemcpyDeviceToHost, s));
+      MN_CUDA(cudaStreamSynchronize(s));
+      const int64_t U = (int64_t)host[1];
+      if (U) {
+        node_slice->indices = (int32_t*)mem.get((size_t)U * 4);
+        if (!node_slice->indices) { st = MN_ERR_OOM; goto done; }
+        MN_CUDA(launch("node_compact", 8.0 * U + 24.0 * nloc, s, [&] {
+          k_node_compact<<<(unsigned)tiles_of(nloc, kNodeThreads), kNodeThreads, 0, s>>>(
+              eoff, C, temp, lofs, noff, nloc, node_slice->indices);
+        }));
+      }
+      node_slice->nnz = U;
+    }
+  }
+  node_slice->num_nodes = nloc;
+  node_slice->offsets = noff;
+  node_slice->owner = mem.a;
+  elem_slice->num_nodes = nloc;
+  elem_slice->nnz = n;
+  elem_slice->offsets = eoff;
+  elem_slice->indices = eidx;
+  elem_slice->owner = mem.a;
+  mem.put(ws);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return MN_ERR_CUDA;
+  return MN_OK;
+done:
+  cudaStreamSynchronize(s);
+  mem.put(ws);
+  mem.put(noff);
+  mem.put(eoff);
+  mem.put(eidx);
+  if (node_slice->indices) mem.put(node_slice->indices);
+  std::memset(node_slice, 0, sizeof(*node_slice));
+  std::memset(elem_slice, 0, sizeof(*elem_slice));
   return st;
 }
 
@@ -1188,18 +1382,25 @@ mn_status mn_exclusive_scan_i32(const int32_t* d_counts, int64_t n, int64_t* d_o
 }
 
 mn_status mn_dist_bucket(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t base, int64_t N, int world,
-                         uint64_t* d_node_keys, uint64_t* d_elem_pairs, int64_t* h_nc, int64_t* h_ec,
-                         const mn_allocator* a, mn_stream stream, mn_error_detail* err) {
+                         int self_rank, uint64_t* d_pairs, int64_t* h_counts, int32_t** d_row_elems,
+                         int32_t** d_rows, int64_t* h_row_counts, const mn_allocator* a, mn_stream stream,
+                         mn_error_detail* err) {
   if (err) { err->elem = -1; err->pos = -1; }
   mn_status st = check_args(t, d_conn, M, N);
   if (st != MN_OK) return st;
-  if (world < 1 || world > 512 || !h_nc || !h_ec || base < 0 || (M > 0 && (!d_node_keys || !d_elem_pairs)))
+  if (world < 1 || world > 512 || self_rank < 0 || self_rank >= world || !h_counts || !h_row_counts ||
+      !d_row_elems || !d_rows || base < 0 || (M > 0 && !d_pairs))
     return MN_ERR_INVALID_ARG;
   if (base + M > INT32_MAX) return MN_ERR_CAPACITY;
+  *d_row_elems = nullptr;
+  *d_rows = nullptr;
   Mem mem(a, (cudaStream_t)stream);
-#define MN_DB(TT)                                                                                        \
-  return world <= 256 ? dist_bucket_impl<TT, 256>(d_conn, M, base, N, world, d_node_keys, d_elem_pairs, h_nc, h_ec, mem, err) \
-                      : dist_bucket_impl<TT, 512>(d_conn, M, base, N, world, d_node_keys, d_elem_pairs, h_nc, h_ec, mem, err)
+#define MN_DB(TT)                                                                                      \
+  return world <= 256                                                                                  \
+             ? dist_bucket_impl<TT, 256>(d_conn, M, base, N, world, self_rank, d_pairs, h_counts,    \
+                                         d_row_elems, d_rows, h_row_counts, mem, err)                \
+             : dist_bucket_impl<TT, 512>(d_conn, M, base, N, world, self_rank, d_pairs, h_counts,    \
+                                         d_row_elems, d_rows, h_row_counts, mem, err)
   switch (t) {
     case MN_TRI3: MN_DB(MN_TRI3);
     case MN_QUAD4: MN_DB(MN_QUAD4);
@@ -1209,77 +1410,25 @@ mn_status mn_dist_bucket(mn_elem_type t, const int32_t* d_conn, int64_t M, int64
 #undef MN_DB
 }
 
-mn_status mn_dist_finish(const uint64_t* d_node_keys, int64_t nn, const uint64_t* d_elem_pairs, int64_t ne,
-                         int64_t N, int64_t lo, int64_t hi, const mn_allocator* a, mn_stream stream,
-                         mn_csr* node_slice, mn_csr* elem_slice) {
-  if (nn < 0 || ne < 0 || N < 0 || N > INT32_MAX || lo < 0 || hi < lo || hi > N || !node_slice || !elem_slice ||
-      (nn > 0 && !d_node_keys) || (ne > 0 && !d_elem_pairs))
+mn_status mn_dist_finish(mn_elem_type t, const uint64_t* d_pairs, int64_t n, const int32_t* d_row_elems,
+                         const int32_t* d_rows, int64_t n_rows, const int32_t* d_conn_shard, int64_t shard_elems,
+                         int64_t global_elem_base, int64_t N, int64_t lo, int64_t hi, const mn_allocator* a,
+                         mn_stream stream, mn_csr* node_slice, mn_csr* elem_slice) {
+  if (t < 0 || t > 3 || n < 0 || n_rows < 0 || shard_elems < 0 || N < 0 || N > INT32_MAX || lo < 0 || hi < lo ||
+      hi > N || !node_slice || !elem_slice || (n > 0 && !d_pairs) || (n_rows > 0 && (!d_row_elems || !d_rows)) ||
+      (shard_elems > 0 && !d_conn_shard) || n > INT32_MAX)
     return MN_ERR_INVALID_ARG;
-  cudaStream_t s = (cudaStream_t)stream;
-  Mem mem(a, s);
-  mn_status st = MN_OK;
-  const int b = node_bits(N);
-  const int64_t nloc = hi - lo;
-  const int bl = node_bits(nloc);
-  std::memset(node_slice, 0, sizeof(*node_slice));
-  std::memset(elem_slice, 0, sizeof(*elem_slice));
-  uint64_t* tmp = nullptr;
-  uint32_t *ek = nullptr, *ev = nullptr;
-  int32_t* idx = nullptr;
-  int64_t* noff = (int64_t*)mem.get((size_t)(nloc + 1) * 8);
-  int64_t* eoff = (int64_t*)mem.get((size_t)(nloc + 1) * 8);
-  int64_t U = 0;
-  if (!noff || !eoff) { st = MN_ERR_OOM; goto fail; }
-  // node slice: rebase, sort on (bl + b) bits, dedupe/offsets against the local node count
-  if (nn > 0) {
-    tmp = (uint64_t*)mem.get((size_t)nn * 8);
-    idx = (int32_t*)mem.get((size_t)nn * 4);
-    if (!tmp || !idx) { st = MN_ERR_OOM; goto fail; }
-    if (launch("rebase_node", 16.0 * nn, s, [&] { k_rebase_node<<<stream_grid(nn), 256, 0, s>>>(d_node_keys, nn, b, lo, tmp); }) != cudaSuccess) { st = MN_ERR_CUDA; goto fail; }
-    st = lsd_sort<uint64_t, false>(tmp, nullptr, nn, bl + b, mem);
-    if (st != MN_OK) goto fail;
+  Mem mem(a, (cudaStream_t)stream);
+#define MN_DF(TT)                                                                                          \
+  return dist_finish_impl<TT>(d_pairs, n, d_row_elems, d_rows, n_rows, d_conn_shard, global_elem_base,   \
+                              shard_elems, N, lo, hi, mem, node_slice, elem_slice)
+  switch (t) {
+    case MN_TRI3: MN_DF(MN_TRI3);
+    case MN_QUAD4: MN_DF(MN_QUAD4);
+    case MN_TET4: MN_DF(MN_TET4);
+    default: MN_DF(MN_HEX8);
   }
-  st = unique_csr<uint64_t>(tmp, nn, b, nloc, noff, idx, &U, mem);
-  if (st != MN_OK) goto fail;
-  mem.put(tmp);
-  tmp = nullptr;
-  node_slice->num_nodes = nloc;
-  node_slice->nnz = U;
-  node_slice->offsets = noff;
-  node_slice->owner = mem.a;
-  if (U) {
-    node_slice->indices = (int32_t*)mem.get((size_t)U * 4);
-    if (!node_slice->indices) { st = MN_ERR_OOM; goto fail; }
-    if (cudaMemcpyAsync(node_slice->indices, idx, (size_t)U * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess) { st = MN_ERR_CUDA; goto fail; }
-  }
-  mem.put(idx);
-  idx = nullptr;
-  noff = nullptr;
-  // element slice: split, stable sort on the local node bits, offsets
-  if (ne > 0) {
-    ek = (uint32_t*)mem.get((size_t)ne * 4);
-    ev = (uint32_t*)mem.get((size_t)ne * 4);
-    if (!ek || !ev) { st = MN_ERR_OOM; goto fail; }
-    if (launch("split_elem", 16.0 * ne, s, [&] { k_split_elem<<<stream_grid(ne), 256, 0, s>>>(d_elem_pairs, ne, lo, ek, ev); }) != cudaSuccess) { st = MN_ERR_CUDA; goto fail; }
-    st = lsd_sort<uint32_t, true>(ek, ev, ne, bl, mem);
-    if (st != MN_OK) goto fail;
-  }
-  if (mn_elem_offsets(ek, ne, nloc, eoff, stream) != MN_OK) { st = MN_ERR_CUDA; goto fail; }
-  mem.put(ek);
-  elem_slice->num_nodes = nloc;
-  elem_slice->nnz = ne;
-  elem_slice->offsets = eoff;
-  elem_slice->indices = (int32_t*)ev;
-  elem_slice->owner = mem.a;
-  if (cudaStreamSynchronize(s) != cudaSuccess) { mn_csr_release(node_slice, stream); mn_csr_release(elem_slice, stream); return MN_ERR_CUDA; }
-  return MN_OK;
-fail:
-  cudaStreamSynchronize(s);
-  mem.put(tmp); mem.put(idx); mem.put(ek); mem.put(ev); mem.put(noff); mem.put(eoff);
-  if (node_slice->indices) mem.put(node_slice->indices);
-  std::memset(node_slice, 0, sizeof(*node_slice));
-  std::memset(elem_slice, 0, sizeof(*elem_slice));
-  return st;
+#undef MN_DF
 }
 
 int64_t mn_launch_count(void) { return g_launches.load(); }

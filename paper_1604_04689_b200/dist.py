@@ -3,16 +3,20 @@
 Each rank holds a contiguous element shard (global element base given).  Nodes are owned in
 contiguous ranges [r*ceil(N/G), (r+1)*ceil(N/G)).  Per call:
 
-  1. mn_dist_bucket   (CUDA)  validate the shard, create the node pairs and the (node, element)
-                              pairs and stably bucket both by owner rank — one onesweep pass each,
-                              the pair creation fused in (no emitted-pair round trip);
-  2. count exchange           all_to_all of the G x 2 pair counts (NCCL over NVLink);
-  3. payload exchange         all_to_all(v) of node keys and element pairs, received in source-rank
-                              order, so element ids stay ascending per node (stable by rank);
-  4. mn_dist_finish   (CUDA)  rebase onto the owned range, sort, dedupe, offsets -> CSR slices.
+  1. mn_dist_bucket   (CUDA)  validate the shard, create its (node, element) incidences and
+                              stably bucket them by owner rank (one onesweep pass, pairs created
+                              from conn); one row per (remote destination, element) goes along;
+  2. count exchange           all_to_all of the G (incidence, row) counts (NCCL over NVLink);
+  3. payload exchange         all_to_all(v) of the pairs, the remote element ids and their rows,
+                              received in source-rank order, so element ids stay ascending;
+  4. mn_dist_finish   (CUDA)  element CSR slice by a stable sort on the local node id; node CSR
+                              slice by the same per-node expansion + dedupe as the 1-GPU path, rows
+                              read from the own shard (local elements) or the received table.
 
-The result on rank r is the CSR of nodes [lo_r, hi_r) with local offsets; concatenating the
-slices in rank order (offsets shifted by the preceding ranks' nnz, returned as ``base``) is
+Only incidences travel (8 bytes each, plus 4(k+1) bytes per remote element row), never the 2E node
+pairs per element; with a spatially coherent numbering almost everything stays on its rank.
+The result on rank r is the CSR of nodes [lo_r, hi_r) with local offsets; concatenating the slices
+in rank order (offsets shifted by the preceding ranks' nnz, returned as ``*_base``) is
 bit-identical to the single-GPU CSR.
 
 ``ops`` is the per-rank compute: the CUDA library by default.  The exchange logic is independent
@@ -35,7 +39,7 @@ class DistResult:
     elem: tuple
     node_base: int       # global offset of this slice in the single-GPU node CSR
     elem_base: int
-    sent_pairs: int      # pairs this rank sent to other ranks (exchange volume)
+    sent_pairs: int      # incidences this rank sent to other ranks (exchange volume)
 
 
 def owner_range(num_nodes: int, world: int, rank: int):
@@ -49,14 +53,14 @@ class CudaOps:
     """The product compute: libmeshnbr's two dist entry points."""
 
     @staticmethod
-    def bucket(conn_shard, etype, elem_base, num_nodes, world):
+    def bucket(conn_shard, etype, elem_base, num_nodes, world, rank):
         from . import dist_bucket
-        return dist_bucket(conn_shard, etype, elem_base, num_nodes, world)
+        return dist_bucket(conn_shard, etype, elem_base, num_nodes, world, rank)
 
     @staticmethod
-    def finish(node_keys, elem_pairs, num_nodes, lo, hi):
+    def finish(etype, pairs, row_elems, rows, conn_shard, elem_base, num_nodes, lo, hi):
         from . import dist_finish
-        return dist_finish(node_keys, elem_pairs, num_nodes, lo, hi)
+        return dist_finish(etype, pairs, row_elems, rows, conn_shard, elem_base, num_nodes, lo, hi)
 
 
 def _a2a(out, inp, out_splits, in_splits, group):
@@ -86,22 +90,26 @@ def find_neighbors_dist(conn_shard: torch.Tensor, etype, global_elem_base: int, 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = conn_shard.device
-    nk, ncount, ep, ecount = ops.bucket(conn_shard, etype, int(global_elem_base), int(num_nodes), world)
+    pairs, count, relems, rows, rcount = ops.bucket(conn_shard, etype, int(global_elem_base), int(num_nodes),
+                                                   world, rank)
+    k = rows.shape[1] if rows.dim() == 2 else 1
     # ---- count exchange: row g of `send` goes to rank g ----
-    send = torch.tensor([[ncount[g], ecount[g]] for g in range(world)], dtype=torch.int64, device=dev)
+    send = torch.tensor([[count[g], rcount[g]] for g in range(world)], dtype=torch.int64, device=dev)
     recv = torch.empty_like(send)
     _a2a(recv.view(-1), send.reshape(-1), None, None, group)
     recv = recv.reshape(world, 2).cpu()
-    rn = recv[:, 0].tolist()
-    re_ = recv[:, 1].tolist()
+    rc, rr = recv[:, 0].tolist(), recv[:, 1].tolist()
     # ---- payload exchange, received in source-rank order ----
-    node_in = torch.empty(sum(rn), dtype=torch.int64, device=dev)
-    elem_in = torch.empty(sum(re_), dtype=torch.int64, device=dev)
-    _a2a(node_in, nk, rn, list(ncount), group)
-    _a2a(elem_in, ep, re_, list(ecount), group)
-    del nk, ep
+    pairs_in = torch.empty(sum(rc), dtype=torch.int64, device=dev)
+    relems_in = torch.empty(sum(rr), dtype=torch.int32, device=dev)
+    rows_in = torch.empty((sum(rr), k), dtype=torch.int32, device=dev)
+    _a2a(pairs_in, pairs, rc, list(count), group)
+    _a2a(relems_in, relems, rr, list(rcount), group)
+    _a2a(rows_in, rows, rr, list(rcount), group)
+    del pairs, relems, rows
     lo, hi = owner_range(num_nodes, world, rank)
-    node, elem = ops.finish(node_in, elem_in, num_nodes, lo, hi)
+    node, elem = ops.finish(etype, pairs_in, relems_in, rows_in, conn_shard, int(global_elem_base),
+                            num_nodes, lo, hi)
     # ---- global bases of the slices (exclusive scan of the per-rank nnz) ----
     mine = torch.tensor([node[1].numel(), elem[1].numel()], dtype=torch.int64, device=dev)
     allv = [torch.empty_like(mine) for _ in range(world)]
@@ -109,7 +117,7 @@ def find_neighbors_dist(conn_shard: torch.Tensor, etype, global_elem_base: int, 
     allv = torch.stack(allv).cpu()
     node_base = int(allv[:rank, 0].sum())
     elem_base = int(allv[:rank, 1].sum())
-    sent = sum(int(ncount[g]) + int(ecount[g]) for g in range(world) if g != rank)
+    sent = sum(int(count[g]) for g in range(world) if g != rank)   # remote incidences
     return DistResult(lo, hi, node, elem, node_base, elem_base, sent)
 
 

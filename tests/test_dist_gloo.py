@@ -30,37 +30,49 @@ class NumpyOps:
     """CPU stand-in with the C ABI's contract (include/meshnbr.h mn_dist_bucket / _finish)."""
 
     @staticmethod
-    def bucket(conn_shard, etype, elem_base, N, world):
+    def bucket(conn_shard, etype, elem_base, N, world, rank):
         conn = conn_shard.numpy()
-        b = _bits(N)
+        k = stages.ARITY[etype]
         chunk = max(1, -(-N // world))
-        a, v = stages.expand_node_pairs(etype, conn)
-        keys = (a.astype(np.int64) << b) | v.astype(np.int64)
-        own = np.minimum(a.astype(np.int64) // chunk, world - 1)
+        en, ee = stages.expand_elem_pairs(etype, conn)          # element-major incidences
+        own = np.minimum(en.astype(np.int64) // chunk, world - 1)
         order = np.argsort(own, kind="stable")
-        nk, ncount = keys[order], np.bincount(own, minlength=world)
-        en, ee = stages.expand_elem_pairs(etype, conn)
-        ep = (en.astype(np.int64) << 32) | (ee.astype(np.int64) + elem_base)
-        eown = np.minimum(en.astype(np.int64) // chunk, world - 1)
-        order = np.argsort(eown, kind="stable")
-        return (torch.from_numpy(nk.copy()), ncount.tolist(),
-                torch.from_numpy(ep[order].copy()), np.bincount(eown, minlength=world).tolist())
+        pairs = ((en.astype(np.int64) << 32) | (ee.astype(np.int64) + elem_base))[order]
+        owns, elems = own[order], ee[order]
+        relems, rows, rcount = [], [], []
+        for g in range(world):
+            sel = np.unique(elems[owns == g]) if g != rank else np.zeros(0, dtype=np.int64)
+            relems.append(sel + elem_base)
+            rows.append(conn.reshape(-1, k)[sel])
+            rcount.append(len(sel))
+        return (torch.from_numpy(pairs.copy()), np.bincount(own, minlength=world).tolist(),
+                torch.from_numpy(np.concatenate(relems).astype(np.int32)),
+                torch.from_numpy(np.concatenate(rows).astype(np.int32).reshape(-1, k)), rcount)
 
     @staticmethod
-    def finish(node_keys, elem_pairs, N, lo, hi):
-        b = _bits(N)
-        k = node_keys.numpy()
-        a, v = (k >> b) - lo, k & ((1 << b) - 1)
-        a, v = stages.unique_pairs(*stages.sort_pairs(a, v))
-        uk, cnt = stages.reduce_by_key_ones(a)
-        noff = stages.exclusive_scan(stages.dense_counts(uk, cnt, hi - lo))
-        p = elem_pairs.numpy()
-        en, ee = (p >> 32) - lo, p & 0xFFFFFFFF
-        en, ee = stages.stable_sort_by_key(en, ee)
-        uk, cnt = stages.reduce_by_key_ones(en)
-        eoff = stages.exclusive_scan(stages.dense_counts(uk, cnt, hi - lo))
-        return ((torch.from_numpy(noff), torch.from_numpy(v.astype(np.int32))),
-                (torch.from_numpy(eoff), torch.from_numpy(ee.astype(np.int32))))
+    def finish(etype, pairs, relems, rows, conn_shard, elem_base, N, lo, hi):
+        p = pairs.numpy()
+        shard = conn_shard.numpy()
+        table = {int(e): r for e, r in zip(relems.numpy().tolist(), rows.numpy().tolist())}
+        nodes, elems = (p >> 32), (p & 0xFFFFFFFF)
+        order = np.argsort(nodes - lo, kind="stable")
+        nloc = hi - lo
+        uk, cnt = stages.reduce_by_key_ones((nodes - lo)[order])
+        eoff = stages.exclusive_scan(stages.dense_counts(uk, cnt, nloc))
+        eidx = elems[order].astype(np.int32)
+        adj = [set() for _ in range(nloc)]
+        for a, e in zip(nodes.tolist(), elems.tolist()):
+            row = shard[e - elem_base].tolist() if 0 <= e - elem_base < len(shard) else table[e]
+            pa = row.index(a)
+            for i, j in stages.EDGES[etype]:
+                if i == pa:
+                    adj[a - lo].add(row[j])
+                if j == pa:
+                    adj[a - lo].add(row[i])
+        noff = stages.exclusive_scan([len(x) for x in adj])
+        nidx = np.array([v for x in adj for v in sorted(x)], dtype=np.int32)
+        return ((torch.from_numpy(noff), torch.from_numpy(nidx)),
+                (torch.from_numpy(eoff), torch.from_numpy(eidx)))
 
 
 MESHES = {

@@ -27,25 +27,27 @@ def _virtual_ranks(conn, et, N, G):
     import paper_1604_04689_b200 as mn
     from paper_1604_04689_b200.dist import owner_range
     M = conn.shape[0]
-    sent = []
+    sent, shards = [], []
     for r in range(G):
         s0, s1 = r * M // G, (r + 1) * M // G
-        nk, nc, ep, ec = mn.dist_bucket(conn[s0:s1].contiguous(), et, s0, N, G)
-        # bucket g must hold exactly the pairs owned by rank g
-        nsplit = list(torch.split(nk, nc))
-        esplit = list(torch.split(ep, ec))
-        sent.append((nsplit, esplit))
-    b = mn.node_key_bits(N)
+        shard = conn[s0:s1].contiguous()
+        pairs, cnt, relems, rows, rcnt = mn.dist_bucket(shard, et, s0, N, G, r)
+        assert rcnt[r] == 0
+        sent.append((list(torch.split(pairs, cnt)), list(torch.split(relems, rcnt)), list(torch.split(rows, rcnt))))
+        shards.append((shard, s0))
     node_parts, elem_parts = [], []
     node_base = elem_base = 0
     for g in range(G):
         lo, hi = owner_range(N, G, g)
-        nin = torch.cat([sent[r][0][g] for r in range(G)])
+        pin = torch.cat([sent[r][0][g] for r in range(G)])
         ein = torch.cat([sent[r][1][g] for r in range(G)])
-        if nin.numel():
-            own = (nin >> b)
+        rin = torch.cat([sent[r][2][g] for r in range(G)])
+        if pin.numel():
+            own = pin >> 32        # bucket g must hold exactly the incidences owned by rank g
             assert bool(((own >= lo) & (own < hi)).all())
-        (no, ni), (eo, ei) = mn.dist_finish(nin, ein, N, lo, hi)
+        if ein.numel() > 1:
+            assert bool((ein[1:] > ein[:-1]).all())   # remote rows: element ids ascending
+        (no, ni), (eo, ei) = mn.dist_finish(et, pin, ein, rin, shards[g][0], shards[g][1], N, lo, hi)
         node_parts.append((no[:-1] + node_base, ni))
         elem_parts.append((eo[:-1] + elem_base, ei))
         node_base += ni.numel()
@@ -57,6 +59,14 @@ def _virtual_ranks(conn, et, N, G):
     return (no, ni), (eo, ei)
 
 
+@pytest.fixture(params=["radix", "transpose"])
+def elem_path(request):
+    import paper_1604_04689_b200 as mn
+    mn.set_elem_path(request.param)
+    yield request.param
+    mn.set_elem_path("auto")
+
+
 @pytest.mark.parametrize("G", [1, 2, 3, 8])
 @pytest.mark.parametrize("name,et,make", [
     ("kuhn_9", meshgen.TET4, lambda: meshgen.kuhn_tets(9)),
@@ -64,7 +74,7 @@ def _virtual_ranks(conn, et, N, G):
     ("sphere", meshgen.TRI3, lambda: meshgen.uv_sphere(64, 33)),
     ("quad", meshgen.QUAD4, lambda: meshgen.quad_grid(40, 50)),
 ])
-def test_virtual_ranks_match_oracle(G, name, et, make):
+def test_virtual_ranks_match_oracle(G, name, et, make, elem_path):
     conn, N = make()
     (no, ni), (eo, ei) = _virtual_ranks(conn.cuda(), et, N, G)
     ro, ri = oracle.node_csr(et, conn, N)
@@ -73,7 +83,7 @@ def test_virtual_ranks_match_oracle(G, name, et, make):
     assert np.array_equal(eo.cpu().numpy(), so) and np.array_equal(ei.cpu().numpy(), si)
 
 
-def test_virtual_ranks_config5_shape_small():
+def test_virtual_ranks_config5_shape_small(elem_path):
     """Config 5's recipe (Kuhn, natural order) at 40^3, 8 ranks: equals the 1-GPU CSR."""
     import paper_1604_04689_b200 as mn
     conn, N = meshgen.kuhn_tets(40, device="cuda")
@@ -87,7 +97,7 @@ def test_bucket_reports_invalid_with_global_ids():
     import paper_1604_04689_b200 as mn
     conn = torch.tensor([[0, 1, 2], [1, 2, 9]], dtype=torch.int32).cuda()
     with pytest.raises(mn.MeshError) as ei:
-        mn.dist_bucket(conn, "tri3", 1000, 5, 2)
+        mn.dist_bucket(conn, "tri3", 1000, 5, 2, 0)
     assert (ei.value.code, ei.value.elem, ei.value.pos) == (2, 1001, 2)
 
 
