@@ -112,6 +112,17 @@ mn_status mn_find_neighbors_both(mn_elem_type type, const int32_t* d_conn, int64
                                  int64_t num_nodes, const mn_allocator* alloc, mn_stream stream,
                                  mn_csr* node_out, mn_csr* elem_out, mn_error_detail* err);
 
+/* Memory-bounded form of mn_find_neighbors_both (the device-memory cost the
+ * paper names as its shortcoming, §3.2.2): the nodes are processed in K
+ * contiguous ranges, K the smallest power of two whose per-range workspace estimate fits in
+ * max_workspace_bytes (outputs not included), each range by the counting-sort transpose +
+ * per-node expansion restricted to its nodes.  Same outputs as mn_find_neighbors_both; blocks
+ * twice per range.  *chunks_used (nullable) receives K. */
+mn_status mn_find_neighbors_both_chunked(mn_elem_type type, const int32_t* d_conn, int64_t num_elems,
+                                         int64_t num_nodes, size_t max_workspace_bytes,
+                                         const mn_allocator* alloc, mn_stream stream, mn_csr* node_out,
+                                         mn_csr* elem_out, int64_t* chunks_used, mn_error_detail* err);
+
 /* Same as mn_find_neighbors_both with HOST buffers: h_conn is host memory (pinned for full PCIe
  * speed); the connectivity is copied to the device, both CSRs are computed and copied back into
  * host memory obtained from `host_alloc` (its alloc receives the byte count; stream unused).
@@ -132,6 +143,9 @@ int mn_abi_version(void);
  * modes: 1 = nodes, 2 = elements, 3 = both. */
 mn_status mn_workspace_bytes(mn_elem_type type, int64_t num_elems, int64_t num_nodes, int modes,
                              size_t* bytes);
+
+/* Estimated per-range workspace of mn_find_neighbors_both_chunked with `chunks` node ranges. */
+size_t mn_chunk_workspace_bytes(mn_elem_type type, int64_t num_elems, int64_t num_nodes, int64_t chunks);
 
 /* ---------------------------------------------------------------------------------------------
  * Stage primitives (one per §8(a) row; the tests check each against oracle/stages.py)

@@ -18,7 +18,7 @@ import torch
 __all__ = [
     "TRI3", "QUAD4", "TET4", "HEX8", "MeshError", "lib_path", "load",
     "find_node_neighbors", "find_node_neighbors_sortpairs", "find_elem_neighbors", "find_neighbors", "find_neighbors_host",
-    "workspace_bytes", "node_key_bits", "node_key_bytes",
+    "workspace_bytes", "node_key_bits", "node_key_bytes", "find_neighbors_chunked", "chunk_workspace_bytes",
     "emit_node_pairs", "emit_elem_pairs", "radix_sort_keys", "radix_sort_pairs_u32",
     "unique_node_csr", "elem_offsets", "exclusive_scan",
     "dist_bucket", "dist_finish",
@@ -84,6 +84,9 @@ def _declare(lib):
                                        _P(_ErrDetail)]),
         "mn_find_neighbors_both_host": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _P(_Allocator), _VP,
                                             _P(_Csr), _P(_Csr), _P(_ErrDetail)]),
+        "mn_find_neighbors_both_chunked": (S, [_INT, _VP, _I64, _I64, ctypes.c_size_t, _P(_Allocator), _VP,
+                                               _P(_Csr), _P(_Csr), _P(_I64), _P(_ErrDetail)]),
+        "mn_chunk_workspace_bytes": (ctypes.c_size_t, [_INT, _I64, _I64, _I64]),
         "mn_csr_release": (None, [_P(_Csr), _VP]),
         "mn_status_string": (ctypes.c_char_p, [_INT]),
         "mn_abi_version": (_INT, []),
@@ -286,6 +289,27 @@ def find_neighbors(conn: torch.Tensor, etype, num_nodes: int, stream=None):
                                         ctypes.byref(err))
     _check(rc, err)
     return _take(al, no), _take(al, eo)
+
+
+def find_neighbors_chunked(conn: torch.Tensor, etype, num_nodes: int, max_workspace_bytes: int, stream=None):
+    """Memory-bounded form of find_neighbors: nodes processed in K ranges whose workspace fits in
+    max_workspace_bytes.  Returns ((node_offsets, node_indices), (elem_offsets, elem_indices), K)."""
+    et = _etype(etype)
+    c, M = _conn_arg(conn, et)
+    lib = load()
+    al = _TorchAllocator(c.device)
+    no, eo, err = _Csr(), _Csr(), _ErrDetail()
+    k = ctypes.c_int64(0)
+    with torch.cuda.device(c.device):
+        rc = lib.mn_find_neighbors_both_chunked(et, c.data_ptr(), M, int(num_nodes), int(max_workspace_bytes),
+                                                ctypes.byref(al.struct), _stream_ptr(stream), ctypes.byref(no),
+                                                ctypes.byref(eo), ctypes.byref(k), ctypes.byref(err))
+    _check(rc, err)
+    return _take(al, no), _take(al, eo), int(k.value)
+
+
+def chunk_workspace_bytes(etype, num_elems: int, num_nodes: int, chunks: int) -> int:
+    return int(load().mn_chunk_workspace_bytes(_etype(etype), int(num_elems), int(num_nodes), int(chunks)))
 
 
 def find_neighbors_host(conn_host: torch.Tensor, etype, num_nodes: int, device=None, stream=None):

@@ -962,7 +962,7 @@ k_locality_sample(const int32_t* __restrict__ conn, int64_t M, unsigned long lon
 template <int T, bool ALIGNED>
 __global__ void __launch_bounds__(256)
 k_elem_count(const int32_t* __restrict__ conn, int64_t M, int64_t N, int32_t* __restrict__ cnt,
-             unsigned long long* __restrict__ err) {
+             unsigned long long* __restrict__ err, int64_t lo = 0, int64_t hi = INT64_MAX) {
   constexpr int K = Elem<T>::K;
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -990,7 +990,8 @@ k_elem_count(const int32_t* __restrict__ conn, int64_t M, int64_t N, int32_t* __
     const bool ok = in && bad < 0;
     if (ok) {
 #pragma unroll
-      for (int p = 0; p < K; ++p) atomicAdd(cnt + v[p], 1);   // fire-and-forget RED
+      for (int p = 0; p < K; ++p)   // fire-and-forget RED; only nodes of the range [lo, hi)
+        if (v[p] >= lo && v[p] < hi) atomicAdd(cnt + (v[p] - lo), 1);
     }
   }
 }
@@ -998,7 +999,8 @@ k_elem_count(const int32_t* __restrict__ conn, int64_t M, int64_t N, int32_t* __
 template <int T, bool ALIGNED>
 __global__ void __launch_bounds__(256)
 k_elem_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __restrict__ eoff,
-               int32_t* __restrict__ cursor, int32_t* __restrict__ eidx, const unsigned long long* __restrict__ err) {
+               int32_t* __restrict__ cursor, int32_t* __restrict__ eidx, const unsigned long long* __restrict__ err,
+               int64_t lo = 0, int64_t hi = INT64_MAX) {
   constexpr int K = Elem<T>::K;
   if (*err != ERR_NONE) return;
   const int lane = threadIdx.x & 31;
@@ -1010,13 +1012,14 @@ k_elem_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __res
     if (in) load_row<T, ALIGNED>(conn, e, v);
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      const int x = in ? v[p] : -1 - lane;
+      const bool mine = in && v[p] >= lo && v[p] < hi;
+      const int x = mine ? (int)(v[p] - lo) : -1 - lane;
       const unsigned peers = __match_any_sync(FULL, x);
       const int leader = __ffs(peers) - 1;
       int b = 0;
-      if (in && lane == leader) b = atomicAdd(cursor + x, (int)__popc(peers));
+      if (mine && lane == leader) b = atomicAdd(cursor + x, (int)__popc(peers));
       b = __shfl_sync(FULL, b, leader);
-      if (in) eidx[eoff[x] + b + __popc(peers & lanemask_lt())] = (int32_t)e;
+      if (mine) eidx[eoff[x] + b + __popc(peers & lanemask_lt())] = (int32_t)e;
     }
   }
 }
@@ -1281,6 +1284,13 @@ k_emit_remote_rows(const uint64_t* __restrict__ pairs, const int32_t* __restrict
 #pragma unroll
     for (int q = 0; q < K; ++q) rrows[o * K + q] = __ldg(conn + (e - elem_base) * K + q);
   }
+}
+
+// Chunked mode: add a base to a slice of offsets (local slice offsets -> global CSR offsets).
+__global__ void __launch_bounds__(256)
+k_shift_offsets(const int64_t* __restrict__ in, int64_t n, int64_t base, int64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i] + base;
 }
 
 // Multi-GPU finish, transpose form (received pairs are element-major, i.e. as coherent as conn):

@@ -707,6 +707,187 @@ done:
   return st;
 }
 
+// ================================================================================================
+// Memory-bounded mode (the paper's stated shortcoming): the
+// nodes are processed in K contiguous ranges, each range by the transpose + expansion path
+// restricted to its nodes (the multi-GPU partition applied in time).  The workspace per range is
+// ~ (4C + 4) bytes per incidence of the range; element slices land directly in the outputs, node
+// slices are concatenated at the end.
+// ================================================================================================
+static size_t chunk_workspace(const Plan& P, int64_t K) {
+  const double inc = (double)P.Pe / (double)K * 1.25 + 64.0;     // incidences of a range (+ imbalance)
+  const double nodes = (double)P.N / (double)K + 2.0;
+  return (size_t)(4.0 * P.C * inc + 48.0 * nodes + 65536.0);
+}
+
+template <int T>
+static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size_t max_ws, int64_t* chunks,
+                              mn_csr* node_out, mn_csr* elem_out, mn_error_detail* err) {
+  cudaStream_t s = mem.s;
+  mn_status st = MN_OK;
+  constexpr int C = Elem<T>::C;
+  const bool aligned = ((uintptr_t)conn & 15) == 0;
+  uint64_t* host = pinned_pair();
+  if (!host) return MN_ERR_CUDA;
+  int64_t K = 1;
+  while (K < P.N && chunk_workspace(P, K) > max_ws) K *= 2;
+  if (chunks) *chunks = K;
+  int64_t* node_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
+  int64_t* elem_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
+  int32_t* elem_idx = P.Pe ? (int32_t*)mem.get((size_t)P.Pe * 4) : nullptr;
+  int32_t* node_idx = nullptr;
+  std::vector<std::pair<int32_t*, int64_t>> parts;
+  void* ws = nullptr;
+  uint32_t* temp = nullptr;
+  int64_t ebase = 0, nbase = 0;
+  if (!node_off || !elem_off || (P.Pe && !elem_idx)) { st = MN_ERR_OOM; goto done; }
+  MN_CUDA(cudaMemsetAsync(node_off, 0, (size_t)(P.N + 1) * 8, s));
+  MN_CUDA(cudaMemsetAsync(elem_off, 0, (size_t)(P.N + 1) * 8, s));
+  for (int64_t k = 0; k < K && P.M > 0; ++k) {
+    const int64_t lo = P.N * k / K, hi = P.N * (k + 1) / K, nloc = hi - lo;
+    if (nloc == 0) continue;
+    Arena ar;
+    unsigned long long* errw = ar.take<unsigned long long>(2);
+    uint32_t* tickets = ar.take<uint32_t>(8);
+    unsigned int* ngiant = ar.take<unsigned int>(1);
+    unsigned int* nsgiant = ar.take<unsigned int>(1);
+    uint64_t* sstatus = ar.take<uint64_t>((size_t)tiles_of(nloc, kScanTile) + 1);
+    int32_t* ecnt = ar.take<int32_t>((size_t)nloc + 1);
+    int32_t* cursor = ar.take<int32_t>((size_t)nloc + 1);
+    const size_t head = ar.off;
+    int64_t* eoff = ar.take<int64_t>((size_t)nloc + 1);
+    int64_t* noff = ar.take<int64_t>((size_t)nloc + 1);
+    int32_t* cnt = ar.take<int32_t>((size_t)nloc + 1);
+    int32_t* lofs = ar.take<int32_t>((size_t)nloc + 1);
+    uint32_t* giants = ar.take<uint32_t>((size_t)nloc + 1);
+    uint32_t* sgiants = ar.take<uint32_t>((size_t)nloc + 1);
+    ws = mem.get(ar.off);
+    if (!ws) { st = MN_ERR_OOM; goto done; }
+    {
+      char* bb = (char*)ws;
+      auto fix = [&](auto* q) { return (decltype(q))(bb + (size_t)q); };
+      errw = fix(errw); tickets = fix(tickets); ngiant = fix(ngiant); nsgiant = fix(nsgiant); sstatus = fix(sstatus);
+      ecnt = fix(ecnt); cursor = fix(cursor); eoff = fix(eoff); noff = fix(noff); cnt = fix(cnt); lofs = fix(lofs);
+      giants = fix(giants); sgiants = fix(sgiants);
+      MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
+      MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
+      // (1) validation + incidence counts of the range, offsets
+      MN_CUDA(launch("elem_count", 4.0 * P.K * P.M, s, [&] {
+        if (aligned) k_elem_count<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw, lo, hi);
+        else k_elem_count<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw, lo, hi);
+      }));
+      MN_CUDA(launch("scan_counts", 12.0 * nloc, s, [&] {
+        k_scan_i32<kThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kThreads, 0, s>>>(
+            ecnt, nloc, eoff, sstatus, tickets, 1);
+      }));
+      MN_CUDA(cudaMemcpyAsync(host, errw, 8, cudaMemcpyDeviceToHost, s));
+      MN_CUDA(cudaMemcpyAsync(host + 1, eoff + nloc, 8, cudaMemcpyDeviceToHost, s));
+      MN_CUDA(cudaStreamSynchronize(s));
+      st = decode_err(host[0], err);
+      if (st != MN_OK) goto done;
+      const int64_t Ie = (int64_t)host[1];
+      int32_t* eslice = elem_idx + ebase;
+      // (2) element slice: scatter + per-node sort, straight into the output
+      temp = Ie ? (uint32_t*)mem.get((size_t)C * Ie * 4) : nullptr;
+      if (Ie && !temp) { st = MN_ERR_OOM; goto done; }
+      if (Ie) {
+        MN_CUDA(launch("elem_scatter", 4.0 * P.K * P.M + 12.0 * Ie, s, [&] {
+          if (aligned) k_elem_scatter<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, eoff, cursor, eslice, errw, lo, hi);
+          else k_elem_scatter<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, eoff, cursor, eslice, errw, lo, hi);
+        }));
+        MN_CUDA(launch("elem_segsort", 8.0 * Ie + 8.0 * (nloc + 1), s, [&] {
+          k_elem_segsort<<<(unsigned)tiles_of(nloc, kSegThreads), kSegThreads, 0, s>>>(eoff, nloc, eslice, sgiants,
+                                                                                    nsgiant, errw);
+        }));
+        const int scap = 48 * 1024;
+        cudaFuncSetAttribute(k_segsort_giant, cudaFuncAttributeMaxDynamicSharedMemorySize, scap * 4);
+        MN_CUDA(launch("segsort_giant", 0.0, s, [&] {
+          k_segsort_giant<<<148, 1024, scap * 4, s>>>(eoff, eslice, sgiants, nsgiant, scap, errw);
+        }));
+        // (3) node slice: per-node expansion + dedupe, counts, offsets
+        const RowSrc rs{conn, 0, P.M, nullptr, nullptr, 0};
+        const unsigned ng = (unsigned)tiles_of(nloc, kNodeThreads);
+        MN_CUDA(launch("node_gather", 8.0 * (nloc + 1) + 4.0 * Ie + 4.0 * P.K * Ie, s, [&] {
+          if (aligned)
+            k_node_gather_t<T, true><<<ng, kNodeThreads, 0, s>>>(eoff, eslice, rs, nloc, temp, cnt, lofs, giants,
+                                                                 ngiant, errw, lo);
+          else
+            k_node_gather_t<T, false><<<ng, kNodeThreads, 0, s>>>(eoff, eslice, rs, nloc, temp, cnt, lofs, giants,
+                                                                  ngiant, errw, lo);
+        }));
+        const int cap = 48 * 1024;
+        cudaFuncSetAttribute(k_node_giant<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
+        cudaFuncSetAttribute(k_node_giant<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
+        MN_CUDA(launch("node_giant", 0.0, s, [&] {
+          if (aligned)
+            k_node_giant<T, true><<<148, 1024, cap * 4, s>>>(eoff, eslice, rs, temp, cnt, lofs, giants, ngiant, cap,
+                                                            errw, lo);
+          else
+            k_node_giant<T, false><<<148, 1024, cap * 4, s>>>(eoff, eslice, rs, temp, cnt, lofs, giants, ngiant, cap,
+                                                             errw, lo);
+        }));
+        MN_CUDA(launch("scan_counts", 12.0 * nloc, s, [&] {
+          k_scan_i32<kThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kThreads, 0, s>>>(
+              cnt, nloc, noff, sstatus, tickets + 1, 2);
+        }));
+      } else {
+        MN_CUDA(cudaMemsetAsync(noff, 0, (size_t)(nloc + 1) * 8, s));
+      }
+      MN_CUDA(launch("shift_offsets", 16.0 * (nloc + 1), s, [&] {
+        k_shift_offsets<<<stream_grid(nloc + 1), 256, 0, s>>>(eoff, nloc + 1, ebase, elem_off + lo);
+      }));
+      MN_CUDA(cudaMemcpyAsync(host + 1, noff + nloc, 8, cudaMemcpyDeviceToHost, s));
+      MN_CUDA(cudaStreamSynchronize(s));
+      const int64_t U = (int64_t)host[1];
+      if (U) {
+        int32_t* part = (int32_t*)mem.get((size_t)U * 4);
+        if (!part) { st = MN_ERR_OOM; goto done; }
+        parts.push_back({part, U});
+        MN_CUDA(launch("node_compact", 8.0 * U + 24.0 * nloc, s, [&] {
+          k_node_compact<<<(unsigned)tiles_of(nloc, kNodeThreads), kNodeThreads, 0, s>>>(eoff, C, temp, lofs, noff,
+                                                                                       nloc, part);
+        }));
+      }
+      MN_CUDA(launch("shift_offsets", 16.0 * (nloc + 1), s, [&] {
+        k_shift_offsets<<<stream_grid(nloc + 1), 256, 0, s>>>(noff, nloc + 1, nbase, node_off + lo);
+      }));
+      ebase += Ie;
+      nbase += U;
+    }
+    mem.put(temp);
+    temp = nullptr;
+    mem.put(ws);
+    ws = nullptr;
+  }
+  // concatenate the node slices (peak: slices + output = 2 x node nnz)
+  if (nbase) {
+    node_idx = (int32_t*)mem.get((size_t)nbase * 4);
+    if (!node_idx) { st = MN_ERR_OOM; goto done; }
+    int64_t o = 0;
+    for (auto& pr : parts) {
+      MN_CUDA(cudaMemcpyAsync(node_idx + o, pr.first, (size_t)pr.second * 4, cudaMemcpyDeviceToDevice, s));
+      o += pr.second;
+    }
+  }
+  for (auto& pr : parts) mem.put(pr.first);
+  parts.clear();
+  MN_CUDA(cudaStreamSynchronize(s));
+  node_out->num_nodes = P.N; node_out->nnz = nbase; node_out->offsets = node_off; node_out->indices = node_idx;
+  node_out->owner = mem.a;
+  elem_out->num_nodes = P.N; elem_out->nnz = P.Pe; elem_out->offsets = elem_off; elem_out->indices = elem_idx;
+  elem_out->owner = mem.a;
+  return MN_OK;
+done:
+  cudaStreamSynchronize(s);
+  mem.put(temp);
+  mem.put(ws);
+  for (auto& pr : parts) mem.put(pr.first);
+  mem.put(node_off); mem.put(elem_off); mem.put(elem_idx); mem.put(node_idx);
+  std::memset(node_out, 0, sizeof(*node_out));
+  std::memset(elem_out, 0, sizeof(*elem_out));
+  return st;
+}
+
 template <int T>
 static mn_status dispatch_key(const Plan& P, const int32_t* conn, Mem& mem, bool wn, bool we,
                               mn_csr* no, mn_csr* eo, mn_error_detail* err) {
@@ -1222,6 +1403,23 @@ mn_status mn_find_neighbors_both(mn_elem_type t, const int32_t* d_conn, int64_t 
   return find(t, d_conn, M, N, a, s, true, true, no, eo, err);
 }
 
+mn_status mn_find_neighbors_both_chunked(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N,
+                                         size_t max_workspace_bytes, const mn_allocator* a, mn_stream stream,
+                                         mn_csr* no, mn_csr* eo, int64_t* chunks_used, mn_error_detail* err) {
+  if (err) { err->elem = -1; err->pos = -1; }
+  mn_status st = check_args(t, d_conn, M, N);
+  if (st != MN_OK) return st;
+  if (!no || !eo) return MN_ERR_INVALID_ARG;
+  Mem mem(a, (cudaStream_t)stream);
+  const Plan P = make_plan(t, M, N);
+  switch (t) {
+    case MN_TRI3: return chunked_both<MN_TRI3>(P, d_conn, mem, max_workspace_bytes, chunks_used, no, eo, err);
+    case MN_QUAD4: return chunked_both<MN_QUAD4>(P, d_conn, mem, max_workspace_bytes, chunks_used, no, eo, err);
+    case MN_TET4: return chunked_both<MN_TET4>(P, d_conn, mem, max_workspace_bytes, chunks_used, no, eo, err);
+    default: return chunked_both<MN_HEX8>(P, d_conn, mem, max_workspace_bytes, chunks_used, no, eo, err);
+  }
+}
+
 mn_status mn_find_neighbors_both_host(mn_elem_type t, const int32_t* h_conn, int64_t M, int64_t N,
                                       const mn_allocator* dev_alloc, const mn_allocator* host_alloc,
                                       mn_stream stream, mn_csr* no, mn_csr* eo, mn_error_detail* err) {
@@ -1278,14 +1476,36 @@ mn_status mn_workspace_bytes(mn_elem_type t, int64_t M, int64_t N, int modes, si
   if (st != MN_OK || !bytes || modes < 1 || modes > 3) return MN_ERR_INVALID_ARG;
   const Plan P = make_plan(t, M, N);
   const bool wn = modes & 1, we = modes & 2;
-  const size_t w = P.key64 ? 8 : 4;
-  const int64_t st_tiles = std::max(wn ? tiles_of(P.Pn, kTile) : 0, we ? tiles_of(P.Pe, kTile) : 0);
-  size_t b = 4096 + (size_t)st_tiles * P.bins * 8 + (wn ? (size_t)tiles_of(P.Pn, kUTile) * 8 : 0);
-  if (wn) b += 2 * (size_t)P.Pn * w;
-  const bool alias = wn && we && (size_t)P.Pn * w >= (size_t)16 * P.Pe;
-  if (we && !alias) b += 16 * (size_t)P.Pe;
-  *bytes = b;
+  // mirrors pipeline_inc's arena (both element paths allocate the same pieces)
+  Arena a;
+  a.take<unsigned long long>(2);
+  a.take<uint32_t>(32);
+  a.take<unsigned int>(1);
+  a.take<unsigned long long>((size_t)P.dp.nd * P.bins);
+  a.take<uint64_t>((size_t)P.dp.nd * P.bins);
+  a.take<uint64_t>((size_t)tiles_of(P.Pe, kTile) * P.bins);
+  a.take<uint64_t>((size_t)tiles_of(P.N, kScanTile) + 1);
+  a.take<int32_t>((size_t)P.N + 1);
+  a.take<unsigned int>(1);
+  a.take<int32_t>((size_t)P.N + 1);
+  a.take<uint32_t>((size_t)P.N + 1);
+  for (int i = 0; i < 4; ++i) a.take<uint32_t>((size_t)P.Pe);
+  if (wn) {
+    a.take<int32_t>((size_t)P.N);
+    a.take<int32_t>((size_t)P.N);
+    a.take<uint32_t>((size_t)P.N);
+    if (!we) {
+      a.take<int64_t>((size_t)P.N + 1);
+      a.take<int32_t>((size_t)P.Pe);
+    }
+  }
+  *bytes = a.off;
   return MN_OK;
+}
+
+size_t mn_chunk_workspace_bytes(mn_elem_type t, int64_t M, int64_t N, int64_t chunks) {
+  if (t < 0 || t > 3 || M < 0 || N < 0 || chunks < 1) return 0;
+  return chunk_workspace(make_plan(t, M, N), chunks);
 }
 
 mn_status mn_emit_node_pairs(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N, void* d_keys,

@@ -59,9 +59,13 @@ def test_host_only_entry_points(lib):
         [1, 1, 1, 2, 2, 3, 11, 20, 21]
     assert mn.node_key_bytes(1089) == 4 and mn.node_key_bytes(501002) == 8
     assert mn.node_key_bytes(65536) == 4 and mn.node_key_bytes(65537) == 8
-    # workspace estimate: config 3 both modes, 8-byte keys, double buffered
+    # workspace estimate, config 3 both modes: 4 element-pair buffers of 4 B per incidence at least
+    Pe = 4 * 12582912
     ws = mn.workspace_bytes("tet4", 12582912, 2146689, 3)
-    assert ws >= 2 * 8 * 150994944
+    assert 16 * Pe <= ws < 24 * Pe
+    # chunked mode: the per-range estimate shrinks with the number of ranges
+    w = [mn.chunk_workspace_bytes("tet4", 12582912, 2146689, k) for k in (1, 2, 4, 8)]
+    assert all(a > b for a, b in zip(w, w[1:])) and w[0] < ws
     with pytest.raises(mn.MeshError):
         mn.workspace_bytes("tet4", -1, 10, 3)
 

@@ -371,3 +371,38 @@ def test_full_size_config5_single_gpu():
     assert torch.equal(no[1:] - no[:-1], val) and torch.equal(eo[1:] - eo[:-1], ne)
     del val, ne
     _sampled_check(et, conn.cpu(), N, (no, ni), (eo, ei), nsample=24)
+
+
+# ------------------------------------------------------------------------------------------------
+# memory-bounded (chunked) mode, SURVEY §8(f) row 4
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name,et,make", SMALL)
+@pytest.mark.parametrize("budget", [1 << 16, 1 << 20])
+def test_chunked_matches_oracle(name, et, make, budget):
+    conn, N = make()
+    (no, ni), (eo, ei), K = mn().find_neighbors_chunked(conn.cuda(), et, N, budget)
+    assert K >= 1
+    _assert_csr((no, ni), oracle.node_csr(et, conn, N), f"{name} chunked node K={K}")
+    _assert_csr((eo, ei), oracle.elem_csr(et, conn, N), f"{name} chunked elem K={K}")
+
+
+def test_chunked_full_size_config3_bit_equal():
+    et, conn, N = meshgen.make_config(3, device="cuda")
+    ref = mn().find_neighbors(conn, et, N)
+    budget = mn().chunk_workspace_bytes(et, conn.shape[0], N, 8)
+    got = mn().find_neighbors_chunked(conn, et, N, budget)
+    assert got[2] >= 8
+    for a, b in zip(ref, got[:2]):
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("ntri", [200, 60000])
+def test_chunked_fans_and_errors(ntri):
+    conn, N = meshgen.nonmanifold_fan(ntri)
+    (no, ni), (eo, ei), K = mn().find_neighbors_chunked(conn.cuda(), 0, N, 1 << 18)
+    _assert_csr((no, ni), oracle.node_csr(0, conn, N), "fan chunked")
+    _assert_csr((eo, ei), oracle.elem_csr(0, conn, N), "fan chunked elem")
+    bad = torch.tensor([[0, 1, 2], [1, 2, 9]], dtype=torch.int32).cuda()
+    with pytest.raises(mn().MeshError) as ei_:
+        mn().find_neighbors_chunked(bad, 0, 5, 1 << 12)
+    assert (ei_.value.code, ei_.value.elem, ei_.value.pos) == (2, 1, 2)
