@@ -436,9 +436,19 @@ done:
 // expansion of the element CSR (C edge-neighbours per incidence), sorted and deduplicated per
 // node, counted, scanned, and compacted into an exact-size output after the one host sync.
 // ================================================================================================
+// Host-buffer calls: the element CSR is copied to the host on a side stream as soon as it is
+// complete, overlapping the node pass (its sizes are known up front; the node CSR's are not).
+struct HostSink {
+  int64_t* h_elem_off;
+  int32_t* h_elem_idx;
+  cudaStream_t side;
+  cudaEvent_t ev;
+  bool issued;
+};
+
 template <int T, int BINS>
 static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool want_node, bool want_elem,
-                              mn_csr* node_out, mn_csr* elem_out, mn_error_detail* err) {
+                              mn_csr* node_out, mn_csr* elem_out, mn_error_detail* err, HostSink* sink = nullptr) {
   cudaStream_t s = mem.s;
   mn_status st = MN_OK;
   const int nd = P.dp.nd;
@@ -629,6 +639,14 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       }));
     }   // LSD element path
 
+    if (sink && want_elem) {   // element CSR complete: stream it to the host during the node pass
+      MN_CUDA(cudaEventRecord(sink->ev, s));
+      MN_CUDA(cudaStreamWaitEvent(sink->side, sink->ev, 0));
+      MN_CUDA(cudaMemcpyAsync(sink->h_elem_off, eoff, (size_t)(P.N + 1) * 8, cudaMemcpyDeviceToHost, sink->side));
+      if (P.Pe)
+        MN_CUDA(cudaMemcpyAsync(sink->h_elem_idx, eidx, (size_t)P.Pe * 4, cudaMemcpyDeviceToHost, sink->side));
+      sink->issued = true;
+    }
     int64_t U = 0;
     if (want_node) {
       // ---- a1 + a3n + a4 (nodes): expand the element CSR per node, sort + dedupe per node ----
@@ -698,6 +716,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     return MN_OK;
   }
 done:
+  if (sink && sink->issued) cudaStreamSynchronize(sink->side);
   if (ws) { cudaStreamSynchronize(s); mem.put(ws); }
   mem.put(node_off);
   mem.put(elem_off);
@@ -908,16 +927,16 @@ static mn_status check_args(int t, const void* conn, int64_t M, int64_t N) {
 
 template <int T>
 static mn_status dispatch_inc(const Plan& P, const int32_t* conn, Mem& mem, bool wn, bool we, mn_csr* no,
-                              mn_csr* eo, mn_error_detail* err) {
-  if (P.bins == 256) return pipeline_inc<T, 256>(P, conn, mem, wn, we, no, eo, err);
-  return pipeline_inc<T, 512>(P, conn, mem, wn, we, no, eo, err);
+                              mn_csr* eo, mn_error_detail* err, HostSink* sink) {
+  if (P.bins == 256) return pipeline_inc<T, 256>(P, conn, mem, wn, we, no, eo, err, sink);
+  return pipeline_inc<T, 512>(P, conn, mem, wn, we, no, eo, err, sink);
 }
 
 // sortpairs = the paper's node pipeline verbatim (node pairs -> global LSD sort -> unique);
 // otherwise the element-CSR expansion path (identical output).
 static mn_status find(int t, const int32_t* conn, int64_t M, int64_t N, const mn_allocator* a,
                       mn_stream stream, bool wn, bool we, mn_csr* no, mn_csr* eo, mn_error_detail* err,
-                      bool sortpairs = false) {
+                      bool sortpairs = false, HostSink* sink = nullptr) {
   if (err) { err->elem = -1; err->pos = -1; }
   mn_status st = check_args(t, conn, M, N);
   if (st != MN_OK) return st;
@@ -933,10 +952,10 @@ static mn_status find(int t, const int32_t* conn, int64_t M, int64_t N, const mn
     }
   }
   switch (t) {
-    case MN_TRI3: return dispatch_inc<MN_TRI3>(P, conn, mem, wn, we, no, eo, err);
-    case MN_QUAD4: return dispatch_inc<MN_QUAD4>(P, conn, mem, wn, we, no, eo, err);
-    case MN_TET4: return dispatch_inc<MN_TET4>(P, conn, mem, wn, we, no, eo, err);
-    default: return dispatch_inc<MN_HEX8>(P, conn, mem, wn, we, no, eo, err);
+    case MN_TRI3: return dispatch_inc<MN_TRI3>(P, conn, mem, wn, we, no, eo, err, sink);
+    case MN_QUAD4: return dispatch_inc<MN_QUAD4>(P, conn, mem, wn, we, no, eo, err, sink);
+    case MN_TET4: return dispatch_inc<MN_TET4>(P, conn, mem, wn, we, no, eo, err, sink);
+    default: return dispatch_inc<MN_HEX8>(P, conn, mem, wn, we, no, eo, err, sink);
   }
 }
 
@@ -1427,38 +1446,61 @@ mn_status mn_find_neighbors_both_host(mn_elem_type t, const int32_t* h_conn, int
   if (st != MN_OK) return st;
   if (!host_alloc || !host_alloc->alloc || !no || !eo) return MN_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
+  static thread_local cudaStream_t side = nullptr;
+  static thread_local cudaEvent_t ev = nullptr;
+  if (!side && cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) return MN_ERR_CUDA;
+  if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return MN_ERR_CUDA;
   Mem mem(dev_alloc, s);
-  const size_t cbytes = (size_t)M * arity_of(t) * 4;
-  int32_t* d_conn = (int32_t*)mem.get(cbytes);
-  if (!d_conn) return MN_ERR_OOM;
+  const int64_t Pe = (int64_t)M * arity_of(t);
+  const size_t cbytes = (size_t)Pe * 4;
+  std::memset(no, 0, sizeof(*no));
+  std::memset(eo, 0, sizeof(*eo));
+  // host outputs whose sizes are known up front
+  no->owner = eo->owner = *host_alloc;
+  no->num_nodes = eo->num_nodes = N;
+  no->offsets = (int64_t*)host_alloc->alloc(host_alloc->ctx, (size_t)(N + 1) * 8, stream);
+  eo->offsets = (int64_t*)host_alloc->alloc(host_alloc->ctx, (size_t)(N + 1) * 8, stream);
+  eo->indices = Pe ? (int32_t*)host_alloc->alloc(host_alloc->ctx, (size_t)Pe * 4, stream) : nullptr;
+  eo->nnz = Pe;
   mn_csr dn{}, de{};
+  int32_t* d_conn = nullptr;
+  HostSink sink{eo->offsets, eo->indices, side, ev, false};
+  if (!no->offsets || !eo->offsets || (Pe && !eo->indices)) { st = MN_ERR_OOM; goto fail; }
+  d_conn = (int32_t*)mem.get(cbytes);
+  if (!d_conn) { st = MN_ERR_OOM; goto fail; }
   if (cbytes && cudaMemcpyAsync(d_conn, h_conn, cbytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
-    mem.put(d_conn);
-    return MN_ERR_CUDA;
+    st = MN_ERR_CUDA;
+    goto fail;
   }
-  st = find(t, d_conn, M, N, &mem.a, stream, true, true, &dn, &de, err);
-  if (st != MN_OK) { mem.put(d_conn); return st; }
-  mn_csr* outs[2] = {no, eo};
-  mn_csr* devs[2] = {&dn, &de};
-  for (int i = 0; i < 2 && st == MN_OK; ++i) {
-    mn_csr* o = outs[i];
-    mn_csr* d = devs[i];
-    std::memset(o, 0, sizeof(*o));
-    o->num_nodes = d->num_nodes;
-    o->nnz = d->nnz;
-    o->owner = *host_alloc;
-    o->offsets = (int64_t*)host_alloc->alloc(host_alloc->ctx, (size_t)(N + 1) * 8, stream);
-    o->indices = d->nnz ? (int32_t*)host_alloc->alloc(host_alloc->ctx, (size_t)d->nnz * 4, stream) : nullptr;
-    if (!o->offsets || (d->nnz && !o->indices)) { st = MN_ERR_OOM; break; }
-    if (cudaMemcpyAsync(o->offsets, d->offsets, (size_t)(N + 1) * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        (d->nnz && cudaMemcpyAsync(o->indices, d->indices, (size_t)d->nnz * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess))
-      st = MN_ERR_CUDA;
+  st = find(t, d_conn, M, N, &mem.a, stream, true, true, &dn, &de, err, false, &sink);
+  if (st != MN_OK) goto fail;
+  if (!sink.issued &&   // (M == 0 returns before the sink point)
+      cudaMemcpyAsync(eo->offsets, de.offsets, (size_t)(N + 1) * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
+    st = MN_ERR_CUDA;
+    goto fail;
   }
-  if (st == MN_OK && cudaStreamSynchronize(s) != cudaSuccess) st = MN_ERR_CUDA;
+  no->nnz = dn.nnz;
+  if (dn.nnz) {
+    no->indices = (int32_t*)host_alloc->alloc(host_alloc->ctx, (size_t)dn.nnz * 4, stream);
+    if (!no->indices) { st = MN_ERR_OOM; goto fail; }
+  }
+  if (cudaMemcpyAsync(no->offsets, dn.offsets, (size_t)(N + 1) * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      (dn.nnz && cudaMemcpyAsync(no->indices, dn.indices, (size_t)dn.nnz * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess))
+    st = MN_ERR_CUDA;
+  if (cudaStreamSynchronize(side) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) st = MN_ERR_CUDA;
+  if (st != MN_OK) goto fail;
   mn_csr_release(&dn, stream);
   mn_csr_release(&de, stream);
   mem.put(d_conn);
-  if (st != MN_OK) { mn_csr_release(no, stream); mn_csr_release(eo, stream); }
+  return MN_OK;
+fail:
+  cudaStreamSynchronize(side);
+  cudaStreamSynchronize(s);
+  mn_csr_release(&dn, stream);
+  mn_csr_release(&de, stream);
+  mem.put(d_conn);
+  mn_csr_release(no, stream);
+  mn_csr_release(eo, stream);
   return st;
 }
 

@@ -218,12 +218,22 @@ def test_high_valence_fans(ntri, elem_path):
     _assert_csr((eo, ei), oracle.elem_csr(0, conn, N), f"fan{ntri} elem")
 
 
-def test_whole_path_host_buffers():
-    conn, N = meshgen.kuhn_tets(9)
-    (no, ni), (eo, ei) = mn().find_neighbors_host(conn.pin_memory(), "tet4", N)
-    assert not no.is_cuda and no.is_pinned()
-    _assert_csr((no, ni), oracle.node_csr(meshgen.TET4, conn, N), "host node")
-    _assert_csr((eo, ei), oracle.elem_csr(meshgen.TET4, conn, N), "host elem")
+@pytest.mark.parametrize("name,et,make", SMALL[:6] + [SMALL[-1]])
+def test_whole_path_host_buffers(name, et, make, elem_path):
+    conn, N = make()
+    (no, ni), (eo, ei) = mn().find_neighbors_host(conn.contiguous().pin_memory(), et, N)
+    assert not no.is_cuda and no.is_pinned() and not ei.is_cuda
+    _assert_csr((no, ni), oracle.node_csr(et, conn, N), name + " host node")
+    _assert_csr((eo, ei), oracle.elem_csr(et, conn, N), name + " host elem")
+
+
+def test_host_buffers_errors_and_empty():
+    bad = torch.tensor([[0, 1, 2], [1, 2, 9]], dtype=torch.int32)
+    with pytest.raises(mn().MeshError) as ei:
+        mn().find_neighbors_host(bad.pin_memory(), 0, 5)
+    assert (ei.value.code, ei.value.elem, ei.value.pos) == (2, 1, 2)
+    (no, ni), (eo, ei_) = mn().find_neighbors_host(torch.zeros((0, 4), dtype=torch.int32), 2, 7)
+    assert no.tolist() == [0] * 8 and eo.tolist() == [0] * 8 and ni.numel() == 0 and ei_.numel() == 0
 
 
 def test_config2_sphere_full(elem_path):
