@@ -49,7 +49,7 @@ def _load():
         lib.oracle_validate.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
                                         ctypes.c_int64, p64, p32]
         lib.oracle_validate.restype = ctypes.c_int
-        for fn in (lib.oracle_node_csr, lib.oracle_elem_csr):
+        for fn in (lib.oracle_node_csr, lib.oracle_elem_csr, lib.oracle_node_shared_csr):
             fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                            pp64, pp32, p64, p64, p32]
             fn.restype = ctypes.c_int
@@ -105,6 +105,11 @@ def _csr(fn, etype, conn, num_nodes):
 def node_csr(etype: int, conn, num_nodes: int):
     """One-ring neighbouring nodes of every vertex as CSR (int64 offsets, int32 indices)."""
     return _csr(_load().oracle_node_csr, etype, conn, num_nodes)
+
+
+def node_shared_csr(etype: int, conn, num_nodes: int):
+    """Element-sharing node adjacency: u, v neighbours iff some element contains both."""
+    return _csr(_load().oracle_node_shared_csr, etype, conn, num_nodes)
 
 
 def elem_csr(etype: int, conn, num_nodes: int):

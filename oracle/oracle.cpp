@@ -103,6 +103,25 @@ int oracle_node_csr(int etype, const int32_t* conn, int64_t M, int64_t N, int64_
   return OK;
 }
 
+// Element-sharing ("FEM sparsity") node mode: adj(v) = { u != v : some element
+// contains both u and v }.  Equals the edge adjacency for simplices; adds the diagonals of quads
+// and hexes.
+int oracle_node_shared_csr(int etype, const int32_t* conn, int64_t M, int64_t N, int64_t** offsets,
+                           int32_t** indices, int64_t* nnz, int64_t* err_elem, int32_t* err_pos) {
+  int rc = oracle_validate(etype, conn, M, N, err_elem, err_pos);
+  if (rc != OK) return rc;
+  const int k = kTables[etype].arity;
+  std::vector<std::set<int32_t>> S((size_t)N);
+  for (int64_t e = 0; e < M; ++e) {
+    const int32_t* row = conn + e * k;
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j)
+        if (i != j) S[(size_t)row[i]].insert(row[j]);
+  }
+  flatten(S, N, offsets, indices, nnz);
+  return OK;
+}
+
 // Element mode: inc(v) = { e : v in conn[e] }, ascending (elements are visited in order).
 int oracle_elem_csr(int etype, const int32_t* conn, int64_t M, int64_t N, int64_t** offsets,
                     int32_t** indices, int64_t* nnz, int64_t* err_elem, int32_t* err_pos) {

@@ -457,3 +457,42 @@ def test_generator_sizes():
     conn, N = meshgen.kuhn_tets(8)
     assert conn.shape == (6 * 512, 4) and N == 729
     assert meshgen.kuhn_tets(8, cell_begin=100, cell_end=200)[0].equal(conn[600:1200])
+
+
+# ------------------------------------------------------------------------------------------------
+# element-sharing node adjacency: pattern(B^T B) - I for every element type,
+# brute force from its definition, and equal to the edge adjacency for simplices
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("make,et", [(lambda: meshgen.hex_grid(3), 3), (lambda: meshgen.quad_grid(4, 5), 1),
+                                     (lambda: meshgen.random_mesh(3, 60, 80, seed=13), 3),
+                                     (lambda: meshgen.random_mesh(1, 90, 60, seed=14), 1)])
+def test_shared_adjacency_is_incidence_pattern(make, et):
+    conn, N = make()
+    B = _incidence(conn, N)
+    A = (B.T @ B).tolil()
+    A.setdiag(0)
+    A = sp.csr_matrix(A)
+    A.eliminate_zeros()
+    A.sort_indices()
+    off, idx = oracle.node_shared_csr(et, conn, N)
+    assert off.tolist() == A.indptr.tolist() and idx.tolist() == A.indices.tolist()
+
+
+def test_shared_adjacency_brute_force_and_simplices():
+    conn, N = meshgen.random_mesh(meshgen.HEX8, 4, 14, seed=15)
+    c = _np(conn)
+    brute = [sorted({int(x) for row in c if v in row.tolist() for x in row.tolist() if x != v}) for v in range(N)]
+    assert _slices(*oracle.node_shared_csr(3, conn, N)) == brute
+    for make, et in [(lambda: meshgen.kuhn_tets(3), 2), (lambda: meshgen.tri_grid(4, 3), 0)]:
+        conn, N = make()
+        a, b = oracle.node_shared_csr(et, conn, N), oracle.node_csr(et, conn, N)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    # interior hex node: 26 sharing neighbours (the 3x3x3 block); interior quad node: 8
+    n = 4
+    conn, N = meshgen.hex_grid(n)
+    off, _ = oracle.node_shared_csr(3, conn, N)
+    v = 2 + 5 * (2 + 5 * 2)
+    assert off[v + 1] - off[v] == 26
+    conn, N = meshgen.quad_grid(4, 4)
+    off, _ = oracle.node_shared_csr(1, conn, N)
+    assert off[12 + 1] - off[12] == 8
