@@ -36,6 +36,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--outputs", default="both", choices=["both", "shared"],
+                    help="both = node + element CSR (the headline); shared = element-sharing node "
+                         "adjacency (SURVEY §8(f) row 3), N=1 only")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
     return ap.parse_args()
 
@@ -132,7 +135,7 @@ def workload(cfg, rank, world, device):
     return et, conn, 0, M, N, info
 
 
-def oracle_sample(conn_full_dev, et, target_s, k_layers_hint=None):
+def oracle_sample(conn_full_dev, et, target_s, k_layers_hint=None, outputs="both"):
     """Time the oracle (std::set serial baseline, 1 thread) on a bounded prefix of the workload:
     the first Ms elements with N trimmed to the largest node id + 1.  Returns (elements/s,
     description, seconds)."""
@@ -145,11 +148,15 @@ def oracle_sample(conn_full_dev, et, target_s, k_layers_hint=None):
         sub = conn_full_dev[:ms].cpu().numpy()
         n_s = int(sub.max()) + 1 if sub.size else 0
         t0 = time.perf_counter()
-        oracle.node_csr(et, sub, n_s)
-        oracle.elem_csr(et, sub, n_s)
+        if outputs == "shared":
+            oracle.node_shared_csr(et, sub, n_s)
+        else:
+            oracle.node_csr(et, sub, n_s)
+            oracle.elem_csr(et, sub, n_s)
         dt = time.perf_counter() - t0
+        what = "element-sharing node CSR" if outputs == "shared" else "node + element CSR"
         if dt >= 0.6 * target_s or ms >= M:
-            return ms / dt, (f"first {ms:,} of {M:,} elements (node ids < {n_s:,}), node + element CSR, "
+            return ms / dt, (f"first {ms:,} of {M:,} elements (node ids < {n_s:,}), {what}, "
                              f"1 thread, {dt:.1f} s"), dt, ms
         ms = min(M, int(ms * max(1.5, min(8.0, target_s / max(dt, 1e-3)))))
 
@@ -245,7 +252,13 @@ def run_ours(args):
     M_local = conn.shape[0]
     torch.cuda.synchronize()
 
-    if world > 1:
+    if args.outputs == "shared":
+        if world > 1:
+            raise SystemExit("--outputs shared is single-GPU")
+
+        def step():
+            return mn.find_node_neighbors_shared(conn, et, N)
+    elif world > 1:
         from paper_1604_04689_b200.dist import find_neighbors_dist
 
         def step():
@@ -321,7 +334,7 @@ def run_ours(args):
 
     # ---- end to end through the public host-buffer API ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.outputs == "both":
         host_conn = conn.cpu().pin_memory()
         h2d = host_conn.numel() * 4
 
@@ -361,7 +374,7 @@ def run_ours(args):
     # ---- CPU baseline: the oracle on a bounded sample, rank 0 at N=1 only ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, desc, dt, ms_s = oracle_sample(conn, et, args.cpu_seconds)
+        v, desc, dt, ms_s = oracle_sample(conn, et, args.cpu_seconds, outputs=args.outputs)
         cpu = {"value": v, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": desc}
 
     if rank == 0:
@@ -372,7 +385,9 @@ def run_ours(args):
             "config": {"workload": f"config {args.config}: {info['desc']}", "elements": M_total, "nodes": N,
                        "parallelism": "single GPU" if world == 1 else
                        f"{world} GPUs: element shards + NCCL all-to-all by owner node range",
-                       "l2": "inputs larger than L2 (no flush needed)", "outputs": "node + element CSR"},
+                       "l2": "inputs larger than L2 (no flush needed)",
+                       "outputs": "node + element CSR" if args.outputs == "both" else
+                       "element-sharing node CSR"},
             "roofline": roofline, "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -101,6 +101,14 @@ mn_status mn_find_node_neighbors_sortpairs(mn_elem_type type, const int32_t* d_c
                                            int64_t num_nodes, const mn_allocator* alloc, mn_stream stream,
                                            mn_csr* out, mn_error_detail* err);
 
+/* Element-sharing ("FEM sparsity") node adjacency (the title's "generic
+ * meshes"): u and v are neighbours iff some element contains both, i.e. the pattern of B^T B minus
+ * the diagonal.  Identical to mn_find_node_neighbors for TRI3/TET4; adds the face and body
+ * diagonals of QUAD4/HEX8.  Same conventions and outputs as mn_find_node_neighbors. */
+mn_status mn_find_node_neighbors_shared(mn_elem_type type, const int32_t* d_conn, int64_t num_elems,
+                                        int64_t num_nodes, const mn_allocator* alloc, mn_stream stream,
+                                        mn_csr* out, mn_error_detail* err);
+
 /* One-ring neighbouring ELEMENTS of every vertex (§2.2.2: pairs (node, element
  * itself), sorted by node, segmented reduction and scan).  Slices list element ids ascending. */
 mn_status mn_find_elem_neighbors(mn_elem_type type, const int32_t* d_conn, int64_t num_elems,

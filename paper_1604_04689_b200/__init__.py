@@ -17,7 +17,7 @@ import torch
 
 __all__ = [
     "TRI3", "QUAD4", "TET4", "HEX8", "MeshError", "lib_path", "load",
-    "find_node_neighbors", "find_node_neighbors_sortpairs", "find_elem_neighbors", "find_neighbors", "find_neighbors_host",
+    "find_node_neighbors", "find_node_neighbors_sortpairs", "find_node_neighbors_shared", "find_elem_neighbors", "find_neighbors", "find_neighbors_host",
     "workspace_bytes", "node_key_bits", "node_key_bytes", "find_neighbors_chunked", "chunk_workspace_bytes",
     "emit_node_pairs", "emit_elem_pairs", "radix_sort_keys", "radix_sort_pairs_u32",
     "unique_node_csr", "elem_offsets", "exclusive_scan",
@@ -80,6 +80,8 @@ def _declare(lib):
         "mn_find_elem_neighbors": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _VP, _P(_Csr), _P(_ErrDetail)]),
         "mn_find_node_neighbors_sortpairs": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _VP, _P(_Csr),
                                                  _P(_ErrDetail)]),
+        "mn_find_node_neighbors_shared": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _VP, _P(_Csr),
+                                              _P(_ErrDetail)]),
         "mn_find_neighbors_both": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _VP, _P(_Csr), _P(_Csr),
                                        _P(_ErrDetail)]),
         "mn_find_neighbors_both_host": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _P(_Allocator), _VP,
@@ -258,6 +260,20 @@ def find_node_neighbors_sortpairs(conn: torch.Tensor, etype, num_nodes: int, str
     with torch.cuda.device(c.device):
         rc = lib.mn_find_node_neighbors_sortpairs(et, c.data_ptr(), M, int(num_nodes), ctypes.byref(al.struct),
                                                   _stream_ptr(stream), ctypes.byref(out), ctypes.byref(err))
+    _check(rc, err)
+    return _take(al, out)
+
+
+def find_node_neighbors_shared(conn: torch.Tensor, etype, num_nodes: int, stream=None):
+    """Element-sharing node adjacency (u, v neighbours iff some element contains both)."""
+    et = _etype(etype)
+    c, M = _conn_arg(conn, et)
+    lib = load()
+    al = _TorchAllocator(c.device)
+    out, err = _Csr(), _ErrDetail()
+    with torch.cuda.device(c.device):
+        rc = lib.mn_find_node_neighbors_shared(et, c.data_ptr(), M, int(num_nodes), ctypes.byref(al.struct),
+                                               _stream_ptr(stream), ctypes.byref(out), ctypes.byref(err))
     _check(rc, err)
     return _take(al, out)
 

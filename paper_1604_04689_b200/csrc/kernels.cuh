@@ -11,6 +11,7 @@
 //   k_elem_offsets    run starts of the sorted element-pair keys -> offsets
 //   k_scan_i32        single-pass look-back exclusive scan (standalone row a5)
 #pragma once
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -720,19 +721,40 @@ constexpr int kNodeThreads = 128;
 constexpr int kHashSlots = 32;
 constexpr int kMaxUnique = 24;
 
+// The L <= NET distinct values in slots [0, L) of a thread's set column, sorted in registers and
+// written to out[0, L).  Node ids are < 2^31, so INT32_MAX pads the network.
+template <int NET, int HS>
+__device__ __forceinline__ void sort_small(uint32_t (*tab)[kNodeThreads], int t, int L, uint32_t* out) {
+  int32_t v[NET];
+#pragma unroll
+  for (int i = 0; i < NET; ++i) v[i] = (i < L && i < HS) ? (int32_t)tab[i < HS ? i : 0][t] : INT32_MAX;
+  oddeven_sort<NET>(v);
+#pragma unroll
+  for (int i = 0; i < NET; ++i)
+    if (i < L) out[i] = (uint32_t)v[i];
+}
+
 // (Fusing the element-list sort of the transpose path into this kernel, with the CTA's incidence
 // range staged in shared memory, was measured slower on B200: the extra registers / shared memory
 // cost more occupancy than the saved pass.)
-template <int T, bool ALIGNED, bool DIST = false>
+// SHARED: element-sharing ("FEM sparsity") adjacency — every other node of an incident element
+// is a neighbour, so each incidence yields CE = K - 1 candidates.
+template <int T, bool ALIGNED, bool DIST = false, bool SHARED = false>
 __global__ void __launch_bounds__(kNodeThreads)
 k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, RowSrc rs,
                 int64_t N, uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, int32_t* __restrict__ lofs,
                 uint32_t* __restrict__ giants, unsigned int* __restrict__ ngiant,
                 const unsigned long long* __restrict__ err, int64_t a_base = 0) {
-  constexpr int C = Elem<T>::C, K = Elem<T>::K, B = 4;   // incidences in flight per thread
+  constexpr int K = Elem<T>::K, B = 4;                   // incidences in flight per thread
+  constexpr int C = SHARED ? K - 1 : Elem<T>::C;          // candidates per incidence
   constexpr uint32_t EMPTY = 0xFFFFFFFFu;
-  __shared__ uint32_t tab[kHashSlots][kNodeThreads];
-  __shared__ uint32_t lst[kMaxUnique + 1][kNodeThreads];
+  // shared hex has 26 distinct neighbours per interior node: a 64-slot set, up to 40 kept; every
+  // other instantiation 32 slots / 24 kept.  The distinct values are compacted in place at the end
+  // (no separate list array: 16 KB / 32 KB per CTA, so registers, not shared memory, bound occupancy)
+  constexpr bool WIDE = SHARED && K == 8;
+  constexpr int HB = WIDE ? 6 : 5, HS = 1 << HB, MU = WIDE ? 40 : kMaxUnique;
+  using Mask = typename std::conditional<(HS > 32), unsigned long long, uint32_t>::type;
+  __shared__ uint32_t tab[HS][kNodeThreads];
   __shared__ uint32_t s_wsum[kNodeThreads / 32];
   if (err && *err != ERR_NONE) return;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -744,12 +766,13 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
   const int32_t* inc = eidx + s0;
   int L = 0;
   int64_t raw = 0;
+  Mask used = 0;   // occupied slots of the set
   if (valid) {
 #pragma unroll
-    for (int i = 0; i < kHashSlots; ++i) tab[i][t] = EMPTY;
+    for (int i = 0; i < HS; ++i) tab[i][t] = EMPTY;
     const int64_t d = d0;
     raw = (int64_t)C * d;
-    for (int64_t i0 = 0; i0 < d && L <= kMaxUnique; i0 += B) {
+    for (int64_t i0 = 0; i0 < d && L <= MU; i0 += B) {
       int e[B];
 #pragma unroll
       for (int q = 0; q < B; ++q) e[q] = (i0 + q < d) ? inc[i0 + q] : -1;
@@ -762,29 +785,29 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
         if (e[q] < 0) continue;
         // simplices (TRI3, TET4): every other node of the element is an edge neighbour, so the
         // candidates are the row values != a; otherwise the local neighbour table is used
-        constexpr bool simplex = (C == K - 1);
+        constexpr bool simplex = (C == K - 1);   // simplices and SHARED: all other row values
         const int p = simplex ? 0 : local_of<T>(row[q], (int)(a + a_base));
 #pragma unroll
         for (int c = 0; c < (simplex ? K : C); ++c) {
           const uint32_t v = simplex ? (uint32_t)row[q][c] : pick<T>(row[q], nbr_local<T>(p, c));
           if (simplex && v == (uint32_t)(a + a_base)) continue;
-          uint32_t h = (v * 0x9E3779B1u) >> 27;
-          while (L <= kMaxUnique) {   // at most kMaxUnique + 1 entries: the set never fills
+          uint32_t h = (v * 0x9E3779B1u) >> (32 - HB);
+          while (L <= MU) {   // at most MU + 1 entries: the set never fills
             const uint32_t x = tab[h][t];
             if (x == v) break;
             if (x == EMPTY) {
               tab[h][t] = v;
-              lst[L][t] = v;
+              used |= Mask(1) << h;
               ++L;
               break;
             }
-            h = (h + 1) & (kHashSlots - 1);
+            h = (h + 1) & (HS - 1);
           }
         }
       }
     }
   }
-  const bool giant = valid && L > kMaxUnique;
+  const bool giant = valid && L > MU;
   // ---- dense per-CTA layout: node lists packed from C * eoff[n0]; a giant reserves raw slots ----
   const uint32_t size = valid ? (giant ? (uint32_t)raw : (uint32_t)L) : 0u;
   uint32_t incl = size;
@@ -805,30 +828,46 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
     giants[atomicAdd(ngiant, 1u)] = (uint32_t)a;
     return;
   }
-  for (int i = 1; i < L; ++i) {
-    const uint32_t x = lst[i][t];
-    int j = i - 1;
-    while (j >= 0 && lst[j][t] > x) {
-      lst[j + 1][t] = lst[j][t];
-      --j;
+  {   // compact the set to its first L slots (write index <= read index)
+    int w = 0;
+    while (used) {
+      const int i = (HS > 32) ? __ffsll((long long)used) - 1 : __ffs((int)used) - 1;
+      used &= used - 1;
+      tab[w++][t] = tab[i][t];
     }
-    lst[j + 1][t] = x;
   }
   uint32_t* out = temp + (size_t)C * eoff[n0] + excl;
-  for (int i = 0; i < L; ++i) out[i] = lst[i][t];
+  // sort: a register bitonic network sized by the warp's largest set (warp-uniform, no divergence)
+  const int lmax = __reduce_max_sync(__activemask(), (unsigned)L);
+  if (lmax <= 8) sort_small<8, HS>(tab, t, L, out);
+  else if (lmax <= 16) sort_small<16, HS>(tab, t, L, out);
+  else if (lmax <= 32) sort_small<32, HS>(tab, t, L, out);
+  else {
+    for (int i = 1; i < L; ++i) {
+      const uint32_t x = tab[i][t];
+      int j = i - 1;
+      while (j >= 0 && tab[j][t] > x) {
+        tab[j + 1][t] = tab[j][t];
+        --j;
+      }
+      tab[j + 1][t] = x;
+    }
+    for (int i = 0; i < L; ++i) out[i] = tab[i][t];
+  }
   cnt[a] = L;
 }
 
 // Nodes with more than 256 raw neighbour entries (or more than 32 distinct neighbours): one CTA per
 // node, the raw entries sorted with a block bitonic network (shared memory when they fit, else in
 // place in the node's global raw region), then adjacent-difference dedupe.
-template <int T, bool ALIGNED, bool DIST = false>
+template <int T, bool ALIGNED, bool DIST = false, bool SHARED = false>
 __global__ void __launch_bounds__(1024)
 k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, RowSrc rs,
              uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, const int32_t* __restrict__ lofs,
              const uint32_t* __restrict__ giants, const unsigned int* __restrict__ ngiant, int smem_cap,
              const unsigned long long* __restrict__ err, int64_t a_base = 0) {
-  constexpr int C = Elem<T>::C, K = Elem<T>::K;
+  constexpr int K = Elem<T>::K;
+  constexpr int C = SHARED ? K - 1 : Elem<T>::C;
   extern __shared__ uint32_t sv[];
   __shared__ int s_u;
   if (err && *err != ERR_NONE) return;
@@ -844,9 +883,16 @@ k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx,
     for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
       int row[K];
       fetch_row<T, ALIGNED, DIST>(rs, eidx[s + i], row);
-      const int p = local_of<T>(row, (int)(a + a_base));
+      if (C == K - 1) {   // simplices and SHARED: the other row values
+        int c = 0;
 #pragma unroll
-      for (int c = 0; c < C; ++c) buf[i * C + c] = pick<T>(row, nbr_local<T>(p, c));
+        for (int q = 0; q < K; ++q)
+          if (row[q] != (int)(a + a_base)) buf[i * C + (c++)] = (uint32_t)row[q];
+      } else {
+        const int p = local_of<T>(row, (int)(a + a_base));
+#pragma unroll
+        for (int c = 0; c < C; ++c) buf[i * C + c] = pick<T>(row, nbr_local<T>(p, c));
+      }
     }
     __syncthreads();
     int64_t n2 = 1;

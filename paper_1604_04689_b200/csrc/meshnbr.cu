@@ -448,7 +448,9 @@ struct HostSink {
 
 template <int T, int BINS>
 static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool want_node, bool want_elem,
-                              mn_csr* node_out, mn_csr* elem_out, mn_error_detail* err, HostSink* sink = nullptr) {
+                              mn_csr* node_out, mn_csr* elem_out, mn_error_detail* err, HostSink* sink = nullptr,
+                              bool shared = false) {
+  const int CE = shared ? P.K - 1 : P.C;   // node candidates per incidence (node raw region: CE * Pe)
   cudaStream_t s = mem.s;
   mn_status st = MN_OK;
   const int nd = P.dp.nd;
@@ -526,7 +528,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       head = a.off;
       if (transpose) sgiants = a.take<uint32_t>((size_t)P.N + 1);
       // ekA | ekB | epA | epB (each 256-byte aligned, contiguous); later the node raw region
-      ekA = a.take<uint32_t>((size_t)P.Pe);
+      ekA = a.take<uint32_t>((size_t)P.Pe * (CE > 4 ? CE - 3 : 1));   // the 4 pieces hold >= CE * Pe
       ekB = a.take<uint32_t>((size_t)P.Pe);
       epA = a.take<uint32_t>((size_t)P.Pe);
       epB = a.take<uint32_t>((size_t)P.Pe);
@@ -650,13 +652,19 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     int64_t U = 0;
     if (want_node) {
       // ---- a1 + a3n + a4 (nodes): expand the element CSR per node, sort + dedupe per node ----
-      uint32_t* temp = ekA;   // C * Pe <= 4 * Pe entries: the dead element-sort buffers
+      uint32_t* temp = ekA;   // CE * Pe entries: the dead element-sort buffers (ekA widened when CE > 4)
       const double gb = 8.0 * (P.N + 1) + 4.0 * P.Pe + 4.0 * P.K * P.Pe;   // offsets, incidences, rows
       const unsigned ng = (unsigned)tiles_of(P.N, kNodeThreads);
       if (P.N > 0) {   // (M > 0 with N == 0 always fails validation: nothing to expand)
         MN_CUDA(launch("node_gather", gb, s, [&] {
           const RowSrc rs{conn, 0, P.M, nullptr, nullptr, 0};
-          if (aligned)
+          if (shared && aligned)
+            k_node_gather_t<T, true, false, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs,
+                                                                              giants, ngiant, errw);
+          else if (shared)
+            k_node_gather_t<T, false, false, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs,
+                                                                               giants, ngiant, errw);
+          else if (aligned)
             k_node_gather_t<T, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs, giants,
                                                                  ngiant, errw);
           else
@@ -669,12 +677,20 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       if (!giant_attr) {
         cudaFuncSetAttribute(k_node_giant<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
         cudaFuncSetAttribute(k_node_giant<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
+        cudaFuncSetAttribute(k_node_giant<T, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
+        cudaFuncSetAttribute(k_node_giant<T, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
         giant_attr = true;
       }
       MN_CUDA(launch("node_giant", 0.0, s, [&] {
         const RowSrc rs{conn, 0, P.M, nullptr, nullptr, 0};
-        if (aligned) k_node_giant<T, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw);
-        else k_node_giant<T, false><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw);
+        if (shared && aligned)
+          k_node_giant<T, true, false, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw);
+        else if (shared)
+          k_node_giant<T, false, false, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw);
+        else if (aligned)
+          k_node_giant<T, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw);
+        else
+          k_node_giant<T, false><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw);
       }));
       // ---- a5 (nodes): exclusive scan of the unique counts -> offsets ----
       if (P.N > 0)   // N == 0 with M > 0 always fails validation; nothing to scan
@@ -695,7 +711,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       if (U && !out) { st = MN_ERR_OOM; goto done; }
       if (U) {
         MN_CUDA(launch("node_compact", 8.0 * U + 24.0 * P.N, s, [&] {
-          k_node_compact<<<(unsigned)tiles_of(P.N, kNodeThreads), kNodeThreads, 0, s>>>(eoff, P.C, ekA, lofs,
+          k_node_compact<<<(unsigned)tiles_of(P.N, kNodeThreads), kNodeThreads, 0, s>>>(eoff, CE, ekA, lofs,
                                                                                          node_off, P.N, out);
         }));
       }
@@ -927,16 +943,16 @@ static mn_status check_args(int t, const void* conn, int64_t M, int64_t N) {
 
 template <int T>
 static mn_status dispatch_inc(const Plan& P, const int32_t* conn, Mem& mem, bool wn, bool we, mn_csr* no,
-                              mn_csr* eo, mn_error_detail* err, HostSink* sink) {
-  if (P.bins == 256) return pipeline_inc<T, 256>(P, conn, mem, wn, we, no, eo, err, sink);
-  return pipeline_inc<T, 512>(P, conn, mem, wn, we, no, eo, err, sink);
+                              mn_csr* eo, mn_error_detail* err, HostSink* sink, bool shared) {
+  if (P.bins == 256) return pipeline_inc<T, 256>(P, conn, mem, wn, we, no, eo, err, sink, shared);
+  return pipeline_inc<T, 512>(P, conn, mem, wn, we, no, eo, err, sink, shared);
 }
 
 // sortpairs = the paper's node pipeline verbatim (node pairs -> global LSD sort -> unique);
 // otherwise the element-CSR expansion path (identical output).
 static mn_status find(int t, const int32_t* conn, int64_t M, int64_t N, const mn_allocator* a,
                       mn_stream stream, bool wn, bool we, mn_csr* no, mn_csr* eo, mn_error_detail* err,
-                      bool sortpairs = false, HostSink* sink = nullptr) {
+                      bool sortpairs = false, HostSink* sink = nullptr, bool shared = false) {
   if (err) { err->elem = -1; err->pos = -1; }
   mn_status st = check_args(t, conn, M, N);
   if (st != MN_OK) return st;
@@ -952,10 +968,10 @@ static mn_status find(int t, const int32_t* conn, int64_t M, int64_t N, const mn
     }
   }
   switch (t) {
-    case MN_TRI3: return dispatch_inc<MN_TRI3>(P, conn, mem, wn, we, no, eo, err, sink);
-    case MN_QUAD4: return dispatch_inc<MN_QUAD4>(P, conn, mem, wn, we, no, eo, err, sink);
-    case MN_TET4: return dispatch_inc<MN_TET4>(P, conn, mem, wn, we, no, eo, err, sink);
-    default: return dispatch_inc<MN_HEX8>(P, conn, mem, wn, we, no, eo, err, sink);
+    case MN_TRI3: return dispatch_inc<MN_TRI3>(P, conn, mem, wn, we, no, eo, err, sink, shared);
+    case MN_QUAD4: return dispatch_inc<MN_QUAD4>(P, conn, mem, wn, we, no, eo, err, sink, shared);
+    case MN_TET4: return dispatch_inc<MN_TET4>(P, conn, mem, wn, we, no, eo, err, sink, shared);
+    default: return dispatch_inc<MN_HEX8>(P, conn, mem, wn, we, no, eo, err, sink, shared);
   }
 }
 
@@ -1409,6 +1425,11 @@ mn_status mn_find_node_neighbors(mn_elem_type t, const int32_t* d_conn, int64_t 
 mn_status mn_find_node_neighbors_sortpairs(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N,
                                            const mn_allocator* a, mn_stream s, mn_csr* out, mn_error_detail* err) {
   return find(t, d_conn, M, N, a, s, true, false, out, nullptr, err, true);
+}
+
+mn_status mn_find_node_neighbors_shared(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N,
+                                        const mn_allocator* a, mn_stream s, mn_csr* out, mn_error_detail* err) {
+  return find(t, d_conn, M, N, a, s, true, false, out, nullptr, err, false, nullptr, true);
 }
 
 mn_status mn_find_elem_neighbors(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N,

@@ -416,3 +416,43 @@ def test_chunked_fans_and_errors(ntri):
     with pytest.raises(mn().MeshError) as ei_:
         mn().find_neighbors_chunked(bad, 0, 5, 1 << 12)
     assert (ei_.value.code, ei_.value.elem, ei_.value.pos) == (2, 1, 2)
+
+
+# ------------------------------------------------------------------------------------------------
+# element-sharing node adjacency, SURVEY §8(f) row 3
+# ------------------------------------------------------------------------------------------------
+SHARED_EXTRA = [
+    # hex nodes with > 30 distinct sharing neighbours: 64-slot set overflow -> block path
+    ("rand_hex_dense", meshgen.HEX8, lambda: meshgen.random_mesh(meshgen.HEX8, 700, 200, seed=11)),
+    ("rand_quad_dense", meshgen.QUAD4, lambda: meshgen.random_mesh(meshgen.QUAD4, 2000, 150, seed=12)),
+    ("hex_grid_20", meshgen.HEX8, lambda: meshgen.hex_grid(20)),
+]
+
+
+@pytest.mark.parametrize("name,et,make", SMALL + SHARED_EXTRA)
+def test_shared_adjacency(name, et, make, elem_path):
+    conn, N = make()
+    _assert_csr(mn().find_node_neighbors_shared(conn.cuda(), et, N), oracle.node_shared_csr(et, conn, N),
+                name + " shared")
+
+
+def test_shared_adjacency_full_size_hex():
+    et, conn, N = meshgen.make_config(4, device="cuda")
+    off, idx = mn().find_node_neighbors_shared(conn, et, N)
+    n = 256
+    w = n + 1
+    i = torch.arange(N, device="cuda")
+    pi = torch.from_numpy(meshgen.seeded_permutation(N, 1604)).cuda()
+    ci, cj, ck = i % w, (i // w) % w, i // (w * w)
+    span = lambda x: 1 + (x > 0).long() + (x < n).long()
+    cnt = torch.zeros_like(off[1:])
+    cnt[pi] = span(ci) * span(cj) * span(ck) - 1        # the 3x3x3 block around the node, clipped
+    assert torch.equal(off[1:] - off[:-1], cnt)
+    assert _symmetric(off, idx)
+
+
+def test_shared_equals_edges_for_simplices_full_size():
+    et, conn, N = meshgen.make_config(3, device="cuda")
+    a = mn().find_node_neighbors_shared(conn, et, N)
+    b = mn().find_node_neighbors(conn, et, N)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
