@@ -193,6 +193,93 @@ def nonmanifold_fan(num_tris: int = 3):
 
 
 # --------------------------------------------------------------------------------------------
+# polygon / mixed-arity surface meshes: (off int64 [M+1], idx int32 [off[M]], num_nodes); element
+# e is the ring idx[off[e]:off[e+1]] (SPEC.md Mesh.element_kind Polygon)
+# --------------------------------------------------------------------------------------------
+def poly_from_conn(conn: torch.Tensor):
+    """A fixed-arity connectivity [M, k] as a polygon mesh (same rings)."""
+    M, k = conn.shape
+    off = torch.arange(M + 1, device=conn.device, dtype=torch.int64) * k
+    return off, conn.reshape(-1).to(torch.int32).contiguous()
+
+
+def poly_mixed_grid(rows: int, cols: int, seed: int = 1604, device=None):
+    """Mixed triangle/quad grid, tri_grid's node numbering.  Cell c = i + cols j becomes, by
+    splitmix64(seed)[c] % 3: 0 -> one quad (v00, v10, v11, v01); 1 -> triangles (v00, v10, v11),
+    (v00, v11, v01); 2 -> triangles (v00, v10, v01), (v10, v11, v01).  Elements in cell order."""
+    d = _dev(device)
+    w = cols + 1
+    i = torch.arange(cols, device=d, dtype=torch.int64)
+    j = torch.arange(rows, device=d, dtype=torch.int64)
+    jj, ii = torch.meshgrid(j, i, indexing="ij")
+    v00 = (ii + w * jj).reshape(-1)
+    v10, v01 = v00 + 1, v00 + w
+    v11 = v01 + 1
+    ch = torch.from_numpy((splitmix64(seed, rows * cols) % np.uint64(3)).astype(np.int64)).to(d)
+    neg = torch.full_like(v00, -1)
+    quad = torch.stack([v00, v10, v11, v01, neg, neg], -1)
+    t1 = torch.stack([v00, v10, v11, v00, v11, v01], -1)
+    t2 = torch.stack([v00, v10, v01, v10, v11, v01], -1)
+    slots = torch.where((ch == 0)[:, None], quad, torch.where((ch == 1)[:, None], t1, t2))
+    idx = slots.reshape(-1)
+    idx = idx[idx >= 0].to(torch.int32).contiguous()
+    ar = torch.where((ch == 0)[:, None], torch.tensor([4, 0], device=d), torch.tensor([3, 3], device=d)).reshape(-1)
+    ar = ar[ar > 0]
+    off = torch.zeros(ar.numel() + 1, dtype=torch.int64, device=d)
+    off[1:] = torch.cumsum(ar, 0)
+    return off, idx, (rows + 1) * (cols + 1)
+
+
+def honeycomb(rows: int, cols: int, device=None):
+    """Hexagon tiling as a brick wall: hexagon (i, j) (i < cols, j < rows), x = 2i + (j mod 2),
+    ring (x, j), (x+1, j), (x+2, j), (x+2, j+1), (x+1, j+1), (x, j+1); node (x, y) -> x + W y,
+    W = 2 cols + 2 (a few corner nodes stay isolated).  Interior nodes have 3 neighbours."""
+    d = _dev(device)
+    W = 2 * cols + 2
+    i = torch.arange(cols, device=d, dtype=torch.int64)
+    j = torch.arange(rows, device=d, dtype=torch.int64)
+    jj, ii = torch.meshgrid(j, i, indexing="ij")
+    x = (2 * ii + (jj % 2)).reshape(-1)
+    y = jj.reshape(-1)
+    ring = torch.stack([x + W * y, x + 1 + W * y, x + 2 + W * y, x + 2 + W * (y + 1), x + 1 + W * (y + 1),
+                        x + W * (y + 1)], -1)
+    off = torch.arange(rows * cols + 1, device=d, dtype=torch.int64) * 6
+    return off, ring.reshape(-1).to(torch.int32).contiguous(), W * (rows + 1)
+
+
+def random_poly(num_elems: int, num_nodes: int, kmin: int, kmax: int, seed: int, device=None):
+    """Polygons of arity uniform in [kmin, kmax] with distinct nodes drawn uniformly from
+    [0, num_nodes): non-manifold, isolated nodes, arbitrary orientation."""
+    rng = np.random.default_rng(seed)
+    ks = rng.integers(kmin, kmax + 1, size=num_elems)
+    off = np.zeros(num_elems + 1, dtype=np.int64)
+    off[1:] = np.cumsum(ks)
+    idx = np.concatenate([rng.choice(num_nodes, size=int(k), replace=False) for k in ks]) if num_elems else \
+        np.zeros(0, dtype=np.int64)
+    d = _dev(device)
+    return torch.from_numpy(off).to(d), torch.from_numpy(idx.astype(np.int32)).to(d), num_nodes
+
+
+def poly_relabel(off: torch.Tensor, idx: torch.Tensor, num_nodes: int, node_seed: int | None,
+                 elem_seed: int | None):
+    """relabel() for polygon meshes: node ids through pi, elements reordered by sigma."""
+    M = off.numel() - 1
+    if elem_seed is not None and M > 0:
+        sigma = torch.from_numpy(seeded_permutation(M, elem_seed)).to(off.device)
+        ar = (off[1:] - off[:-1])[sigma]
+        noff = torch.zeros_like(off)
+        noff[1:] = torch.cumsum(ar, 0)
+        start = off[:-1][sigma]
+        pos = torch.arange(int(noff[-1]), device=off.device) - torch.repeat_interleave(noff[:-1], ar)
+        idx = idx[torch.repeat_interleave(start, ar) + pos]
+        off = noff
+    if node_seed is not None:
+        pi = torch.from_numpy(seeded_permutation(num_nodes, node_seed)).to(idx.device)
+        idx = pi.to(torch.int32)[idx.long()]
+    return off.contiguous(), idx.to(torch.int32).contiguous()
+
+
+# --------------------------------------------------------------------------------------------
 # the five BASELINE.json configs
 # --------------------------------------------------------------------------------------------
 CONFIGS = {
@@ -207,6 +294,18 @@ CONFIGS = {
     5: dict(name="kuhn_tet_320", etype=TET4,
             desc="Kuhn tet mesh 320^3 cells (196,608,000 tets)"),
 }
+
+# polygon workload (not a BASELINE.json config): mixed tri/quad grid
+POLY_CONFIGS = {
+    6: dict(name="poly_mixed_8192", desc="mixed triangle/quad polygon grid 8192x8192 cells (seed 1604)"),
+}
+
+
+def make_poly_config(cfg: int, device=None):
+    """(off, idx, num_nodes) of a polygon workload."""
+    if cfg == 6:
+        return poly_mixed_grid(8192, 8192, 1604, device)
+    raise ValueError(f"unknown polygon config {cfg}")
 
 
 def make_config(cfg: int, device=None):

@@ -25,7 +25,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.cpp")
 
-OK, ERR_ARG, ERR_RANGE, ERR_DEGENERATE = 0, 1, 2, 3
+OK, ERR_ARG, ERR_RANGE, ERR_DEGENERATE, ERR_ARITY = 0, 1, 2, 3, 4
 
 
 def build(force: bool = False) -> str:
@@ -53,6 +53,12 @@ def _load():
             fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                            pp64, pp32, p64, p64, p32]
             fn.restype = ctypes.c_int
+        lib.oracle_poly_validate.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                             p64, p32]
+        lib.oracle_poly_validate.restype = ctypes.c_int
+        lib.oracle_poly_csr.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                        ctypes.c_int64, pp64, pp32, p64, p64, p32]
+        lib.oracle_poly_csr.restype = ctypes.c_int
         lib.oracle_free.argtypes = [ctypes.c_void_p]
         lib.oracle_free.restype = None
         _lib = lib
@@ -115,6 +121,58 @@ def node_shared_csr(etype: int, conn, num_nodes: int):
 def elem_csr(etype: int, conn, num_nodes: int):
     """One-ring neighbouring elements of every vertex as CSR (int64 offsets, int32 indices)."""
     return _csr(_load().oracle_elem_csr, etype, conn, num_nodes)
+
+
+# ---- polygon / mixed-arity meshes: (off int64[M+1], idx int32[off[M]]), ring edges ----
+def _as_poly(off, idx):
+    if hasattr(off, "detach"):
+        off = off.detach().cpu().numpy()
+    if hasattr(idx, "detach"):
+        idx = idx.detach().cpu().numpy()
+    return np.ascontiguousarray(off, dtype=np.int64), np.ascontiguousarray(idx, dtype=np.int32)
+
+
+def poly_validate(off, idx, num_nodes: int):
+    """(code, elem, pos) of the first invalid polygon, or (OK, -1, -1); ERR_ARITY has pos -1."""
+    lib = _load()
+    o, i = _as_poly(off, idx)
+    ee, ep = ctypes.c_int64(-1), ctypes.c_int32(-1)
+    rc = lib.oracle_poly_validate(o.ctypes.data, i.ctypes.data, o.shape[0] - 1, num_nodes,
+                                  ctypes.byref(ee), ctypes.byref(ep))
+    return rc, ee.value, ep.value
+
+
+def _poly(mode, off, idx, num_nodes):
+    lib = _load()
+    o, i = _as_poly(off, idx)
+    po = ctypes.POINTER(ctypes.c_int64)()
+    pi = ctypes.POINTER(ctypes.c_int32)()
+    nnz = ctypes.c_int64(0)
+    ee, ep = ctypes.c_int64(-1), ctypes.c_int32(-1)
+    rc = lib.oracle_poly_csr(mode, o.ctypes.data, i.ctypes.data, o.shape[0] - 1, num_nodes, ctypes.byref(po),
+                             ctypes.byref(pi), ctypes.byref(nnz), ctypes.byref(ee), ctypes.byref(ep))
+    if rc != OK:
+        raise OracleMeshError(rc, ee.value, ep.value)
+    offsets = np.ctypeslib.as_array(po, shape=(num_nodes + 1,)).copy()
+    indices = (np.ctypeslib.as_array(pi, shape=(nnz.value,)).copy() if nnz.value else np.zeros(0, np.int32))
+    lib.oracle_free(ctypes.cast(po, ctypes.c_void_p))
+    lib.oracle_free(ctypes.cast(pi, ctypes.c_void_p))
+    return offsets, indices
+
+
+def poly_node_csr(off, idx, num_nodes: int):
+    """Ring-edge node adjacency of a polygon mesh as CSR."""
+    return _poly(0, off, idx, num_nodes)
+
+
+def poly_elem_csr(off, idx, num_nodes: int):
+    """Element incidence of a polygon mesh as CSR."""
+    return _poly(1, off, idx, num_nodes)
+
+
+def poly_shared_csr(off, idx, num_nodes: int):
+    """Element-sharing node adjacency of a polygon mesh as CSR."""
+    return _poly(2, off, idx, num_nodes)
 
 
 from . import stages  # noqa: E402,F401  (numpy step-by-step oracle)

@@ -135,6 +135,64 @@ int oracle_elem_csr(int etype, const int32_t* conn, int64_t M, int64_t N, int64_
   return OK;
 }
 
+// ---- polygon / mixed-arity surface meshes (SPEC Mesh.element_kind Polygon) ----
+// Element e is the ring idx[off[e]], ..., idx[off[e+1]-1]; its edges are consecutive ring entries
+// plus the closing edge (SPEC Element: "order defines the edge ring for surface elements").
+// Validation per element, ascending (reading R18): arity >= 3 first (ERR_ARITY, pos -1), then the
+// range check over the ring, then the repeated-node check, as for the fixed types.
+enum { ERR_ARITY = 4 };
+
+int oracle_poly_validate(const int64_t* off, const int32_t* idx, int64_t M, int64_t N, int64_t* eelem,
+                         int32_t* epos) {
+  if (M < 0 || N < 0 || (M > 0 && off[0] != 0)) return ERR_ARG;
+  for (int64_t e = 0; e < M; ++e)
+    if (off[e + 1] < off[e]) return ERR_ARG;
+  *eelem = -1;
+  *epos = -1;
+  for (int64_t e = 0; e < M; ++e) {
+    const int64_t k = off[e + 1] - off[e];
+    const int32_t* row = idx + off[e];
+    if (k < 3) { *eelem = e; *epos = -1; return ERR_ARITY; }
+    for (int64_t p = 0; p < k; ++p)
+      if (row[p] < 0 || (int64_t)row[p] >= N) { *eelem = e; *epos = (int32_t)p; return ERR_RANGE; }
+    for (int64_t p = 1; p < k; ++p)
+      for (int64_t q = 0; q < p; ++q)
+        if (row[q] == row[p]) { *eelem = e; *epos = (int32_t)p; return ERR_DEGENERATE; }
+  }
+  return OK;
+}
+
+// mode 0: ring-edge node adjacency; 1: element incidence; 2: element-sharing node adjacency
+int oracle_poly_csr(int mode, const int64_t* off, const int32_t* idx, int64_t M, int64_t N, int64_t** offsets,
+                    int32_t** indices, int64_t* nnz, int64_t* err_elem, int32_t* err_pos) {
+  int rc = oracle_poly_validate(off, idx, M, N, err_elem, err_pos);
+  if (rc != OK) return rc;
+  if (mode == 1) {
+    std::vector<std::vector<int32_t>> L((size_t)N);
+    for (int64_t e = 0; e < M; ++e)
+      for (int64_t p = off[e]; p < off[e + 1]; ++p) L[(size_t)idx[p]].push_back((int32_t)e);
+    flatten(L, N, offsets, indices, nnz);
+    return OK;
+  }
+  std::vector<std::set<int32_t>> S((size_t)N);
+  for (int64_t e = 0; e < M; ++e) {
+    const int64_t k = off[e + 1] - off[e];
+    const int32_t* row = idx + off[e];
+    for (int64_t i = 0; i < k; ++i) {
+      if (mode == 0) {
+        const int32_t a = row[i], b = row[(i + 1) % k];
+        S[(size_t)a].insert(b);
+        S[(size_t)b].insert(a);
+      } else {
+        for (int64_t j = 0; j < k; ++j)
+          if (i != j) S[(size_t)row[i]].insert(row[j]);
+      }
+    }
+  }
+  flatten(S, N, offsets, indices, nnz);
+  return OK;
+}
+
 void oracle_free(void* p) { std::free(p); }
 
 }  // extern "C"
