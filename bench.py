@@ -120,6 +120,12 @@ class ClockSampler:
 def workload(cfg, rank, world, device):
     """(etype, conn shard on device, global element base, total elements, num_nodes, desc)."""
     import meshgen
+    if cfg in meshgen.POLY_CONFIGS:   # polygon workload: etype None, conn = (off, idx)
+        if world > 1:
+            raise SystemExit("polygon configs are single-GPU")
+        off, idx, N = meshgen.make_poly_config(cfg, device=device)
+        info = dict(meshgen.POLY_CONFIGS[cfg], etype=None)
+        return None, (off, idx), 0, off.numel() - 1, N, info
     info = meshgen.CONFIGS[cfg]
     if cfg in (3, 5) and world > 1:
         n = 128 if cfg == 3 else 320
@@ -142,6 +148,26 @@ def oracle_sample(conn_full_dev, et, target_s, k_layers_hint=None, outputs="both
     import numpy as np
 
     import oracle
+    if et is None:   # polygon workload
+        off_d, idx_d = conn_full_dev
+        M = off_d.numel() - 1
+        ms = min(M, 200_000)
+        while True:
+            off = off_d[:ms + 1].cpu().numpy()
+            idx = idx_d[:int(off[-1])].cpu().numpy()
+            n_s = int(idx.max()) + 1 if idx.size else 0
+            t0 = time.perf_counter()
+            if outputs == "shared":
+                oracle.poly_shared_csr(off, idx, n_s)
+            else:
+                oracle.poly_node_csr(off, idx, n_s)
+                oracle.poly_elem_csr(off, idx, n_s)
+            dt = time.perf_counter() - t0
+            what = "element-sharing node CSR" if outputs == "shared" else "node + element CSR"
+            if dt >= 0.6 * target_s or ms >= M:
+                return ms / dt, (f"first {ms:,} of {M:,} polygons (node ids < {n_s:,}), {what}, "
+                                 f"1 thread, {dt:.1f} s"), dt, ms
+            ms = min(M, int(ms * max(1.5, min(8.0, target_s / max(dt, 1e-3)))))
     M = conn_full_dev.shape[0]
     ms = min(M, 200_000)
     while True:
@@ -172,6 +198,8 @@ def run_reference(args):
 
     import meshgen
     import oracle
+    if args.config in meshgen.POLY_CONFIGS:
+        return run_reference_poly(args)
     if args.config == 5:   # only the leading cell layers are ever sampled: build just those
         et, conn = meshgen.TET4, meshgen.kuhn_tets(320, cell_begin=0, cell_end=320 * 320 * 48)[0]
     else:
@@ -217,6 +245,57 @@ def run_reference(args):
     return 0
 
 
+def run_reference_poly(args):
+    """Reference arm on a polygon workload: the oracle's polygon functions on a prefix sample."""
+    import meshgen
+    import oracle
+    off_t, idx_t, _ = meshgen.make_poly_config(args.config, device="cpu")
+    off_all, idx_all = off_t.numpy(), idx_t.numpy()
+    M = off_all.shape[0] - 1
+    per_step = max(1.0, min(20.0, 150.0 / (args.steps + args.warmup)))
+
+    def sample(ms):
+        off = off_all[:ms + 1]
+        idx = idx_all[:int(off[-1])]
+        return off, idx, int(idx.max()) + 1
+
+    def one(off, idx, n_s):
+        oracle.poly_node_csr(off, idx, n_s)
+        oracle.poly_elem_csr(off, idx, n_s)
+
+    ms = min(M, 100_000)
+    while True:
+        t0 = time.perf_counter()
+        one(*sample(ms))
+        dt = time.perf_counter() - t0
+        if dt >= 0.6 * per_step or ms >= M:
+            break
+        ms = min(M, int(ms * max(1.5, min(8.0, per_step / max(dt, 1e-3)))))
+    off, idx, n_s = sample(ms)
+    for _ in range(args.warmup):
+        one(off, idx, n_s)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        one(off, idx, n_s)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    v = ms / t
+    sample_desc = (f"first {ms:,} polygons of config {args.config} ({meshgen.POLY_CONFIGS[args.config]['name']}), "
+                   f"node ids < {n_s:,}; std::set oracle, node + element CSR, 1 thread")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": meshgen.POLY_CONFIGS[args.config]["name"], "sample_elements": ms,
+                       "parallelism": "host, 1 thread"},
+            "cpu_baseline": {"value": v, "unit": "elements/s", "cores": 1, "kind": "oracle",
+                             "sample": sample_desc},
+            "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ------------------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------------------
@@ -249,10 +328,15 @@ def run_ours(args):
     mn.load()
 
     et, conn, base, M_total, N, info = workload(args.config, rank, world, dev)
-    M_local = conn.shape[0]
+    poly = et is None
     torch.cuda.synchronize()
 
-    if args.outputs == "shared":
+    if poly:
+        shared = args.outputs == "shared"
+
+        def step():
+            return mn.find_poly_neighbors(conn[0], conn[1], N, node=not shared, elem=not shared, shared=shared)
+    elif args.outputs == "shared":
         if world > 1:
             raise SystemExit("--outputs shared is single-GPU")
 
@@ -335,10 +419,22 @@ def run_ours(args):
     # ---- end to end through the public host-buffer API ----
     e2e = None
     if not args.no_e2e and args.outputs == "both":
-        host_conn = conn.cpu().pin_memory()
-        h2d = host_conn.numel() * 4
+        host_conn = (conn[0].cpu().pin_memory(), conn[1].cpu().pin_memory()) if poly else conn.cpu().pin_memory()
+        h2d = (host_conn[0].numel() * 8 + host_conn[1].numel() * 4) if poly else host_conn.numel() * 4
 
-        if world > 1:
+        if poly:
+            def estep():
+                o = host_conn[0].to(dev, non_blocking=True)
+                i = host_conn[1].to(dev, non_blocking=True)
+                (no, ni), (eo, ei), _ = mn.find_poly_neighbors(o, i, N, node=True, elem=True)
+                outs = []
+                for x in (no, ni, eo, ei):   # pinned (torch's caching host allocator), async D2H
+                    h = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+                    h.copy_(x, non_blocking=True)
+                    outs.append(h)
+                torch.cuda.current_stream().synchronize()
+                return outs
+        elif world > 1:
             from paper_1604_04689_b200.dist import find_neighbors_dist
 
             def estep():
@@ -381,8 +477,9 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32" if poly else "u64", "data": "synthetic",
             "config": {"workload": f"config {args.config}: {info['desc']}", "elements": M_total, "nodes": N,
+                       **({"conn_entries": int(conn[1].numel())} if poly else {}),
                        "parallelism": "single GPU" if world == 1 else
                        f"{world} GPUs: element shards + NCCL all-to-all by owner node range",
                        "l2": "inputs larger than L2 (no flush needed)",

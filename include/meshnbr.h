@@ -52,7 +52,12 @@ typedef enum {
   MN_ERR_DEGENERATE = 3,         /* conn[e][p] == conn[e][q] for some q < p; detail = (e, p)    */
   MN_ERR_CAPACITY = 4,           /* too many pairs for the 54-bit counters, or caller capacity */
   MN_ERR_OOM = 5,                /* the allocator returned NULL                                  */
-  MN_ERR_CUDA = 6                /* a CUDA runtime error (launch, copy, sync)                    */
+  MN_ERR_CUDA = 6,               /* a CUDA runtime error (launch, copy, sync)                    */
+  MN_ERR_ARITY = 7,              /* polygon meshes: an element with fewer than 3 nodes;
+                                    detail = (e, -1) (SPEC ArityMismatch, R18)         */
+  MN_ERR_SYNTAX = 8,             /* OFF/OBJ: malformed line; detail = (line, token position)    */
+  MN_ERR_COUNT_MISMATCH = 9,     /* OFF: fewer / more vertex or face lines than the counts line  */
+  MN_ERR_ZERO_INDEX = 10         /* OBJ: face index 0; detail = (line, token position)           */
 } mn_status;
 
 typedef void* mn_stream; /* cudaStream_t */
@@ -108,6 +113,23 @@ mn_status mn_find_node_neighbors_sortpairs(mn_elem_type type, const int32_t* d_c
 mn_status mn_find_node_neighbors_shared(mn_elem_type type, const int32_t* d_conn, int64_t num_elems,
                                         int64_t num_nodes, const mn_allocator* alloc, mn_stream stream,
                                         mn_csr* out, mn_error_detail* err);
+
+/* Polygon / mixed-arity surface meshes (PAPER.md title "generic meshes",
+ * §2.2; SPEC.md Mesh element_kind Polygon S:L32-36).  Connectivity in CSR form, device
+ * memory: element e is the ring d_idx[d_off[e]], ..., d_idx[d_off[e+1]-1] (arity >= 3), its edges
+ * are consecutive ring entries plus the closing edge.  d_off: num_elems + 1 int64 with d_off[0] = 0
+ * and d_off[num_elems] = conn_len (else MN_ERR_INVALID_ARG); d_idx: conn_len int32.
+ * Outputs (each nullable, at least one non-null), same conventions as mn_find_node_neighbors:
+ *   node_out   ring-edge node adjacency (one-ring neighbouring nodes)
+ *   elem_out   one-ring neighbouring elements (ascending)
+ *   shared_out element-sharing node adjacency (pattern of B^T B minus the diagonal)
+ * Validation per element in ascending order (R18): arity >= 3 (MN_ERR_ARITY, pos -1), then the
+ * range check, then the repeated-node check; the lowest offending element is reported.
+ * Blocks three times (offset bounds, validation + sizes, the node nnz values). */
+mn_status mn_find_poly_neighbors(const int64_t* d_off, const int32_t* d_idx, int64_t num_elems,
+                                 int64_t conn_len, int64_t num_nodes, const mn_allocator* alloc,
+                                 mn_stream stream, mn_csr* node_out, mn_csr* elem_out, mn_csr* shared_out,
+                                 mn_error_detail* err);
 
 /* One-ring neighbouring ELEMENTS of every vertex (§2.2.2: pairs (node, element
  * itself), sorted by node, segmented reduction and scan).  Slices list element ids ascending. */
@@ -268,6 +290,28 @@ int mn_profile_collect(void);
  * (sum over launches of the bytes the stage must move by definition, DESIGN.md §"Roofline"). */
 mn_status mn_profile_entry(int i, const char** name, int64_t* launches, double* total_ms,
                            double* alg_bytes);
+
+/* ------------------------------------------------------------------------------------------ *
+ * Mesh ingestion (host; SURVEY.md §8(f) row 3 "OFF/OBJ ingestion"; SPEC.md mesh-io load_off /
+ * load_obj; rules in csrc/meshio.cu and DESIGN.md R19).  The file image (bytes, len)
+ * is parsed into the polygon CSR form of mn_find_poly_neighbors, in host memory owned by the
+ * library (release with mn_host_mesh_free).  Vertex coordinates are checked to be numeric and
+ * dropped (topology only).  The result is validated (R18); every failure is a typed status with
+ * detail (line, token) for format errors and (face, position) for validation errors; the output
+ * is zeroed on failure.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct {
+  int64_t num_nodes;      /* vertex count                                                 */
+  int64_t num_elems;      /* face count M                                                 */
+  int64_t conn_len;       /* off[M]                                                       */
+  int64_t* off;           /* M + 1 ring offsets, off[0] = 0                               */
+  int32_t* idx;           /* conn_len 0-based vertex ids                                  */
+  int32_t uniform_arity;  /* k if every face has k nodes (3 -> TRI3, 4 -> QUAD4 conn), else 0 */
+} mn_host_mesh;
+
+mn_status mn_parse_off(const char* bytes, size_t len, mn_host_mesh* out, mn_error_detail* err);
+mn_status mn_parse_obj(const char* bytes, size_t len, mn_host_mesh* out, mn_error_detail* err);
+void mn_host_mesh_free(mn_host_mesh* mesh);
 
 #ifdef __cplusplus
 }

@@ -183,3 +183,30 @@ def elem_neighbors_sample(etype: int, conn, num_nodes: int, sample):
     for v in sample.tolist():
         out[v] = rows[(sub == v).any(1)].astype(np.int32)
     return out
+
+
+def poly_neighbors_sample(off, idx, num_nodes: int, sample):
+    """Polygon meshes (ring e = idx[off[e]:off[e+1]]), for each v in ``sample`` straight from the
+    definitions: the elements whose ring contains v (ascending), v's two ring neighbours in each
+    of them (ring-edge adjacency), and all other nodes of them (element-sharing adjacency).
+    -> {v: (node sorted array, elem array, shared sorted array)}"""
+    off = np.asarray(off.cpu() if hasattr(off, "cpu") else off, dtype=np.int64)
+    idx = np.asarray(idx.cpu() if hasattr(idx, "cpu") else idx, dtype=np.int64)
+    sample = np.asarray(sample, dtype=np.int64)
+    lut = np.zeros(num_nodes, dtype=bool)
+    lut[sample] = True
+    pos = np.nonzero(lut[idx])[0]                              # ring entries holding a sampled node
+    elem = np.searchsorted(off, pos, side="right") - 1         # their elements
+    out = {int(v): (set(), [], set()) for v in sample}
+    for p, e in zip(pos.tolist(), elem.tolist()):
+        b, k = int(off[e]), int(off[e + 1] - off[e])
+        ring = idx[b:b + k].tolist()
+        q = p - b
+        v = ring[q]
+        node, inc, shared = out[v]
+        node.add(ring[(q - 1) % k])
+        node.add(ring[(q + 1) % k])
+        inc.append(e)
+        shared.update(x for x in ring if x != v)
+    return {v: (np.array(sorted(a), dtype=np.int32), np.array(b, dtype=np.int32),
+                np.array(sorted(c), dtype=np.int32)) for v, (a, b, c) in out.items()}

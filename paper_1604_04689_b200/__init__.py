@@ -13,11 +13,13 @@ from __future__ import annotations
 import ctypes
 import os
 
+import numpy as np
 import torch
 
 __all__ = [
     "TRI3", "QUAD4", "TET4", "HEX8", "MeshError", "lib_path", "load",
-    "find_node_neighbors", "find_node_neighbors_sortpairs", "find_node_neighbors_shared", "find_elem_neighbors", "find_neighbors", "find_neighbors_host",
+    "find_node_neighbors", "find_node_neighbors_sortpairs", "find_node_neighbors_shared", "find_elem_neighbors",
+    "find_poly_neighbors", "find_neighbors", "find_neighbors_host", "load_off", "load_obj",
     "workspace_bytes", "node_key_bits", "node_key_bytes", "find_neighbors_chunked", "chunk_workspace_bytes",
     "emit_node_pairs", "emit_elem_pairs", "radix_sort_keys", "radix_sort_pairs_u32",
     "unique_node_csr", "elem_offsets", "exclusive_scan",
@@ -31,7 +33,8 @@ _NAMES = {"tri3": TRI3, "tri": TRI3, "quad4": QUAD4, "quad": QUAD4, "tet4": TET4
           "hex8": HEX8, "hex": HEX8}
 
 MN_OK, MN_ERR_INVALID_ARG, MN_ERR_INDEX_OUT_OF_RANGE, MN_ERR_DEGENERATE = 0, 1, 2, 3
-MN_ERR_CAPACITY, MN_ERR_OOM, MN_ERR_CUDA = 4, 5, 6
+MN_ERR_CAPACITY, MN_ERR_OOM, MN_ERR_CUDA, MN_ERR_ARITY = 4, 5, 6, 7
+MN_ERR_SYNTAX, MN_ERR_COUNT_MISMATCH, MN_ERR_ZERO_INDEX = 8, 9, 10
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 
@@ -64,6 +67,12 @@ class _Csr(ctypes.Structure):
                 ("offsets", ctypes.c_void_p), ("indices", ctypes.c_void_p), ("owner", _Allocator)]
 
 
+class _HostMesh(ctypes.Structure):
+    _fields_ = [("num_nodes", ctypes.c_int64), ("num_elems", ctypes.c_int64), ("conn_len", ctypes.c_int64),
+                ("off", ctypes.POINTER(ctypes.c_int64)), ("idx", ctypes.POINTER(ctypes.c_int32)),
+                ("uniform_arity", ctypes.c_int32)]
+
+
 class _ErrDetail(ctypes.Structure):
     _fields_ = [("elem", ctypes.c_int64), ("pos", ctypes.c_int32)]
 
@@ -82,6 +91,11 @@ def _declare(lib):
                                                  _P(_ErrDetail)]),
         "mn_find_node_neighbors_shared": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _VP, _P(_Csr),
                                               _P(_ErrDetail)]),
+        "mn_parse_off": (S, [ctypes.c_char_p, ctypes.c_size_t, _P(_HostMesh), _P(_ErrDetail)]),
+        "mn_parse_obj": (S, [ctypes.c_char_p, ctypes.c_size_t, _P(_HostMesh), _P(_ErrDetail)]),
+        "mn_host_mesh_free": (None, [_P(_HostMesh)]),
+        "mn_find_poly_neighbors": (S, [_VP, _VP, _I64, _I64, _I64, _P(_Allocator), _VP, _P(_Csr), _P(_Csr),
+                                       _P(_Csr), _P(_ErrDetail)]),
         "mn_find_neighbors_both": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _VP, _P(_Csr), _P(_Csr),
                                        _P(_ErrDetail)]),
         "mn_find_neighbors_both_host": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _P(_Allocator), _VP,
@@ -305,6 +319,62 @@ def find_neighbors(conn: torch.Tensor, etype, num_nodes: int, stream=None):
                                         ctypes.byref(err))
     _check(rc, err)
     return _take(al, no), _take(al, eo)
+
+
+def find_poly_neighbors(off: torch.Tensor, idx: torch.Tensor, num_nodes: int, node: bool = True,
+                        elem: bool = True, shared: bool = False, stream=None):
+    """Polygon / mixed-arity mesh (element e = ring idx[off[e]:off[e+1]], arity >= 3): any of the
+    ring-edge node CSR, the element CSR and the element-sharing node CSR, as (offsets, indices)
+    pairs in that order (None where not requested)."""
+    for t, dt, nm in ((off, torch.int64, "off"), (idx, torch.int32, "idx")):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise TypeError(f"{nm} must be a CUDA tensor (there is no CPU path)")
+        if t.dtype != dt:
+            raise TypeError(f"{nm} must be {dt}")
+    if off.numel() < 1:
+        raise ValueError("off needs num_elems + 1 entries")
+    off, idx = off.contiguous(), idx.contiguous()
+    lib = load()
+    al = _TorchAllocator(off.device)
+    outs = [_Csr() if w else None for w in (node, elem, shared)]
+    err = _ErrDetail()
+    ref = [ctypes.byref(o) if o is not None else None for o in outs]
+    with torch.cuda.device(off.device):
+        rc = lib.mn_find_poly_neighbors(off.data_ptr(), idx.data_ptr() if idx.numel() else None, off.numel() - 1,
+                                        idx.numel(), int(num_nodes), ctypes.byref(al.struct), _stream_ptr(stream),
+                                        *ref, ctypes.byref(err))
+    _check(rc, err)
+    return tuple(_take(al, o) if o is not None else None for o in outs)
+
+
+def _parse(fn, data):
+    if isinstance(data, (str, os.PathLike)):
+        with open(data, "rb") as f:
+            data = f.read()
+    if isinstance(data, str):
+        data = data.encode()
+    m, err = _HostMesh(), _ErrDetail()
+    rc = fn(data, len(data), ctypes.byref(m), ctypes.byref(err))
+    _check(rc, err)
+    try:
+        M, L = int(m.num_elems), int(m.conn_len)
+        off = torch.from_numpy(np.ctypeslib.as_array(m.off, shape=(M + 1,)).copy())
+        idx = torch.from_numpy(np.ctypeslib.as_array(m.idx, shape=(L,)).copy() if L else np.zeros(0, np.int32))
+        return off, idx, int(m.num_nodes), int(m.uniform_arity)
+    finally:
+        load().mn_host_mesh_free(ctypes.byref(m))
+
+
+def load_off(data):
+    """Parse an OFF file (path or bytes/str) with the native parser: (off int64[M+1], idx int32,
+    num_nodes, uniform_arity) on the host; uniform_arity is k when every face has k nodes, else 0."""
+    return _parse(load().mn_parse_off, data)
+
+
+def load_obj(data):
+    """Parse an OBJ file (path or bytes/str); same result as load_off (1-based, negative and
+    "/t/n" face tokens resolved)."""
+    return _parse(load().mn_parse_obj, data)
 
 
 def find_neighbors_chunked(conn: torch.Tensor, etype, num_nodes: int, max_workspace_bytes: int, stream=None):

@@ -857,6 +857,43 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
   cnt[a] = L;
 }
 
+// Block-wide: ascending bitonic sort of buf[0, raw) (implicit +inf padding to a power of two;
+// pairs past raw are skipped), then thread 0 writes the distinct values to out (out may alias buf).
+// Returns the distinct count (valid in every thread after the trailing barrier).
+__device__ __forceinline__ int block_sort_dedupe(uint32_t* buf, int64_t raw, uint32_t* out) {
+  __shared__ int s_u;
+  int64_t n2 = 1;
+  while (n2 < raw) n2 <<= 1;
+  for (int64_t k = 2; k <= n2; k <<= 1) {
+    for (int64_t j = k >> 1; j > 0; j >>= 1) {
+      for (int64_t t = threadIdx.x; t < n2 / 2; t += blockDim.x) {
+        int64_t lo, hi;
+        const int64_t blk = t / j, o = t % j;
+        if (j == (k >> 1)) {   // flip step: compare i with its mirror inside the k-block
+          lo = blk * k + o;
+          hi = blk * k + k - 1 - o;
+        } else {
+          lo = blk * 2 * j + o;
+          hi = lo + j;
+        }
+        if (hi < raw) {
+          const uint32_t x = buf[lo], y = buf[hi];
+          if (x > y) { buf[lo] = y; buf[hi] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    int u = 0;
+    for (int64_t i = 0; i < raw; ++i)
+      if (i == 0 || buf[i] != buf[i - 1]) out[u++] = buf[i];
+    s_u = u;
+  }
+  __syncthreads();
+  return s_u;
+}
+
 // Nodes with more than 256 raw neighbour entries (or more than 32 distinct neighbours): one CTA per
 // node, the raw entries sorted with a block bitonic network (shared memory when they fit, else in
 // place in the node's global raw region), then adjacent-difference dedupe.
@@ -869,7 +906,6 @@ k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx,
   constexpr int K = Elem<T>::K;
   constexpr int C = SHARED ? K - 1 : Elem<T>::C;
   extern __shared__ uint32_t sv[];
-  __shared__ int s_u;
   if (err && *err != ERR_NONE) return;
   const unsigned ng = *ngiant;
   for (unsigned g = blockIdx.x; g < ng; g += gridDim.x) {
@@ -895,37 +931,8 @@ k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx,
       }
     }
     __syncthreads();
-    int64_t n2 = 1;
-    while (n2 < raw) n2 <<= 1;
-    // ascending bitonic sort of raw entries, implicit +inf padding to n2 (pairs past raw skipped)
-    for (int64_t k = 2; k <= n2; k <<= 1) {
-      for (int64_t j = k >> 1; j > 0; j >>= 1) {
-        for (int64_t t = threadIdx.x; t < n2 / 2; t += blockDim.x) {
-          int64_t lo, hi;
-          if (j == (k >> 1)) {   // flip step: compare i with its mirror inside the k-block
-            const int64_t blk = t / j, off = t % j;
-            lo = blk * k + off;
-            hi = blk * k + k - 1 - off;
-          } else {
-            const int64_t blk = t / j, off = t % j;
-            lo = blk * 2 * j + off;
-            hi = lo + j;
-          }
-          if (hi < raw) {
-            const uint32_t x = buf[lo], y = buf[hi];
-            if (x > y) { buf[lo] = y; buf[hi] = x; }
-          }
-        }
-        __syncthreads();
-      }
-    }
-    if (threadIdx.x == 0) {
-      int u = 0;
-      for (int64_t i = 0; i < raw; ++i)
-        if (i == 0 || buf[i] != buf[i - 1]) out[u++] = buf[i];
-      cnt[a] = u;
-      s_u = u;
-    }
+    const int u = block_sort_dedupe(buf, raw, out);
+    if (threadIdx.x == 0) cnt[a] = u;
     __syncthreads();
   }
 }
@@ -936,13 +943,13 @@ k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx,
 __global__ void __launch_bounds__(kNodeThreads)
 k_node_compact(const int64_t* __restrict__ eoff, int C, const uint32_t* __restrict__ temp,
                const int32_t* __restrict__ lofs, const int64_t* __restrict__ noff, int64_t N,
-               int32_t* __restrict__ out) {
+               int32_t* __restrict__ out, const int64_t* __restrict__ rawoff = nullptr) {
   __shared__ int64_t s_src[kNodeThreads];
   __shared__ int64_t s_dst[kNodeThreads + 1];
   const int64_t n0 = (int64_t)blockIdx.x * kNodeThreads;
   const int t = threadIdx.x;
   const int nloc = (int)(N - n0 < kNodeThreads ? N - n0 : kNodeThreads);
-  const int64_t base = (int64_t)C * eoff[n0];
+  const int64_t base = rawoff ? rawoff[n0] : (int64_t)C * eoff[n0];   // (rawoff: polygon meshes)
   if (t < nloc) {
     s_src[t] = base + lofs[n0 + t];
     s_dst[t] = noff[n0 + t];

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "poly.cuh"
 
 namespace mn {
 
@@ -976,6 +977,227 @@ static mn_status find(int t, const int32_t* conn, int64_t M, int64_t N, const mn
 }
 
 // ================================================================================================
+// Polygon / mixed-arity surface meshes (kernels in poly.cuh).  Transpose
+// path with variable-length rings; outputs any of: ring-edge node CSR, element CSR, element-sharing
+// node CSR.  Three blocking reads: the offset bounds, validation + offsets (also sizes the raw
+// regions), and the node nnz values.
+// ================================================================================================
+static mn_status decode_poly_err(uint64_t w, mn_error_detail* err) {
+  if (w == ERR_NONE) return MN_OK;
+  const int kind = (int)((w >> 22) & 3);
+  if (err) {
+    err->elem = (int64_t)(w >> 24);
+    err->pos = kind >= 2 ? -1 : (int32_t)(w & 0x3FFFFF);
+  }
+  switch (kind) {
+    case 0: return MN_ERR_INDEX_OUT_OF_RANGE;
+    case 1: return MN_ERR_DEGENERATE;
+    case 2: return MN_ERR_ARITY;
+    default: return MN_ERR_INVALID_ARG;
+  }
+}
+
+static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, int64_t L, int64_t N, Mem& mem,
+                           mn_csr* node_out, mn_csr* elem_out, mn_csr* shared_out, mn_error_detail* err) {
+  cudaStream_t s = mem.s;
+  mn_status st = MN_OK;
+  uint64_t* host = pinned_pair();
+  if (!host) return MN_ERR_CUDA;
+  const bool wn = node_out != nullptr, we = elem_out != nullptr, wsh = shared_out != nullptr;
+  const int64_t scan_tiles = tiles_of(N, kScanTile);
+  const unsigned ng = (unsigned)tiles_of(N, kNodeThreads);
+  constexpr int cap = 48 * 1024;   // giant raw entries staged in shared memory
+  int64_t *elem_off = nullptr, *node_off = nullptr, *sh_off = nullptr;
+  int32_t *elem_idx = nullptr, *nidx = nullptr, *sidx = nullptr;
+  uint32_t *tempR = nullptr, *tempS = nullptr;
+  void* ws = nullptr;
+  int64_t rawtotal = 0, Un = 0, Us = 0;
+  // workspace pieces
+  unsigned long long* errw = nullptr;
+  uint32_t *tickets = nullptr, *giants = nullptr, *sgiants = nullptr;
+  unsigned int *ngiant = nullptr, *nsgiant = nullptr;
+  uint64_t* sstatus = nullptr;
+  int32_t *cinc = nullptr, *cursor = nullptr, *rawcnt = nullptr, *cntR = nullptr, *lofsR = nullptr,
+          *cntS = nullptr, *lofsS = nullptr;
+  int64_t *eoff = nullptr, *rawoff = nullptr;
+  int32_t* eidx = nullptr;
+  size_t head = 0;
+  auto fill = [&](mn_csr* o, int64_t* offs, int32_t* ind, int64_t nnz) {
+    o->num_nodes = N; o->nnz = nnz; o->offsets = offs; o->indices = ind; o->owner = mem.a;
+  };
+  // the offsets must span exactly [0, conn_len] (an argument error, reported before any element's)
+  if (cudaMemcpyAsync(host, off, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(host + 1, off + M, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return MN_ERR_CUDA;
+  if ((int64_t)host[0] != 0 || (int64_t)host[1] != L) return MN_ERR_INVALID_ARG;
+  if (wn) { node_off = (int64_t*)mem.get((size_t)(N + 1) * 8); if (!node_off) { st = MN_ERR_OOM; goto done; } }
+  if (wsh) { sh_off = (int64_t*)mem.get((size_t)(N + 1) * 8); if (!sh_off) { st = MN_ERR_OOM; goto done; } }
+  if (we) {
+    elem_off = (int64_t*)mem.get((size_t)(N + 1) * 8);
+    elem_idx = L ? (int32_t*)mem.get((size_t)L * 4) : nullptr;
+    if (!elem_off || (L && !elem_idx)) { st = MN_ERR_OOM; goto done; }
+  }
+  {
+    auto layout = [&](Arena& a) {
+      errw = a.take<unsigned long long>(2);
+      tickets = a.take<uint32_t>(32);
+      ngiant = a.take<unsigned int>(1);
+      nsgiant = a.take<unsigned int>(1);
+      sstatus = a.take<uint64_t>((size_t)scan_tiles + 1);
+      cinc = a.take<int32_t>((size_t)N + 1);
+      cursor = a.take<int32_t>((size_t)N + 1);
+      if (wsh) rawcnt = a.take<int32_t>((size_t)N + 1);
+      head = a.off;
+      sgiants = a.take<uint32_t>((size_t)N + 1);
+      giants = a.take<uint32_t>((size_t)N + 1);
+      eoff = we ? elem_off : a.take<int64_t>((size_t)N + 1);
+      eidx = we ? elem_idx : a.take<int32_t>((size_t)L);
+      if (wsh) rawoff = a.take<int64_t>((size_t)N + 1);
+      if (wn) { cntR = a.take<int32_t>((size_t)N + 1); lofsR = a.take<int32_t>((size_t)N + 1); }
+      if (wsh) { cntS = a.take<int32_t>((size_t)N + 1); lofsS = a.take<int32_t>((size_t)N + 1); }
+    };
+    Arena ar;
+    layout(ar);
+    ws = mem.get(ar.off);
+    if (!ws) { st = MN_ERR_OOM; goto done; }
+    ar = Arena{};
+    ar.base = (char*)ws;
+    layout(ar);
+  }
+  MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
+  MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
+  if (M == 0) {
+    MN_CUDA(cudaMemsetAsync(eoff, 0, (size_t)(N + 1) * 8, s));
+  } else {
+    MN_CUDA(launch("poly_count", 16.0 * M + 4.0 * L, s, [&] {
+      k_poly_count<<<hist_grid(M), 256, 0, s>>>(off, idx, M, L, N, cinc, wsh ? rawcnt : nullptr, errw);
+    }));
+    if (N > 0) {
+      MN_CUDA(launch("scan_counts", 12.0 * N, s, [&] {
+        k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(cinc, N, eoff, sstatus,
+                                                                                 tickets + 29, 1);
+      }));
+      if (wsh)
+        MN_CUDA(launch("scan_counts", 12.0 * N, s, [&] {
+          k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(rawcnt, N, rawoff, sstatus,
+                                                                                   tickets + 28, 3);
+        }));
+    }
+  }
+  // ---- blocking read 1: validation word (+ the element-sharing raw total) ----
+  MN_CUDA(cudaMemcpyAsync(host, errw, 8, cudaMemcpyDeviceToHost, s));
+  if (wsh && M > 0 && N > 0) MN_CUDA(cudaMemcpyAsync(host + 1, rawoff + N, 8, cudaMemcpyDeviceToHost, s));
+  MN_CUDA(cudaStreamSynchronize(s));
+  st = decode_poly_err(host[0], err);
+  if (st != MN_OK) goto done;
+  rawtotal = (wsh && M > 0 && N > 0) ? (int64_t)host[1] : 0;
+  if (M > 0) {
+    MN_CUDA(launch("poly_scatter", 16.0 * M + 16.0 * L, s, [&] {
+      k_poly_scatter<<<hist_grid(M), 256, 0, s>>>(off, idx, M, eoff, cursor, eidx, errw);
+    }));
+    if (we) {
+      MN_CUDA(launch("elem_segsort", 8.0 * L + 8.0 * (N + 1), s, [&] {
+        k_elem_segsort<<<(unsigned)tiles_of(N, kSegThreads), kSegThreads, 0, s>>>(eoff, N, eidx, sgiants, nsgiant,
+                                                                                 errw);
+      }));
+      static bool seg_attr = false;
+      if (!seg_attr) {
+        cudaFuncSetAttribute(k_segsort_giant, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
+        seg_attr = true;
+      }
+      MN_CUDA(launch("segsort_giant", 0.0, s, [&] {
+        k_segsort_giant<<<148, 1024, cap * 4, s>>>(eoff, eidx, sgiants, nsgiant, cap, errw);
+      }));
+    }
+    static bool poly_attr = false;
+    if (!poly_attr) {
+      cudaFuncSetAttribute(k_poly_giant<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
+      cudaFuncSetAttribute(k_poly_giant<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
+      poly_attr = true;
+    }
+    if (wn) {   // ring-edge node adjacency: 2 raw candidates per incidence
+      tempR = L ? (uint32_t*)mem.get((size_t)2 * L * 4) : nullptr;
+      if (L && !tempR) { st = MN_ERR_OOM; goto done; }
+      MN_CUDA(launch("poly_gather", 8.0 * (N + 1) + 4.0 * L + 24.0 * L, s, [&] {
+        k_poly_gather<false><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, off, idx, N, nullptr, 2, tempR, cntR, lofsR,
+                                                        giants, ngiant, errw);
+      }));
+      MN_CUDA(launch("poly_giant", 0.0, s, [&] {
+        k_poly_giant<false><<<148, 1024, cap * 4, s>>>(eoff, eidx, off, idx, nullptr, 2, tempR, cntR, lofsR, giants,
+                                                       ngiant, cap, errw);
+      }));
+      MN_CUDA(launch("scan_counts", 12.0 * N, s, [&] {
+        k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(cntR, N, node_off, sstatus,
+                                                                                 tickets + 31, 2);
+      }));
+      MN_CUDA(cudaMemcpyAsync(host + 2, node_off + N, 8, cudaMemcpyDeviceToHost, s));
+    }
+    if (wsh) {   // element-sharing adjacency: k_e - 1 raw candidates per incidence
+      tempS = rawtotal ? (uint32_t*)mem.get((size_t)rawtotal * 4) : nullptr;
+      if (rawtotal && !tempS) { st = MN_ERR_OOM; goto done; }
+      MN_CUDA(cudaMemsetAsync(ngiant, 0, 4, s));
+      MN_CUDA(launch("poly_gather", 16.0 * (N + 1) + 4.0 * L + 4.0 * rawtotal, s, [&] {
+        k_poly_gather<true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, off, idx, N, rawoff, 0, tempS, cntS, lofsS,
+                                                       giants, ngiant, errw);
+      }));
+      MN_CUDA(launch("poly_giant", 0.0, s, [&] {
+        k_poly_giant<true><<<148, 1024, cap * 4, s>>>(eoff, eidx, off, idx, rawoff, 0, tempS, cntS, lofsS, giants,
+                                                      ngiant, cap, errw);
+      }));
+      MN_CUDA(launch("scan_counts", 12.0 * N, s, [&] {
+        k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(cntS, N, sh_off, sstatus,
+                                                                                 tickets + 30, 4);
+      }));
+      MN_CUDA(cudaMemcpyAsync(host + 3, sh_off + N, 8, cudaMemcpyDeviceToHost, s));
+    }
+  } else {
+    if (wn) MN_CUDA(cudaMemsetAsync(node_off, 0, (size_t)(N + 1) * 8, s));
+    if (wsh) MN_CUDA(cudaMemsetAsync(sh_off, 0, (size_t)(N + 1) * 8, s));
+    host[2] = host[3] = 0;
+  }
+  // ---- blocking read 2: node nnz values ----
+  MN_CUDA(cudaStreamSynchronize(s));
+  Un = (wn && M > 0) ? (int64_t)host[2] : 0;
+  Us = (wsh && M > 0) ? (int64_t)host[3] : 0;
+  if (Un) {
+    nidx = (int32_t*)mem.get((size_t)Un * 4);
+    if (!nidx) { st = MN_ERR_OOM; goto done; }
+    MN_CUDA(launch("node_compact", 8.0 * Un + 24.0 * N, s, [&] {
+      k_node_compact<<<ng, kNodeThreads, 0, s>>>(eoff, 2, tempR, lofsR, node_off, N, nidx);
+    }));
+  }
+  if (Us) {
+    sidx = (int32_t*)mem.get((size_t)Us * 4);
+    if (!sidx) { st = MN_ERR_OOM; goto done; }
+    MN_CUDA(launch("node_compact", 8.0 * Us + 32.0 * N, s, [&] {
+      k_node_compact<<<ng, kNodeThreads, 0, s>>>(eoff, 0, tempS, lofsS, sh_off, N, sidx, rawoff);
+    }));
+  }
+  if (wn) fill(node_out, node_off, nidx, Un);
+  if (we) fill(elem_out, elem_off, elem_idx, L);
+  if (wsh) fill(shared_out, sh_off, sidx, Us);
+  mem.put(tempR);
+  mem.put(tempS);
+  mem.put(ws);
+  return MN_OK;
+done:
+  cudaStreamSynchronize(s);
+  mem.put(tempR);
+  mem.put(tempS);
+  mem.put(ws);
+  mem.put(node_off);
+  mem.put(sh_off);
+  mem.put(elem_off);
+  mem.put(elem_idx);
+  mem.put(nidx);
+  mem.put(sidx);
+  for (mn_csr* o : {node_out, elem_out, shared_out})
+    if (o) std::memset(o, 0, sizeof(*o));
+  return st;
+}
+
+// ================================================================================================
 // generic LSD sorts (stage entry points and the multi-GPU finish)
 // ================================================================================================
 template <typename KeyT, bool PAYLOAD>
@@ -1410,6 +1632,10 @@ const char* mn_status_string(mn_status s) {
     case MN_ERR_CAPACITY: return "capacity exceeded";
     case MN_ERR_OOM: return "out of device memory";
     case MN_ERR_CUDA: return "CUDA error";
+    case MN_ERR_ARITY: return "element with fewer than 3 nodes";
+    case MN_ERR_SYNTAX: return "mesh file syntax error";
+    case MN_ERR_COUNT_MISMATCH: return "mesh file count mismatch";
+    case MN_ERR_ZERO_INDEX: return "OBJ face index 0";
   }
   return "unknown status";
 }
@@ -1430,6 +1656,18 @@ mn_status mn_find_node_neighbors_sortpairs(mn_elem_type t, const int32_t* d_conn
 mn_status mn_find_node_neighbors_shared(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N,
                                         const mn_allocator* a, mn_stream s, mn_csr* out, mn_error_detail* err) {
   return find(t, d_conn, M, N, a, s, true, false, out, nullptr, err, false, nullptr, true);
+}
+
+mn_status mn_find_poly_neighbors(const int64_t* d_off, const int32_t* d_idx, int64_t num_elems, int64_t conn_len,
+                                 int64_t num_nodes, const mn_allocator* a, mn_stream s, mn_csr* node_out,
+                                 mn_csr* elem_out, mn_csr* shared_out, mn_error_detail* err) {
+  if (err) { err->elem = -1; err->pos = -1; }
+  if (num_elems < 0 || conn_len < 0 || num_nodes < 0 || num_nodes > INT32_MAX) return MN_ERR_INVALID_ARG;
+  if (num_elems > INT32_MAX || conn_len > INT32_MAX) return MN_ERR_CAPACITY;
+  if (!d_off || (conn_len > 0 && !d_idx)) return MN_ERR_INVALID_ARG;
+  if (!node_out && !elem_out && !shared_out) return MN_ERR_INVALID_ARG;
+  Mem mem(a, (cudaStream_t)s);
+  return poly_find(d_off, d_idx, num_elems, conn_len, num_nodes, mem, node_out, elem_out, shared_out, err);
 }
 
 mn_status mn_find_elem_neighbors(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N,

@@ -132,3 +132,18 @@ def test_validation_rules():
     # empty mesh, isolated nodes
     o, i = oracle.poly_node_csr(np.zeros(1, np.int64), np.zeros(0, np.int32), 4)
     assert o.tolist() == [0, 0, 0, 0, 0] and len(i) == 0
+
+
+@pytest.mark.parametrize("make", [lambda: meshgen.random_poly(200, 60, 3, 12, 2), lambda: meshgen.poly_mixed_grid(9, 7, 5),
+                                  lambda: meshgen.honeycomb(5, 4)])
+def test_sampled_form_matches_full(make):
+    from oracle import stages
+    off, idx, N = make()
+    smp = stages.poly_neighbors_sample(off, idx, N, list(range(0, N, 3)))
+    o, i = oracle.poly_node_csr(off, idx, N)
+    eo, ei = oracle.poly_elem_csr(off, idx, N)
+    so, si = oracle.poly_shared_csr(off, idx, N)
+    for v, (a, b, c) in smp.items():
+        assert a.tolist() == i[o[v]:o[v + 1]].tolist()
+        assert b.tolist() == ei[eo[v]:eo[v + 1]].tolist()
+        assert c.tolist() == si[so[v]:so[v + 1]].tolist()
