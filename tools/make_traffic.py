@@ -12,7 +12,9 @@ from collections import OrderedDict
 NAMES = [("k_node_gather_t", "node_gather"), ("k_elem_scatter", "elem_scatter"), ("k_elem_segsort", "elem_segsort"),
          ("k_elem_count", "elem_count"), ("k_node_compact", "node_compact"), ("k_scan_i32", "scan_counts"),
          ("k_hist_validate", "hist_validate"), ("k_node_giant", "node_giant"), ("k_segsort_giant", "segsort_giant"),
-         ("k_locality_sample", "locality_sample"), ("k_bucket_bases", "bucket_bases")]
+         ("k_locality_sample", "locality_sample"), ("k_bucket_bases", "bucket_bases"),
+         ("k_poly_count", "poly_count"), ("k_poly_scatter", "poly_scatter"), ("k_poly_gather", "poly_gather"),
+         ("k_poly_giant", "poly_giant")]
 
 
 def main():
