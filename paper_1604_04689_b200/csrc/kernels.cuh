@@ -739,8 +739,11 @@ __device__ __forceinline__ void sort_small(uint32_t (*tab)[kNodeThreads], int t,
 // cost more occupancy than the saved pass.)
 // SHARED: element-sharing ("FEM sparsity") adjacency — every other node of an incident element
 // is a neighbour, so each incidence yields CE = K - 1 candidates.
-template <int T, bool ALIGNED, bool DIST = false, bool SHARED = false>
-__global__ void __launch_bounds__(kNodeThreads)
+// >= 10 CTAs per SM (<= 48 registers) for arity <= 4: 4.48 vs 4.75 ms on config 5; hex keeps its
+// registers for the 8-int rows (48 registers: 3.25 vs 2.63 ms on config 4).  profiles/round1/sweep_gather_minb.txt
+template <int T, bool ALIGNED, bool DIST = false, bool SHARED = false,
+          int MINB = (Elem<T>::K <= 4) ? 10 : 1>
+__global__ void __launch_bounds__(kNodeThreads, MINB)
 k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, RowSrc rs,
                 int64_t N, uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, int32_t* __restrict__ lofs,
                 uint32_t* __restrict__ giants, unsigned int* __restrict__ ngiant,
@@ -1083,11 +1086,12 @@ constexpr int kSegSmem = 8192;   // elements of a 128-node chunk staged in share
 // A CTA per kSegThreads consecutive nodes: their segments form one contiguous range, staged
 // through shared memory with coalesced loads/stores; each thread sorts its own segment with a
 // register sorting network sized by the largest segment of its warp (warp-uniform choice).
-__global__ void __launch_bounds__(kSegThreads)
+template <int SMEM = kSegSmem, int MINB = 1>
+__global__ void __launch_bounds__(kSegThreads, MINB)
 k_elem_segsort(const int64_t* __restrict__ eoff, int64_t N, int32_t* __restrict__ eidx,
                uint32_t* __restrict__ giants, unsigned int* __restrict__ ngiant,
                const unsigned long long* __restrict__ err) {
-  __shared__ int32_t buf[kSegSmem];
+  __shared__ int32_t buf[SMEM];
   if (err && *err != ERR_NONE) return;
   const int t = threadIdx.x;
   const int64_t n0 = (int64_t)blockIdx.x * kSegThreads;
@@ -1099,7 +1103,7 @@ k_elem_segsort(const int64_t* __restrict__ eoff, int64_t N, int32_t* __restrict_
   const int d = valid ? (int)(eoff[a + 1] - s) : 0;
   const bool big = d > kSegMax;
   if (valid && big) giants[atomicAdd(ngiant, 1u)] = (uint32_t)a;
-  const bool staged = c1 - c0 <= kSegSmem;   // CTA-uniform
+  const bool staged = c1 - c0 <= SMEM;   // CTA-uniform
   if (staged) {
     for (int64_t i = c0 + t; i < c1; i += kSegThreads) buf[i - c0] = eidx[i];
     __syncthreads();

@@ -126,8 +126,15 @@ constexpr int kTile = kPassThreads * kPassItems;   // keys per onesweep tile
 constexpr int kThreads = 256;
 constexpr int kItems = 16;
 constexpr int kUTile = kThreads * kItems;
+// single-pass scans: 1024 x 16 tiles (measured 0.39 vs 0.50 ms for config 5's two 33 M-entry scans
+// with 256 x 16: fewer look-back steps)
+constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 16;
-constexpr int kScanTile = kThreads * kScanItems;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+// segment sort: 4096 staged entries (16 KB) and >= 8 CTAs per SM (64 registers): 2.17 ms on config 5
+// vs 2.34 ms for 8192 entries / 78 registers (profiles/round1/sweep_segsort.txt)
+static auto* const segsort_fn = &k_elem_segsort<4096, 8>;
 
 struct Plan {
   int T, K, E, C;
@@ -169,6 +176,13 @@ static int64_t tiles_of(int64_t n, int tile) { return (n + tile - 1) / tile; }
 static int hist_grid(int64_t M) {
   int64_t g = (M + 255) / 256;
   if (g > 148 * 8) g = 148 * 8;
+  return g < 1 ? 1 : (int)g;
+}
+// the transpose count: a 2-wave grid (1.49 vs 1.55 ms on config 5); the scatter keeps hist_grid's
+// single resident wave, which keeps its write window inside L2 (4 or 32 CTAs/SM: +40%)
+static int count_grid(int64_t M) {
+  int64_t g = (M + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
   return g < 1 ? 1 : (int)g;
 }
 static int stream_grid(int64_t n) {
@@ -558,12 +572,12 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     if (transpose) {
       // ---- a2 + a3e + a4 + a5 (elements) as a counting-sort transpose ----
       MN_CUDA(launch("elem_count", 4.0 * P.K * P.M, s, [&] {
-        if (aligned) k_elem_count<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw);
-        else k_elem_count<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw);
+        if (aligned) k_elem_count<T, true><<<count_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw);
+        else k_elem_count<T, false><<<count_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw);
       }));
       if (P.N > 0)
         MN_CUDA(launch("scan_counts", 4.0 * P.N + 8.0 * (P.N + 1), s, [&] {
-          k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(ecnt, P.N, eoff, sstatus,
+          k_scan_i32<kScanThreads, kScanItems><<<(unsigned)scan_tiles, kScanThreads, 0, s>>>(ecnt, P.N, eoff, sstatus,
                                                                                    tickets + 29, 1);
         }));
       MN_CUDA(launch("elem_scatter", 4.0 * P.K * P.M + 12.0 * P.Pe, s, [&] {
@@ -579,7 +593,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       if (want_elem) {
         if (P.N > 0)
           MN_CUDA(launch("elem_segsort", 8.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
-            k_elem_segsort<<<(unsigned)tiles_of(P.N, kSegThreads), kSegThreads, 0, s>>>(eoff, P.N, eidx, sgiants,
+            segsort_fn<<<(unsigned)tiles_of(P.N, kSegThreads), kSegThreads, 0, s>>>(eoff, P.N, eidx, sgiants,
                                                                                      nsgiant, errw);
           }));
         MN_CUDA(launch("segsort_giant", 0.0, s, [&] {
@@ -637,7 +651,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     // ---- a5 (elements): exclusive scan of the per-node counts -> offsets ----
     if (P.N > 0)
       MN_CUDA(launch("scan_counts", 4.0 * P.N + 8.0 * (P.N + 1), s, [&] {
-        k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(ecnt, P.N, eoff, sstatus,
+        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)scan_tiles, kScanThreads, 0, s>>>(ecnt, P.N, eoff, sstatus,
                                                                                  tickets + 29, 1);
       }));
     }   // LSD element path
@@ -696,7 +710,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       // ---- a5 (nodes): exclusive scan of the unique counts -> offsets ----
       if (P.N > 0)   // N == 0 with M > 0 always fails validation; nothing to scan
       MN_CUDA(launch("scan_counts", 4.0 * P.N + 8.0 * (P.N + 1), s, [&] {
-        k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(cnt, P.N, node_off, sstatus,
+        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)scan_tiles, kScanThreads, 0, s>>>(cnt, P.N, node_off, sstatus,
                                                                                  tickets + 31, 2);
       }));
       MN_CUDA(cudaMemcpyAsync(host + 1, node_off + P.N, 8, cudaMemcpyDeviceToHost, s));
@@ -813,7 +827,7 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
         else k_elem_count<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw, lo, hi);
       }));
       MN_CUDA(launch("scan_counts", 12.0 * nloc, s, [&] {
-        k_scan_i32<kThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kThreads, 0, s>>>(
+        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kScanThreads, 0, s>>>(
             ecnt, nloc, eoff, sstatus, tickets, 1);
       }));
       MN_CUDA(cudaMemcpyAsync(host, errw, 8, cudaMemcpyDeviceToHost, s));
@@ -832,7 +846,7 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
           else k_elem_scatter<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, eoff, cursor, eslice, errw, lo, hi);
         }));
         MN_CUDA(launch("elem_segsort", 8.0 * Ie + 8.0 * (nloc + 1), s, [&] {
-          k_elem_segsort<<<(unsigned)tiles_of(nloc, kSegThreads), kSegThreads, 0, s>>>(eoff, nloc, eslice, sgiants,
+          segsort_fn<<<(unsigned)tiles_of(nloc, kSegThreads), kSegThreads, 0, s>>>(eoff, nloc, eslice, sgiants,
                                                                                     nsgiant, errw);
         }));
         const int scap = 48 * 1024;
@@ -863,7 +877,7 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
                                                              errw, lo);
         }));
         MN_CUDA(launch("scan_counts", 12.0 * nloc, s, [&] {
-          k_scan_i32<kThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kThreads, 0, s>>>(
+          k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kScanThreads, 0, s>>>(
               cnt, nloc, noff, sstatus, tickets + 1, 2);
         }));
       } else {
@@ -1075,12 +1089,12 @@ static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, in
     }));
     if (N > 0) {
       MN_CUDA(launch("scan_counts", 12.0 * N, s, [&] {
-        k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(cinc, N, eoff, sstatus,
+        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)scan_tiles, kScanThreads, 0, s>>>(cinc, N, eoff, sstatus,
                                                                                  tickets + 29, 1);
       }));
       if (wsh)
         MN_CUDA(launch("scan_counts", 12.0 * N, s, [&] {
-          k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(rawcnt, N, rawoff, sstatus,
+          k_scan_i32<kScanThreads, kScanItems><<<(unsigned)scan_tiles, kScanThreads, 0, s>>>(rawcnt, N, rawoff, sstatus,
                                                                                    tickets + 28, 3);
         }));
     }
@@ -1098,7 +1112,7 @@ static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, in
     }));
     if (we) {
       MN_CUDA(launch("elem_segsort", 8.0 * L + 8.0 * (N + 1), s, [&] {
-        k_elem_segsort<<<(unsigned)tiles_of(N, kSegThreads), kSegThreads, 0, s>>>(eoff, N, eidx, sgiants, nsgiant,
+        segsort_fn<<<(unsigned)tiles_of(N, kSegThreads), kSegThreads, 0, s>>>(eoff, N, eidx, sgiants, nsgiant,
                                                                                  errw);
       }));
       static bool seg_attr = false;
@@ -1128,7 +1142,7 @@ static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, in
                                                        ngiant, cap, errw);
       }));
       MN_CUDA(launch("scan_counts", 12.0 * N, s, [&] {
-        k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(cntR, N, node_off, sstatus,
+        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)scan_tiles, kScanThreads, 0, s>>>(cntR, N, node_off, sstatus,
                                                                                  tickets + 31, 2);
       }));
       MN_CUDA(cudaMemcpyAsync(host + 2, node_off + N, 8, cudaMemcpyDeviceToHost, s));
@@ -1146,7 +1160,7 @@ static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, in
                                                       ngiant, cap, errw);
       }));
       MN_CUDA(launch("scan_counts", 12.0 * N, s, [&] {
-        k_scan_i32<kThreads, kScanItems><<<(unsigned)scan_tiles, kThreads, 0, s>>>(cntS, N, sh_off, sstatus,
+        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)scan_tiles, kScanThreads, 0, s>>>(cntS, N, sh_off, sstatus,
                                                                                  tickets + 30, 4);
       }));
       MN_CUDA(cudaMemcpyAsync(host + 3, sh_off + N, 8, cudaMemcpyDeviceToHost, s));
@@ -1410,7 +1424,7 @@ static mn_status dist_bucket_impl(const int32_t* conn, int64_t M, int64_t base, 
         k_mark_remote_rows<<<stream_grid(P.Pe), 256, 0, s>>>(pairs, P.Pe, chunk, world, self, flags, errw);
       }));
       MN_CUDA(launch("scan_counts", 12.0 * P.Pe, s, [&] {
-        k_scan_i32<kThreads, kScanItems><<<(unsigned)tiles_of(P.Pe, kScanTile), kThreads, 0, s>>>(
+        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(P.Pe, kScanTile), kScanThreads, 0, s>>>(
             flags, P.Pe, pos, sstatus, tickets + 1, 1);
       }));
       MN_CUDA(launch("row_counts", 0.0, s, [&] { k_row_counts<<<1, 512, 0, s>>>(pos, bases, world, P.Pe, rcnt); }));
@@ -1509,14 +1523,14 @@ static mn_status dist_finish_impl(const uint64_t* pairs, int64_t n, const int32_
         if (nloc > 0) {
           MN_CUDA(launch("elem_count", 8.0 * n, s, [&] { k_pairs_count<<<stream_grid(n), 256, 0, s>>>(pairs, n, lo, cnt); }));
           MN_CUDA(launch("scan_counts", 12.0 * nloc, s, [&] {
-            k_scan_i32<kThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kThreads, 0, s>>>(
+            k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kScanThreads, 0, s>>>(
                 cnt, nloc, eoff, sstatus, tickets + 2, 1);
           }));
           MN_CUDA(launch("elem_scatter", 16.0 * n, s, [&] {
             k_pairs_scatter<<<stream_grid(n), 256, 0, s>>>(pairs, n, lo, eoff, lofs, eidx);
           }));
           MN_CUDA(launch("elem_segsort", 8.0 * n + 8.0 * (nloc + 1), s, [&] {
-            k_elem_segsort<<<(unsigned)tiles_of(nloc, kSegThreads), kSegThreads, 0, s>>>(eoff, nloc, eidx, giants,
+            segsort_fn<<<(unsigned)tiles_of(nloc, kSegThreads), kSegThreads, 0, s>>>(eoff, nloc, eidx, giants,
                                                                                       ngiant, errw);
           }));
           const int scap = 48 * 1024;
@@ -1569,7 +1583,7 @@ static mn_status dist_finish_impl(const uint64_t* pairs, int64_t n, const int32_
                                                                    cap, errw, lo);
         }));
         MN_CUDA(launch("scan_counts", 12.0 * nloc, s, [&] {   // epoch 2: the element scan may have used 1
-          k_scan_i32<kThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kThreads, 0, s>>>(
+          k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kScanThreads, 0, s>>>(
               cnt, nloc, noff, sstatus, tickets + 1, 2);
         }));
       } else {
@@ -1895,7 +1909,7 @@ mn_status mn_exclusive_scan_i32(const int32_t* d_counts, int64_t n, int64_t* d_o
   if (cudaMemsetAsync(ws, 0, bytes, s) != cudaSuccess) st = MN_ERR_CUDA;
   if (st == MN_OK &&
       launch("scan_i32", 4.0 * n + 8.0 * (n + 1), s, [&] {
-        k_scan_i32<kThreads, kScanItems><<<(unsigned)tiles, kThreads, 0, s>>>(d_counts, n, d_out, status, ticket, 1);
+        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles, kScanThreads, 0, s>>>(d_counts, n, d_out, status, ticket, 1);
       }) != cudaSuccess)
     st = MN_ERR_CUDA;
   mem.put(ws);
