@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--outputs", default="both", choices=["both", "shared"],
                     help="both = node + element CSR (the headline); shared = element-sharing node "
                          "adjacency (SURVEY §8(f) row 3), N=1 only")
+    ap.add_argument("--elem-path", default="auto", choices=["auto", "radix", "transpose"],
+                    help="element-CSR algorithm (auto = locality test; see DESIGN.md §3.5)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
     return ap.parse_args()
 
@@ -326,6 +328,7 @@ def run_ours(args):
             dist.init_process_group(backend)
         dist.barrier()
     mn.load()
+    mn.set_elem_path(args.elem_path)
 
     et, conn, base, M_total, N, info = workload(args.config, rank, world, dev)
     poly = et is None

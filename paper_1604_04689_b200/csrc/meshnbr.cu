@@ -529,6 +529,9 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     unsigned int* nsgiant = nullptr;
     int64_t* eoff = elem_off;
     int32_t* eidx = elem_idx;
+    const int64_t nchunks = tiles_of(P.N, kChunkNodes);
+    int32_t *ccnt = nullptr, *ccur = nullptr;
+    int64_t* cbase = nullptr;
     auto layout = [&](Arena& a) {
       errw = a.take<unsigned long long>(2);
       tickets = a.take<uint32_t>(32);
@@ -540,8 +543,13 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       ecnt = a.take<int32_t>((size_t)P.N + 1);   // per-node incidence counts (atomics in the last pass)
       nsgiant = a.take<unsigned int>(1);
       if (transpose) cursor = a.take<int32_t>((size_t)P.N + 1);
+      if (transpose) {
+        ccnt = a.take<int32_t>((size_t)nchunks + 1);
+        ccur = a.take<int32_t>((size_t)nchunks + 1);
+      }
       head = a.off;
       if (transpose) sgiants = a.take<uint32_t>((size_t)P.N + 1);
+      if (transpose) cbase = a.take<int64_t>((size_t)nchunks + 1);
       // ekA | ekB | epA | epB (each 256-byte aligned, contiguous); later the node raw region
       ekA = a.take<uint32_t>((size_t)P.Pe * (CE > 4 ? CE - 3 : 1));   // the 4 pieces hold >= CE * Pe
       ekB = a.take<uint32_t>((size_t)P.Pe);
@@ -569,37 +577,44 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
     MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
 
+    const int scap = 48 * 1024;
+    static bool seg_attr = false;
+    if (!seg_attr) {
+      cudaFuncSetAttribute(k_segsort_giant, cudaFuncAttributeMaxDynamicSharedMemorySize, scap * 4);
+      seg_attr = true;
+    }
     if (transpose) {
-      // ---- a2 + a3e + a4 + a5 (elements) as a counting-sort transpose ----
+      // ---- a2 + a3e + a4 + a5 (elements): transpose bucketed by 128-node chunk ----
+      int32_t* belem = reinterpret_cast<int32_t*>(ekA);
+      uint8_t* bnode = reinterpret_cast<uint8_t*>(ekB);
       MN_CUDA(launch("elem_count", 4.0 * P.K * P.M, s, [&] {
-        if (aligned) k_elem_count<T, true><<<count_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw);
-        else k_elem_count<T, false><<<count_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw);
+        if (aligned) k_chunk_count<T, true><<<count_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ccnt, errw);
+        else k_chunk_count<T, false><<<count_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ccnt, errw);
       }));
-      if (P.N > 0)
-        MN_CUDA(launch("scan_counts", 4.0 * P.N + 8.0 * (P.N + 1), s, [&] {
-          k_scan_i32<kScanThreads, kScanItems><<<(unsigned)scan_tiles, kScanThreads, 0, s>>>(ecnt, P.N, eoff, sstatus,
-                                                                                   tickets + 29, 1);
+      if (nchunks > 0)
+        MN_CUDA(launch("scan_counts", 12.0 * nchunks, s, [&] {
+          k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nchunks, kScanTile), kScanThreads, 0, s>>>(
+              ccnt, nchunks, cbase, sstatus, tickets + 29, 1);
         }));
-      MN_CUDA(launch("elem_scatter", 4.0 * P.K * P.M + 12.0 * P.Pe, s, [&] {
-        if (aligned) k_elem_scatter<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, eoff, cursor, eidx, errw);
-        else k_elem_scatter<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, eoff, cursor, eidx, errw);
+      MN_CUDA(launch("elem_scatter", 4.0 * P.K * P.M + 5.0 * P.Pe, s, [&] {
+        if (aligned)
+          k_chunk_scatter<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, cbase, ccur, belem, bnode, errw);
+        else
+          k_chunk_scatter<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, cbase, ccur, belem, bnode, errw);
       }));
-      const int scap = 48 * 1024;
-      static bool seg_attr = false;
-      if (!seg_attr) {
-        cudaFuncSetAttribute(k_segsort_giant, cudaFuncAttributeMaxDynamicSharedMemorySize, scap * 4);
-        seg_attr = true;
-      }
-      if (want_elem) {
-        if (P.N > 0)
-          MN_CUDA(launch("elem_segsort", 8.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
-            segsort_fn<<<(unsigned)tiles_of(P.N, kSegThreads), kSegThreads, 0, s>>>(eoff, P.N, eidx, sgiants,
-                                                                                     nsgiant, errw);
-          }));
+      if (nchunks > 0)
+        MN_CUDA(launch("elem_segsort", 9.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
+          if (want_elem)
+            k_chunk_sort<true><<<(unsigned)nchunks, kChunkNodes, 0, s>>>(cbase, P.N, belem, bnode, eoff, eidx,
+                                                                          sgiants, nsgiant, errw);
+          else
+            k_chunk_sort<false><<<(unsigned)nchunks, kChunkNodes, 0, s>>>(cbase, P.N, belem, bnode, eoff, eidx,
+                                                                           sgiants, nsgiant, errw);
+        }));
+      if (want_elem)
         MN_CUDA(launch("segsort_giant", 0.0, s, [&] {
           k_segsort_giant<<<148, 1024, scap * 4, s>>>(eoff, eidx, sgiants, nsgiant, scap, errw);
         }));
-      }
     } else {
     // ---- a1/a2 validation + digit histograms of the node ids ----
     MN_CUDA(launch("hist_validate", 4.0 * P.K * P.M, s, [&] {
