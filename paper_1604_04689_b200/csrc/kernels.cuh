@@ -861,7 +861,8 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
 }
 
 // Block-wide: ascending bitonic sort of buf[0, raw) (implicit +inf padding to a power of two;
-// pairs past raw are skipped), then thread 0 writes the distinct values to out (out may alias buf).
+// pairs past raw are skipped), then the distinct values are written to out (in parallel: per-thread
+// ranges + a block scan; serially by thread 0 when out aliases buf).  blockDim: a multiple of 32.
 // Returns the distinct count (valid in every thread after the trailing barrier).
 __device__ __forceinline__ int block_sort_dedupe(uint32_t* buf, int64_t raw, uint32_t* out) {
   __shared__ int s_u;
@@ -887,12 +888,46 @@ __device__ __forceinline__ int block_sort_dedupe(uint32_t* buf, int64_t raw, uin
       __syncthreads();
     }
   }
-  if (threadIdx.x == 0) {
-    int u = 0;
-    for (int64_t i = 0; i < raw; ++i)
-      if (i == 0 || buf[i] != buf[i - 1]) out[u++] = buf[i];
-    s_u = u;
+  if (buf == out) {   // in place (global memory, > smem capacity): serial, reads ahead of writes
+    if (threadIdx.x == 0) {
+      int u = 0;
+      for (int64_t i = 0; i < raw; ++i)
+        if (i == 0 || buf[i] != buf[i - 1]) out[u++] = buf[i];
+      s_u = u;
+    }
+    __syncthreads();
+    return s_u;
   }
+  // parallel: each thread a contiguous range, block exclusive scan of the distinct counts
+  __shared__ int s_ws[32];
+  const int nt = blockDim.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t per = (raw + nt - 1) / nt;
+  const int64_t lo = (int64_t)t * per, hi = lo + per < raw ? lo + per : raw;
+  int c = 0;
+  for (int64_t i = lo; i < hi; ++i) c += (i == 0 || buf[i] != buf[i - 1]) ? 1 : 0;
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_ws[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = nt >> 5;
+    int x = lane < nw ? s_ws[lane] : 0, xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, xi, o);
+      if (lane >= o) xi += y;
+    }
+    if (lane < nw) s_ws[lane] = xi - x;
+    if (lane == nw - 1) s_u = xi;
+  }
+  __syncthreads();
+  int pos = s_ws[warp] + incl - c;
+  for (int64_t i = lo; i < hi; ++i)
+    if (i == 0 || buf[i] != buf[i - 1]) out[pos++] = buf[i];
   __syncthreads();
   return s_u;
 }
