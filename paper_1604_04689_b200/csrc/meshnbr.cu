@@ -252,7 +252,7 @@ static mn_status pipeline(const Plan& P, const int32_t* conn, Mem& mem, bool wan
   }
   if (want_elem) {
     elem_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
-    elem_idx = P.Pe ? (int32_t*)mem.get((size_t)P.Pe * 4) : nullptr;
+    elem_idx = P.Pe ? (int32_t*)mem.get((size_t)P.Pe * 4 + 16) : nullptr;
     if (!elem_off || (P.Pe && !elem_idx)) { st = MN_ERR_OOM; goto done; }
   }
 
@@ -487,7 +487,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
   }
   if (want_elem) {
     elem_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
-    elem_idx = P.Pe ? (int32_t*)mem.get((size_t)P.Pe * 4) : nullptr;
+    elem_idx = P.Pe ? (int32_t*)mem.get((size_t)P.Pe * 4 + 16) : nullptr;
     if (!elem_off || (P.Pe && !elem_idx)) { st = MN_ERR_OOM; goto done; }
   }
   if (P.M == 0) {
@@ -561,7 +561,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
         giants = a.take<uint32_t>((size_t)(giant_cap ? giant_cap : 1));
         if (!want_elem) {
           eoff = a.take<int64_t>((size_t)P.N + 1);
-          eidx = a.take<int32_t>((size_t)P.Pe);
+          eidx = a.take<int32_t>((size_t)P.Pe + 4);
         }
       }
     };
@@ -799,7 +799,7 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
   if (chunks) *chunks = K;
   int64_t* node_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
   int64_t* elem_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
-  int32_t* elem_idx = P.Pe ? (int32_t*)mem.get((size_t)P.Pe * 4) : nullptr;
+  int32_t* elem_idx = P.Pe ? (int32_t*)mem.get((size_t)P.Pe * 4 + 16) : nullptr;
   int32_t* node_idx = nullptr;
   std::vector<std::pair<int32_t*, int64_t>> parts;
   void* ws = nullptr;
@@ -1495,7 +1495,7 @@ static mn_status dist_finish_impl(const uint64_t* pairs, int64_t n, const int32_
   std::memset(elem_slice, 0, sizeof(*elem_slice));
   int64_t* noff = (int64_t*)mem.get((size_t)(nloc + 1) * 8);
   int64_t* eoff = (int64_t*)mem.get((size_t)(nloc + 1) * 8);
-  int32_t* eidx = n ? (int32_t*)mem.get((size_t)n * 4) : nullptr;
+  int32_t* eidx = n ? (int32_t*)mem.get((size_t)n * 4 + 16) : nullptr;   // +16: aligned 16-byte reads
   void* ws = nullptr;
   if (!noff || !eoff || (n && !eidx)) { st = MN_ERR_OOM; goto done; }
   if (n == 0) {
