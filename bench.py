@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--outputs", default="both", choices=["both", "shared"],
                     help="both = node + element CSR (the headline); shared = element-sharing node "
                          "adjacency (SURVEY §8(f) row 3), N=1 only")
+    ap.add_argument("--max-workspace-gb", type=float, default=None,
+                    help="memory-bounded mode (SURVEY §8(f) row 4): node ranges whose workspace fits this budget")
     ap.add_argument("--elem-path", default="auto", choices=["auto", "radix", "transpose"],
                     help="element-CSR algorithm (auto = locality test; see DESIGN.md §3.5)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
@@ -350,6 +352,14 @@ def run_ours(args):
 
         def step():
             return find_neighbors_dist(conn, et, base, N)
+    elif args.max_workspace_gb:
+        budget = int(args.max_workspace_gb * 2**30)
+        chunks_used = []
+
+        def step():
+            no, eo, k = mn.find_neighbors_chunked(conn, et, N, budget)
+            chunks_used.append(k)
+            return no, eo
     else:
         def step():
             return mn.find_neighbors(conn, et, N)
@@ -421,7 +431,7 @@ def run_ours(args):
 
     # ---- end to end through the public host-buffer API ----
     e2e = None
-    if not args.no_e2e and args.outputs == "both":
+    if not args.no_e2e and args.outputs == "both" and not args.max_workspace_gb:
         host_conn = (conn[0].cpu().pin_memory(), conn[1].cpu().pin_memory()) if poly else conn.cpu().pin_memory()
         h2d = (host_conn[0].numel() * 8 + host_conn[1].numel() * 4) if poly else host_conn.numel() * 4
 
@@ -487,7 +497,9 @@ def run_ours(args):
                        f"{world} GPUs: element shards + NCCL all-to-all by owner node range",
                        "l2": "inputs larger than L2 (no flush needed)",
                        "outputs": "node + element CSR" if args.outputs == "both" else
-                       "element-sharing node CSR"},
+                       "element-sharing node CSR",
+                       **({"max_workspace_gb": args.max_workspace_gb, "node_ranges": chunks_used[-1]}
+                          if args.max_workspace_gb and not poly and world == 1 else {})},
             "roofline": roofline, "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),

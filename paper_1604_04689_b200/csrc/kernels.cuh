@@ -1052,7 +1052,7 @@ k_locality_sample(const int32_t* __restrict__ conn, int64_t M, unsigned long lon
   unsigned groups = 0;
 #pragma unroll
   for (int p = 0; p < K; ++p) {
-    const int x = in ? row[p] : -1 - lane;
+    const int x = in ? row[p] : -1;   // one shared sentinel: match cost grows with distinct values
     const unsigned peers = __match_any_sync(FULL, x);
     groups += (in && lane == __ffs(peers) - 1) ? 1u : 0u;
   }
@@ -1118,7 +1118,7 @@ k_elem_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __res
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       const bool mine = in && v[p] >= lo && v[p] < hi;
-      const int x = mine ? (int)(v[p] - lo) : -1 - lane;
+      const int x = mine ? (int)(v[p] - lo) : -1;   // one shared sentinel: match cost grows with distinct values
       const unsigned peers = __match_any_sync(FULL, x);
       const int leader = __ffs(peers) - 1;
       int b = 0;
@@ -1187,10 +1187,11 @@ k_elem_segsort(const int64_t* __restrict__ eoff, int64_t N, int32_t* __restrict_
 constexpr int kChunkNodes = 128;
 constexpr int kChunkCap = 4096;   // bucket entries staged in shared memory (Kuhn tets: 3072)
 
-template <int T, bool ALIGNED>
+// RANGE: only nodes of [lo, hi) (the memory-bounded mode); compiled out of the whole-path kernels
+template <int T, bool ALIGNED, bool RANGE = false>
 __global__ void __launch_bounds__(256)
 k_chunk_count(const int32_t* __restrict__ conn, int64_t M, int64_t N, int32_t* __restrict__ ccnt,
-              unsigned long long* __restrict__ err) {
+              unsigned long long* __restrict__ err, int64_t lo = 0, int64_t hi = INT64_MAX) {
   constexpr int K = Elem<T>::K;
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1217,19 +1218,20 @@ k_chunk_count(const int32_t* __restrict__ conn, int64_t M, int64_t N, int32_t* _
     }
     const bool ok = in && bad < 0;
 #pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const int x = ok ? (v[p] >> 7) : -1 - lane;
-      const unsigned peers = __match_any_sync(FULL, x);
-      if (ok && lane == __ffs(peers) - 1) atomicAdd(ccnt + x, (int)__popc(peers));
+    for (int p = 0; p < K; ++p) {   // only nodes of [lo, hi) (the memory-bounded mode's range)
+      const bool mine = ok && (!RANGE || (v[p] >= lo && v[p] < hi));
+      const int x = mine ? (RANGE ? (int)((v[p] - lo) >> 7) : (v[p] >> 7)) : -1;   // one shared sentinel
+      const unsigned peers = __match_any_sync(FULL, x);   // (match cost grows with distinct values)
+      if (mine && lane == __ffs(peers) - 1) atomicAdd(ccnt + x, (int)__popc(peers));
     }
   }
 }
 
-template <int T, bool ALIGNED>
+template <int T, bool ALIGNED, bool RANGE = false>
 __global__ void __launch_bounds__(256)
 k_chunk_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __restrict__ cbase,
                 int32_t* __restrict__ ccur, int32_t* __restrict__ belem, uint8_t* __restrict__ bnode,
-                const unsigned long long* __restrict__ err) {
+                const unsigned long long* __restrict__ err, int64_t lo = 0, int64_t hi = INT64_MAX) {
   constexpr int K = Elem<T>::K;
   if (*err != ERR_NONE) return;
   const int lane = threadIdx.x & 31;
@@ -1241,16 +1243,17 @@ k_chunk_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __re
     if (in) load_row<T, ALIGNED>(conn, e, v);
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      const int x = in ? (v[p] >> 7) : -1 - lane;
+      const bool mine = in && (!RANGE || (v[p] >= lo && v[p] < hi));
+      const int x = mine ? (RANGE ? (int)((v[p] - lo) >> 7) : (v[p] >> 7)) : -1;   // one shared sentinel
       const unsigned peers = __match_any_sync(FULL, x);
       const int leader = __ffs(peers) - 1;
       int b = 0;
-      if (in && lane == leader) b = atomicAdd(ccur + x, (int)__popc(peers));
+      if (mine && lane == leader) b = atomicAdd(ccur + x, (int)__popc(peers));
       b = __shfl_sync(FULL, b, leader);
-      if (in) {
+      if (mine) {
         const int64_t pos = cbase[x] + b + __popc(peers & lanemask_lt());
         belem[pos] = (int32_t)e;
-        bnode[pos] = (uint8_t)(v[p] & (kChunkNodes - 1));
+        bnode[pos] = (uint8_t)((RANGE ? (int)(v[p] - lo) : v[p]) & (kChunkNodes - 1));
       }
     }
   }
@@ -1604,7 +1607,7 @@ k_pairs_locality(const uint64_t* __restrict__ pairs, int64_t n, unsigned long lo
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t j = (int64_t)((double)n * (double)gw / (double)nw) + lane;
   const bool in = j < n;
-  const int64_t x = in ? (int64_t)(pairs[j] >> 32) : -1 - lane;
+  const int64_t x = in ? (int64_t)(pairs[j] >> 32) : -1;   // one shared sentinel: match cost grows with distinct values
   const unsigned peers = __match_any_sync(FULL, (unsigned long long)x);
   const unsigned g = __reduce_add_sync(FULL, (in && lane == __ffs(peers) - 1) ? 1u : 0u);
   const unsigned act = __popc(__ballot_sync(FULL, in));
@@ -1629,7 +1632,7 @@ k_pairs_scatter(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, const
     const int64_t j = base + lane;
     const bool in = j < n;
     const uint64_t p = in ? pairs[j] : 0;
-    const int64_t a = in ? (int64_t)(p >> 32) - lo : -1 - lane;
+    const int64_t a = in ? (int64_t)(p >> 32) - lo : -1;   // one shared sentinel: match cost grows with distinct values
     const unsigned peers = __match_any_sync(FULL, (unsigned long long)a);
     const int leader = __ffs(peers) - 1;
     int b = 0;

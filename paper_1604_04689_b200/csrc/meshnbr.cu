@@ -817,9 +817,11 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
     unsigned int* ngiant = ar.take<unsigned int>(1);
     unsigned int* nsgiant = ar.take<unsigned int>(1);
     uint64_t* sstatus = ar.take<uint64_t>((size_t)tiles_of(nloc, kScanTile) + 1);
-    int32_t* ecnt = ar.take<int32_t>((size_t)nloc + 1);
-    int32_t* cursor = ar.take<int32_t>((size_t)nloc + 1);
+    const int64_t nch = tiles_of(nloc, kChunkNodes);
+    int32_t* ecnt = ar.take<int32_t>((size_t)nch + 1);     // per-chunk counts / cursors
+    int32_t* cursor = ar.take<int32_t>((size_t)nch + 1);
     const size_t head = ar.off;
+    int64_t* cbase = ar.take<int64_t>((size_t)nch + 1);
     int64_t* eoff = ar.take<int64_t>((size_t)nloc + 1);
     int64_t* noff = ar.take<int64_t>((size_t)nloc + 1);
     int32_t* cnt = ar.take<int32_t>((size_t)nloc + 1);
@@ -833,20 +835,21 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
       auto fix = [&](auto* q) { return (decltype(q))(bb + (size_t)q); };
       errw = fix(errw); tickets = fix(tickets); ngiant = fix(ngiant); nsgiant = fix(nsgiant); sstatus = fix(sstatus);
       ecnt = fix(ecnt); cursor = fix(cursor); eoff = fix(eoff); noff = fix(noff); cnt = fix(cnt); lofs = fix(lofs);
+      cbase = fix(cbase);
       giants = fix(giants); sgiants = fix(sgiants);
       MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
       MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
-      // (1) validation + incidence counts of the range, offsets
+      // (1) validation + per-chunk incidence counts of the range, chunk bases
       MN_CUDA(launch("elem_count", 4.0 * P.K * P.M, s, [&] {
-        if (aligned) k_elem_count<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw, lo, hi);
-        else k_elem_count<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw, lo, hi);
+        if (aligned) k_chunk_count<T, true, true><<<count_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw, lo, hi);
+        else k_chunk_count<T, false, true><<<count_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ecnt, errw, lo, hi);
       }));
-      MN_CUDA(launch("scan_counts", 12.0 * nloc, s, [&] {
-        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kScanThreads, 0, s>>>(
-            ecnt, nloc, eoff, sstatus, tickets, 1);
+      MN_CUDA(launch("scan_counts", 12.0 * nch, s, [&] {
+        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nch, kScanTile), kScanThreads, 0, s>>>(
+            ecnt, nch, cbase, sstatus, tickets, 1);
       }));
       MN_CUDA(cudaMemcpyAsync(host, errw, 8, cudaMemcpyDeviceToHost, s));
-      MN_CUDA(cudaMemcpyAsync(host + 1, eoff + nloc, 8, cudaMemcpyDeviceToHost, s));
+      MN_CUDA(cudaMemcpyAsync(host + 1, cbase + nch, 8, cudaMemcpyDeviceToHost, s));
       MN_CUDA(cudaStreamSynchronize(s));
       st = decode_err(host[0], err);
       if (st != MN_OK) goto done;
@@ -856,13 +859,20 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
       temp = Ie ? (uint32_t*)mem.get((size_t)C * Ie * 4) : nullptr;
       if (Ie && !temp) { st = MN_ERR_OOM; goto done; }
       if (Ie) {
-        MN_CUDA(launch("elem_scatter", 4.0 * P.K * P.M + 12.0 * Ie, s, [&] {
-          if (aligned) k_elem_scatter<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, eoff, cursor, eslice, errw, lo, hi);
-          else k_elem_scatter<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, eoff, cursor, eslice, errw, lo, hi);
+        // buckets (element id + local node byte, 5 B per incidence) in the range's node raw region
+        int32_t* belem = reinterpret_cast<int32_t*>(temp);
+        uint8_t* bnode = reinterpret_cast<uint8_t*>(temp + Ie);
+        MN_CUDA(launch("elem_scatter", 4.0 * P.K * P.M + 5.0 * Ie, s, [&] {
+          if (aligned)
+            k_chunk_scatter<T, true, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, cbase, cursor, belem, bnode, errw,
+                                                                          lo, hi);
+          else
+            k_chunk_scatter<T, false, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, cbase, cursor, belem, bnode, errw,
+                                                                           lo, hi);
         }));
-        MN_CUDA(launch("elem_segsort", 8.0 * Ie + 8.0 * (nloc + 1), s, [&] {
-          segsort_fn<<<(unsigned)tiles_of(nloc, kSegThreads), kSegThreads, 0, s>>>(eoff, nloc, eslice, sgiants,
-                                                                                    nsgiant, errw);
+        MN_CUDA(launch("elem_segsort", 9.0 * Ie + 8.0 * (nloc + 1), s, [&] {
+          k_chunk_sort<true><<<(unsigned)nch, kChunkNodes, 0, s>>>(cbase, nloc, belem, bnode, eoff, eslice, sgiants,
+                                                                   nsgiant, errw);
         }));
         const int scap = 48 * 1024;
         cudaFuncSetAttribute(k_segsort_giant, cudaFuncAttributeMaxDynamicSharedMemorySize, scap * 4);
@@ -895,8 +905,9 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
           k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kScanThreads, 0, s>>>(
               cnt, nloc, noff, sstatus, tickets + 1, 2);
         }));
-      } else {
+      } else {   // no incidence in the range: both slices empty
         MN_CUDA(cudaMemsetAsync(noff, 0, (size_t)(nloc + 1) * 8, s));
+        MN_CUDA(cudaMemsetAsync(eoff, 0, (size_t)(nloc + 1) * 8, s));
       }
       MN_CUDA(launch("shift_offsets", 16.0 * (nloc + 1), s, [&] {
         k_shift_offsets<<<stream_grid(nloc + 1), 256, 0, s>>>(eoff, nloc + 1, ebase, elem_off + lo);

@@ -88,7 +88,7 @@ k_poly_scatter(const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
     const int kmax = (int)__reduce_max_sync(FULL, (unsigned)k);
     for (int p = 0; p < kmax; ++p) {
       const bool mine = p < k;
-      const int x = mine ? idx[b + p] : -1 - lane;
+      const int x = mine ? idx[b + p] : -1;   // one shared sentinel: match cost grows with distinct values
       const unsigned peers = __match_any_sync(FULL, x);
       const int leader = __ffs(peers) - 1;
       int c = 0;
