@@ -1180,7 +1180,7 @@ k_elem_segsort(const int64_t* __restrict__ eoff, int64_t N, int32_t* __restrict_
 //   k_scan_i32       chunk bases
 //   k_chunk_scatter  appends (element id, local node) to the chunk's bucket: runs of consecutive
 //                    slots, so only a bucket's tail sector is ever partially written
-//   k_chunk_sort     one CTA per chunk: bucket -> shared memory, counting sort by local node, each
+//   k_chunk_sort     one CTA per chunk: bucket -> fixed per-node slots in shared memory, each
 //                    node's list sorted in registers (warp-uniform network), element CSR range and
 //                    the chunk's offsets written coalesced; lists > kSegMax go to k_segsort_giant
 // ------------------------------------------------------------------------------------------------
@@ -1259,55 +1259,64 @@ k_chunk_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __re
   }
 }
 
-// One CTA (kChunkNodes threads) per chunk.  SORT = false (node-only calls) groups by node without
-// ordering each list.  The bucket is read twice from global memory (counts, then placement; the
-// second read hits L2) with 4 loads in flight per thread and placed into a skewed shared-memory
-// array (16.5 KB per CTA); buckets above kChunkCap are placed and sorted in global memory instead
-// (same result).  (Measured slower: warp-aggregating the shared atomics with __match_any_sync, 2.4x;
-// 8-entry vector groups with run-length atomics, +17%; staging the bucket in shared memory, +10%.)
-__device__ __forceinline__ int chunk_skew(int x) { return x + (x >> 5); }
+// One CTA (kChunkNodes threads) per chunk, one pass over the bucket (SORT = false, node-only
+// calls, groups by node without ordering each list).  Each local node owns kSegMax fixed slots (column t of a skewed
+// 32 x 129 array: per-thread column reads and per-warp row copies are both conflict-free); the slot
+// cursor is the count.  A node with more than kSegMax entries flags the chunk, which then takes the
+// two-pass global path (counts already known).  Sorted lists go back to their columns and each warp
+// copies its 32 nodes' lists out, one coalesced store per node.  (2.77 ms on config 5; measured
+// slower: a count pass + skewed staging array, 3.11 ms; staging the bucket in shared memory, 3.43;
+// warp-aggregating the shared atomics with __match_any_sync, 7.39; 8-entry vector groups, 3.65.)
+constexpr int kSlotPitch = kChunkNodes + 1;
 
 template <int NET>
-__device__ __forceinline__ void sort_chunk_segment(int32_t* buf, int s0, int d) {
+__device__ __forceinline__ void sort_slot_column(int32_t* slots, int t, int d) {
   int32_t v[NET];
 #pragma unroll
-  for (int i = 0; i < NET; ++i) v[i] = i < d ? buf[chunk_skew(s0 + i)] : INT32_MAX;
+  for (int i = 0; i < NET; ++i) v[i] = i < d ? slots[i * kSlotPitch + t] : INT32_MAX;
   oddeven_sort<NET>(v);
 #pragma unroll
   for (int i = 0; i < NET; ++i)
-    if (i < d) buf[chunk_skew(s0 + i)] = v[i];
+    if (i < d) slots[i * kSlotPitch + t] = v[i];
 }
 
 template <bool SORT, int MINB = 8>
 __global__ void __launch_bounds__(kChunkNodes, MINB)
 k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __restrict__ belem,
-             const uint8_t* __restrict__ bnode, int64_t* __restrict__ eoff, int32_t* __restrict__ eidx,
-             uint32_t* __restrict__ giants, unsigned int* __restrict__ ngiant,
-             const unsigned long long* __restrict__ err) {
-  __shared__ int32_t s_out[kChunkCap + kChunkCap / 32];
+              const uint8_t* __restrict__ bnode, int64_t* __restrict__ eoff, int32_t* __restrict__ eidx,
+              uint32_t* __restrict__ giants, unsigned int* __restrict__ ngiant,
+              const unsigned long long* __restrict__ err) {
+  __shared__ int32_t slots[kSegMax * kSlotPitch];
   __shared__ int s_cnt[kChunkNodes];
+  __shared__ int s_ex[kChunkNodes];
   __shared__ int s_wsum[kChunkNodes / 32];
+  __shared__ int s_over;
   if (err && *err != ERR_NONE) return;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t c = blockIdx.x;
   const int64_t n0 = c * kChunkNodes;
   const int64_t b0 = cbase[c], b1 = cbase[c + 1];
   const int n = (int)(b1 - b0);
-  const bool staged = n <= kChunkCap;   // CTA-uniform
   s_cnt[t] = 0;
+  if (t == 0) s_over = 0;
   __syncthreads();
-  // counts per local node: 4 independent loads in flight per thread, then fire-and-forget atomics
   constexpr int U = 4;
   for (int i0 = 0; i0 < n; i0 += U * kChunkNodes) {
     int nd[U];
+    int32_t el[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * kChunkNodes + t;
       nd[u] = i < n ? (int)__ldg(bnode + b0 + i) : -1;
+      el[u] = i < n ? __ldg(belem + b0 + i) : 0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (nd[u] >= 0) atomicAdd(&s_cnt[nd[u]], 1);
+      if (nd[u] >= 0) {
+        const int pos = atomicAdd(&s_cnt[nd[u]], 1);
+        if (pos < kSegMax) slots[pos * kSlotPitch + nd[u]] = el[u];
+        else s_over = 1;
+      }
   }
   __syncthreads();
   const int d = s_cnt[t];
@@ -1326,43 +1335,41 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
   const int64_t a = n0 + t;
   if (a < N) eoff[a] = b0 + excl;
   if (a == N - 1) eoff[N] = b1;
-  __syncthreads();
-  s_cnt[t] = excl;   // per-node cursor
-  __syncthreads();
-  // placement (second read of the bucket, from L2): 4 loads, then 4 independent returning atomics
-  for (int i0 = 0; i0 < n; i0 += U * kChunkNodes) {
-    int nd[U];
-    int32_t el[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = i0 + u * kChunkNodes + t;
-      nd[u] = i < n ? (int)__ldg(bnode + b0 + i) : -1;
-      el[u] = i < n ? __ldg(belem + b0 + i) : 0;
+  s_ex[t] = excl;
+  const bool over = s_over != 0;   // CTA-uniform (read after the barrier above)
+  if (!over) {
+    const int dd = SORT ? d : 0;
+    const int wmax = __reduce_max_sync(FULL, (unsigned)dd);
+    if (wmax > 1) {
+      if (wmax <= 8) sort_slot_column<8>(slots, t, dd);
+      else if (wmax <= 16) sort_slot_column<16>(slots, t, dd);
+      else sort_slot_column<32>(slots, t, dd);
     }
-    int pos[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) pos[u] = nd[u] >= 0 ? atomicAdd(&s_cnt[nd[u]], 1) : 0;
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (nd[u] >= 0) {
-        if (staged) s_out[chunk_skew(pos[u])] = el[u];
-        else eidx[b0 + pos[u]] = el[u];
-      }
+    __syncthreads();
+    // warp w copies the lists of nodes 32w .. 32w+31: lane i writes entry i of the node
+#pragma unroll 4
+    for (int q = 0; q < 32; ++q) {
+      const int nodeq = warp * 32 + q;
+      const int dq = s_cnt[nodeq];
+      if (lane < dq) eidx[b0 + s_ex[nodeq] + lane] = slots[lane * kSlotPitch + nodeq];
+    }
+    return;
+  }
+  // overflowed chunk: place in global memory with the known counts, sort there (lists > kSegMax
+  // go to k_segsort_giant)
+  __syncthreads();
+  s_cnt[t] = excl;
+  __syncthreads();
+  for (int i = t; i < n; i += kChunkNodes) {
+    const int slot = atomicAdd(&s_cnt[(int)__ldg(bnode + b0 + i)], 1);
+    eidx[b0 + slot] = __ldg(belem + b0 + i);
   }
   const bool big = d > kSegMax;
   if (a < N && big && SORT) giants[atomicAdd(ngiant, 1u)] = (uint32_t)a;
   const int dd = (SORT && !big) ? d : 0;
   const int wmax = __reduce_max_sync(FULL, (unsigned)dd);
-  __syncthreads();   // placement complete (shared and, unstaged, this CTA's global writes)
-  if (staged) {
-    if (wmax > 1) {
-      if (wmax <= 8) sort_chunk_segment<8>(s_out, excl, dd);
-      else if (wmax <= 16) sort_chunk_segment<16>(s_out, excl, dd);
-      else sort_chunk_segment<32>(s_out, excl, dd);
-    }
-    __syncthreads();
-    for (int i = t; i < n; i += kChunkNodes) eidx[b0 + i] = s_out[chunk_skew(i)];
-  } else if (wmax > 1) {
+  __syncthreads();   // the CTA's global writes are visible to the CTA after the barrier
+  if (wmax > 1) {
     int32_t* seg = eidx + b0 + excl;
     if (wmax <= 8) sort_segment<8>(seg, dd);
     else if (wmax <= 16) sort_segment<16>(seg, dd);
