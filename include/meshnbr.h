@@ -276,6 +276,13 @@ mn_status mn_dist_finish(mn_elem_type type, const uint64_t* d_pairs, int64_t n, 
 mn_status mn_set_elem_path(int mode);
 int mn_get_elem_path(void);
 
+/* Test knob (process-wide): upper bound on the capacity, in entries, of the fixed-size 128-node
+ * chunk buckets the transpose path scatters into in one read of conn (auto: twice the mean chunk
+ * load, 2 * k * M / ceil(N / 128), rounded down to a multiple of 32).  0 restores auto.  When a
+ * chunk overflows its bucket the counted path (count, scan, scatter) runs instead, so results never
+ * depend on it; tests use a small cap to force that fallback.  MN_ERR_INVALID_ARG if cap < 0. */
+mn_status mn_set_chunk_cap(int cap);
+
 /* ---------------------------------------------------------------------------------------------
  * Instrumentation (bench only; not thread-safe)
  * ------------------------------------------------------------------------------------------- */

@@ -24,7 +24,7 @@ __all__ = [
     "emit_node_pairs", "emit_elem_pairs", "radix_sort_keys", "radix_sort_pairs_u32",
     "unique_node_csr", "elem_offsets", "exclusive_scan",
     "dist_bucket", "dist_finish",
-    "launch_count", "profile_enable", "profile_reset", "profile_collect", "set_elem_path", "get_elem_path",
+    "launch_count", "profile_enable", "profile_reset", "profile_collect", "set_elem_path", "get_elem_path", "set_chunk_cap",
 ]
 
 TRI3, QUAD4, TET4, HEX8 = 0, 1, 2, 3
@@ -123,6 +123,7 @@ def _declare(lib):
         "mn_launch_count": (_I64, []),
         "mn_set_elem_path": (S, [_INT]),
         "mn_get_elem_path": (_INT, []),
+        "mn_set_chunk_cap": (S, [_INT]),
         "mn_profile_enable": (None, [_INT]),
         "mn_profile_reset": (None, []),
         "mn_profile_collect": (_INT, []),
@@ -581,6 +582,11 @@ ELEM_PATHS = {"auto": 0, "radix": 1, "transpose": 2}
 def set_elem_path(mode="auto"):
     """Element-CSR algorithm (process-wide): "auto" | "radix" | "transpose" (include/meshnbr.h)."""
     _check(load().mn_set_elem_path(ELEM_PATHS[mode] if isinstance(mode, str) else int(mode)))
+
+
+def set_chunk_cap(cap: int = 0):
+    """Test knob: cap the fixed chunk-bucket capacity of the transpose path (0 = auto; include/meshnbr.h)."""
+    _check(load().mn_set_chunk_cap(int(cap)))
 
 
 def get_elem_path() -> str:

@@ -29,6 +29,7 @@ namespace mn {
 static std::atomic<int64_t> g_launches{0};
 // element-CSR algorithm: 0 = auto (locality test), 1 = LSD radix sort, 2 = counting-sort transpose
 static std::atomic<int> g_elem_path{0};
+static std::atomic<int> g_chunk_cap{0};   // test knob: cap on the fixed chunk-bucket capacity (0 = auto)
 constexpr int64_t kTransposeMinElems = 1 << 20;
 constexpr double kTransposeMaxGroupRatio = 0.5;
 static bool g_prof = false;
@@ -531,6 +532,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     int32_t* eidx = elem_idx;
     const int64_t nchunks = tiles_of(P.N, kChunkNodes);
     int32_t *ccnt = nullptr, *ccur = nullptr;
+    unsigned int* ovf = nullptr;   // a fixed-capacity chunk bucket overflowed
     int64_t* cbase = nullptr;
     auto layout = [&](Arena& a) {
       errw = a.take<unsigned long long>(2);
@@ -546,6 +548,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       if (transpose) {
         ccnt = a.take<int32_t>((size_t)nchunks + 1);
         ccur = a.take<int32_t>((size_t)nchunks + 1);
+        ovf = a.take<unsigned int>(1);
       }
       head = a.off;
       if (transpose) sgiants = a.take<uint32_t>((size_t)P.N + 1);
@@ -585,31 +588,57 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     }
     if (transpose) {
       // ---- a2 + a3e + a4 + a5 (elements): transpose bucketed by 128-node chunk ----
+      // belem spans ekA + ekB (>= 2 Pe entries), bnode the bytes of epA + epB (>= 8 Pe)
       int32_t* belem = reinterpret_cast<int32_t*>(ekA);
-      uint8_t* bnode = reinterpret_cast<uint8_t*>(ekB);
-      MN_CUDA(launch("elem_count", 4.0 * P.K * P.M, s, [&] {
-        if (aligned) k_chunk_count<T, true><<<count_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ccnt, errw);
-        else k_chunk_count<T, false><<<count_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ccnt, errw);
+      uint8_t* bnode = reinterpret_cast<uint8_t*>(epA);
+      // single conn read: fixed-capacity buckets of cap entries (2 Pe / nchunks, i.e. twice the mean
+      // chunk load); on overflow the counted path below runs (guarded by *ovf) and replaces it
+      int64_t capl = nchunks > 0 ? (2 * P.Pe / nchunks) & ~(int64_t)31 : 0;
+      const int ovr = g_chunk_cap.load();
+      if (ovr > 0 && ovr < capl) capl = ovr;
+      if (capl > (int64_t)INT32_MAX - 4096) capl = (int64_t)INT32_MAX - 4096;
+      const int cap = (int)capl;
+      MN_CUDA(launch("elem_scatter", 4.0 * P.K * P.M + 5.0 * P.Pe, s, [&] {
+        if (aligned)
+          k_chunk_scatter_fixed<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, cap, ccur, belem, bnode,
+                                                                         errw, ovf);
+        else
+          k_chunk_scatter_fixed<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, cap, ccur, belem, bnode,
+                                                                          errw, ovf);
       }));
       if (nchunks > 0)
         MN_CUDA(launch("scan_counts", 12.0 * nchunks, s, [&] {
           k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nchunks, kScanTile), kScanThreads, 0, s>>>(
-              ccnt, nchunks, cbase, sstatus, tickets + 29, 1);
+              ccur, nchunks, cbase, sstatus, tickets + 29, 1);
         }));
-      MN_CUDA(launch("elem_scatter", 4.0 * P.K * P.M + 5.0 * P.Pe, s, [&] {
+      // ---- fallback (only if a bucket overflowed; otherwise each kernel returns at once) ----
+      MN_CUDA(launch("count_fallback", 0.0, s, [&] {
         if (aligned)
-          k_chunk_scatter<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, cbase, ccur, belem, bnode, errw);
+          k_chunk_count<T, true><<<count_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ccnt, errw, 0, INT64_MAX, ovf);
         else
-          k_chunk_scatter<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, cbase, ccur, belem, bnode, errw);
+          k_chunk_count<T, false><<<count_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, ccnt, errw, 0, INT64_MAX, ovf);
+      }));
+      if (nchunks > 0)
+        MN_CUDA(launch("scan_fallback", 0.0, s, [&] {
+          k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nchunks, kScanTile), kScanThreads, 0, s>>>(
+              ccnt, nchunks, cbase, sstatus, tickets + 28, 3, ovf);
+        }));
+      MN_CUDA(launch("scatter_fallback", 0.0, s, [&] {
+        if (aligned)
+          k_chunk_scatter<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, cbase, cursor, belem, bnode, errw,
+                                                                   0, INT64_MAX, ovf);
+        else
+          k_chunk_scatter<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, cbase, cursor, belem, bnode, errw,
+                                                                    0, INT64_MAX, ovf);
       }));
       if (nchunks > 0)
         MN_CUDA(launch("elem_segsort", 9.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
           if (want_elem)
             k_chunk_sort<true><<<(unsigned)nchunks, kChunkNodes, 0, s>>>(cbase, P.N, belem, bnode, eoff, eidx,
-                                                                          sgiants, nsgiant, errw);
+                                                                          sgiants, nsgiant, errw, ovf, cap);
           else
             k_chunk_sort<false><<<(unsigned)nchunks, kChunkNodes, 0, s>>>(cbase, P.N, belem, bnode, eoff, eidx,
-                                                                           sgiants, nsgiant, errw);
+                                                                           sgiants, nsgiant, errw, ovf, cap);
         }));
       if (want_elem)
         MN_CUDA(launch("segsort_giant", 0.0, s, [&] {
@@ -1829,7 +1858,12 @@ mn_status mn_workspace_bytes(mn_elem_type t, int64_t M, int64_t N, int modes, si
   a.take<int32_t>((size_t)P.N + 1);
   a.take<unsigned int>(1);
   a.take<int32_t>((size_t)P.N + 1);
+  const size_t nch = (size_t)tiles_of(P.N, kChunkNodes);   // transpose: chunk counts, cursors, flag
+  a.take<int32_t>(nch + 1);
+  a.take<int32_t>(nch + 1);
+  a.take<unsigned int>(1);
   a.take<uint32_t>((size_t)P.N + 1);
+  a.take<int64_t>(nch + 1);
   for (int i = 0; i < 4; ++i) a.take<uint32_t>((size_t)P.Pe);
   if (wn) {
     a.take<int32_t>((size_t)P.N);
@@ -2001,6 +2035,12 @@ mn_status mn_set_elem_path(int mode) {
 }
 
 int mn_get_elem_path(void) { return g_elem_path.load(); }
+
+mn_status mn_set_chunk_cap(int cap) {
+  if (cap < 0) return MN_ERR_INVALID_ARG;
+  g_chunk_cap.store(cap);
+  return MN_OK;
+}
 
 void mn_profile_enable(int on) { g_prof = on != 0; }
 

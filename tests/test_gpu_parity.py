@@ -199,6 +199,28 @@ def test_whole_path_both(name, et, make, elem_path):
     _assert_csr((eo, ei), oracle.elem_csr(et, conn, N), name + " elem " + elem_path)
 
 
+@pytest.mark.parametrize("cap", [32, 96, 1 << 20])
+@pytest.mark.parametrize("name,et,make", SMALL + [("kuhn_40", meshgen.TET4, lambda: meshgen.kuhn_tets(40)),
+                                                  ("sphere_1000x50", meshgen.TRI3, lambda: meshgen.uv_sphere(1000, 50))])
+def test_transpose_fixed_bucket_capacity(name, et, make, cap):
+    """The transpose's single-read scatter into fixed-capacity chunk buckets: with a small cap some
+    buckets overflow and the guarded counted path must replace the result; with a large cap (auto)
+    the fixed layout is used whenever it fits.  Same CSRs either way."""
+    conn, N = make()
+    mn().set_elem_path("transpose")
+    mn().set_chunk_cap(cap)
+    try:
+        (no, ni), (eo, ei) = mn().find_neighbors(conn.cuda(), et, N)
+        eo2, ei2 = mn().find_elem_neighbors(conn.cuda(), et, N)
+    finally:
+        mn().set_chunk_cap(0)
+        mn().set_elem_path("auto")
+    _assert_csr((no, ni), oracle.node_csr(et, conn, N), f"{name} node cap {cap}")
+    exp = oracle.elem_csr(et, conn, N)
+    _assert_csr((eo, ei), exp, f"{name} elem cap {cap}")
+    _assert_csr((eo2, ei2), exp, f"{name} elem-only cap {cap}")
+
+
 @pytest.mark.parametrize("name,et,make", SMALL)
 def test_whole_path_single_modes(name, et, make, elem_path):
     conn, N = make()

@@ -14,7 +14,8 @@ NAMES = [("k_node_gather_t", "node_gather"), ("k_elem_scatter", "elem_scatter"),
          ("k_hist_validate", "hist_validate"), ("k_node_giant", "node_giant"), ("k_segsort_giant", "segsort_giant"),
          ("k_locality_sample", "locality_sample"), ("k_bucket_bases", "bucket_bases"),
          ("k_poly_count", "poly_count"), ("k_poly_scatter", "poly_scatter"), ("k_poly_gather", "poly_gather"),
-         ("k_poly_giant", "poly_giant"), ("k_chunk_count", "elem_count"), ("k_chunk_scatter", "elem_scatter"),
+         ("k_poly_giant", "poly_giant"), ("k_chunk_count", "count_fallback"), ("k_chunk_scatter<", "scatter_fallback"),
+         ("k_chunk_scatter_fixed", "elem_scatter"),
          ("k_chunk_sort", "elem_segsort")]
 
 
