@@ -1269,19 +1269,24 @@ k_chunk_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __re
 // cap sets *ovf and keeps only its first cap entries: the host queues the counted path
 // (k_chunk_count -> k_scan_i32 -> k_chunk_scatter, each guarded by *ovf) behind it, so the result
 // never depends on cap.  Saves the count pass's read of conn (config 5: 1.08 ms of 11.3).
-template <int T, bool ALIGNED>
-__global__ void __launch_bounds__(256)
+template <int T, bool ALIGNED, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB)
 k_chunk_scatter_fixed(const int32_t* __restrict__ conn, int64_t M, int64_t N, int cap,
                       int32_t* __restrict__ ccur, int32_t* __restrict__ belem, uint8_t* __restrict__ bnode,
                       unsigned long long* __restrict__ err, unsigned int* __restrict__ ovf) {
   constexpr int K = Elem<T>::K;
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < M; base += stride) {
+  int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  int nv[K];   // the next row, loaded one iteration ahead
+  if (base + lane < M) load_row<T, ALIGNED>(conn, base + lane, nv);
+  for (; base < M; base += stride) {
     const int64_t e = base + lane;
     const bool in = e < M;
     int v[K];
-    if (in) load_row<T, ALIGNED>(conn, e, v);
+#pragma unroll
+    for (int p = 0; p < K; ++p) v[p] = nv[p];
+    if (base + stride + lane < M) load_row<T, ALIGNED>(conn, base + stride + lane, nv);
     int bad = -1, kind = 0;
     if (in) {
 #pragma unroll
@@ -1299,19 +1304,23 @@ k_chunk_scatter_fixed(const int32_t* __restrict__ conn, int64_t M, int64_t N, in
       if (bad >= 0) atomicMin(err, (unsigned long long)err_encode((uint64_t)e, kind, bad));
     }
     const bool ok = in && bad < 0;
+    // all K returning atomics issued before any result is used (one L2 round trip per row, not K)
+    int x[K], b[K];
+    unsigned peers[K];
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      const int x = ok ? (v[p] >> 7) : -1;   // one shared sentinel (match cost grows with distinct values)
-      const unsigned peers = __match_any_sync(FULL, x);
-      const int leader = __ffs(peers) - 1;
-      int b = 0;
-      if (ok && lane == leader) {
-        b = atomicAdd(ccur + x, (int)__popc(peers));
-        if (b + (int)__popc(peers) > cap) *ovf = 1u;
-      }
-      b = __shfl_sync(FULL, b, leader) + __popc(peers & lanemask_lt());
-      if (ok && b < cap) {
-        const int64_t pos = (int64_t)x * cap + b;
+      x[p] = ok ? (v[p] >> 7) : -1;   // one shared sentinel (match cost grows with distinct values)
+      peers[p] = __match_any_sync(FULL, x[p]);
+      b[p] = 0;
+      if (ok && lane == __ffs(peers[p]) - 1) b[p] = atomicAdd(ccur + x[p], (int)__popc(peers[p]));
+    }
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      const int leader = __ffs(peers[p]) - 1;
+      if (ok && lane == leader && b[p] + (int)__popc(peers[p]) > cap) *ovf = 1u;
+      const int q = __shfl_sync(FULL, b[p], leader) + __popc(peers[p] & lanemask_lt());
+      if (ok && q < cap) {
+        const int64_t pos = (int64_t)x[p] * cap + q;
         belem[pos] = (int32_t)e;
         bnode[pos] = (uint8_t)(v[p] & (kChunkNodes - 1));
       }
@@ -1364,6 +1373,33 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
   if (t == 0) s_over = 0;
   __syncthreads();
   constexpr int U = 4;
+  if ((bb & 15) == 0) {   // CTA-uniform: 16-byte aligned bucket (the fixed layout) -> vector loads
+    // thread t takes entries [i0 + 4t, i0 + 4t + 4): one 4-byte node load + one int4 element load
+    for (int i0 = 0; i0 < n; i0 += U * kChunkNodes) {
+      const int i = i0 + U * t;
+      int nd[U];
+      int32_t el[U];
+      if (i + U <= n) {
+        const uint32_t nq = __ldg(reinterpret_cast<const uint32_t*>(bnode + bb + i));
+        const int4 eq = __ldg(reinterpret_cast<const int4*>(belem + bb + i));
+        nd[0] = nq & 255; nd[1] = (nq >> 8) & 255; nd[2] = (nq >> 16) & 255; nd[3] = nq >> 24;
+        el[0] = eq.x; el[1] = eq.y; el[2] = eq.z; el[3] = eq.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          nd[u] = i + u < n ? (int)__ldg(bnode + bb + i + u) : -1;
+          el[u] = i + u < n ? __ldg(belem + bb + i + u) : 0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (nd[u] >= 0) {
+          const int pos = atomicAdd(&s_cnt[nd[u]], 1);
+          if (pos < kSegMax) slots[pos * kSlotPitch + nd[u]] = el[u];
+          else s_over = 1;
+        }
+    }
+  } else {
   for (int i0 = 0; i0 < n; i0 += U * kChunkNodes) {
     int nd[U];
     int32_t el[U];
@@ -1380,6 +1416,7 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
         if (pos < kSegMax) slots[pos * kSlotPitch + nd[u]] = el[u];
         else s_over = 1;
       }
+  }
   }
   __syncthreads();
   const int d = s_cnt[t];
