@@ -804,10 +804,20 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
         // candidates are the row values != a; otherwise the local neighbour table is used
         constexpr bool simplex = (C == K - 1);   // simplices and SHARED: all other row values
         const int p = simplex ? 0 : local_of<T>(row[q], (int)(a + a_base));
+        // simplex: the K - 1 values != a compacted with selects (other[j] = row[j + 1] once a has
+        // been passed), so every lane inserts on every step (no divergent skip of a itself)
+        uint32_t other[K > 1 ? K - 1 : 1];
+        if (simplex) {
+          bool passed = false;
 #pragma unroll
-        for (int c = 0; c < (simplex ? K : C); ++c) {
-          const uint32_t v = simplex ? (uint32_t)row[q][c] : pick<T>(row[q], nbr_local<T>(p, c));
-          if (simplex && v == (uint32_t)(a + a_base)) continue;
+          for (int j = 0; j < K - 1; ++j) {
+            passed = passed || row[q][j] == (int)(a + a_base);
+            other[j] = (uint32_t)(passed ? row[q][j + 1] : row[q][j]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const uint32_t v = simplex ? other[c] : pick<T>(row[q], nbr_local<T>(p, c));
           uint32_t h = (v * 0x9E3779B1u) >> (32 - HB);
           while (L <= MU) {   // at most MU + 1 entries: the set never fills
             const uint32_t x = tab[h][t];
