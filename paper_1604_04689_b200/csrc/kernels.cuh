@@ -739,6 +739,8 @@ __device__ __forceinline__ void sort_small(uint32_t (*tab)[kNodeThreads], int t,
 // cost more occupancy than the saved pass.)
 // SHARED: element-sharing ("FEM sparsity") adjacency — every other node of an incident element
 // is a neighbour, so each incidence yields CE = K - 1 candidates.
+// (prefetching the next batch's incidence window one batch ahead: 4.47 / 4.54 ms at 10 / 8 CTAs per
+// SM vs 4.19 on config 5 -- not kept)
 // >= 10 CTAs per SM (<= 48 registers) for arity <= 4: 4.48 vs 4.75 ms on config 5; hex keeps its
 // registers for the 8-int rows (48 registers: 3.25 vs 2.63 ms on config 4).  profiles/round1/sweep_gather_minb.txt
 template <int T, bool ALIGNED, bool DIST = false, bool SHARED = false,
@@ -819,16 +821,34 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
         for (int c = 0; c < C; ++c) {
           const uint32_t v = simplex ? other[c] : pick<T>(row[q], nbr_local<T>(p, c));
           uint32_t h = (v * 0x9E3779B1u) >> (32 - HB);
-          while (L <= MU) {   // at most MU + 1 entries: the set never fills
-            const uint32_t x = tab[h][t];
-            if (x == v) break;
-            if (x == EMPTY) {
-              tab[h][t] = v;
-              used |= Mask(1) << h;
-              ++L;
-              break;
+          if (WIDE) {   // (measured: this form is 5% faster for the 64-slot set, 8% slower for 32)
+            if (L <= MU) {   // at most MU + 1 entries: the set never fills
+              // first probe resolves most candidates (hit or empty slot) without a branch
+              uint32_t x = tab[h][t];
+              if (x != v && x != EMPTY) {
+                do {
+                  h = (h + 1) & (HS - 1);
+                  x = tab[h][t];
+                } while (x != v && x != EMPTY);
+              }
+              if (x == EMPTY) {
+                tab[h][t] = v;
+                used |= Mask(1) << h;
+                ++L;
+              }
             }
-            h = (h + 1) & (HS - 1);
+          } else {
+            while (L <= MU) {   // at most MU + 1 entries: the set never fills
+              const uint32_t x = tab[h][t];
+              if (x == v) break;
+              if (x == EMPTY) {
+                tab[h][t] = v;
+                used |= Mask(1) << h;
+                ++L;
+                break;
+              }
+              h = (h + 1) & (HS - 1);
+            }
           }
         }
       }
@@ -1286,17 +1306,20 @@ k_chunk_scatter_fixed(const int32_t* __restrict__ conn, int64_t M, int64_t N, in
                       unsigned long long* __restrict__ err, unsigned int* __restrict__ ovf) {
   constexpr int K = Elem<T>::K;
   const int lane = threadIdx.x & 31;
+  // (grid-stride; a blocked assignment, each CTA on its own contiguous element range so that few
+  // CTAs share a chunk counter at a time, measured the same: 2.10-2.28 vs 2.14 ms on config 5)
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  const int64_t hi = M;
   int nv[K];   // the next row, loaded one iteration ahead
-  if (base + lane < M) load_row<T, ALIGNED>(conn, base + lane, nv);
-  for (; base < M; base += stride) {
+  if (base + lane < hi) load_row<T, ALIGNED>(conn, base + lane, nv);
+  for (; base < hi; base += stride) {
     const int64_t e = base + lane;
-    const bool in = e < M;
+    const bool in = e < hi;
     int v[K];
 #pragma unroll
     for (int p = 0; p < K; ++p) v[p] = nv[p];
-    if (base + stride + lane < M) load_row<T, ALIGNED>(conn, base + stride + lane, nv);
+    if (base + stride + lane < hi) load_row<T, ALIGNED>(conn, base + stride + lane, nv);
     int bad = -1, kind = 0;
     if (in) {
 #pragma unroll
