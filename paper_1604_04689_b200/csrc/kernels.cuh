@@ -1479,12 +1479,24 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
       else sort_slot_column<32>(slots, t, dd);
     }
     __syncthreads();
-    // warp w copies the lists of nodes 32w .. 32w+31: lane i writes entry i of the node
+    if (n >= 8 * kChunkNodes) {
+      // long lists (mean >= 8): warp w copies the lists of nodes 32w .. 32w+31, lane i writing
+      // entry i of the node (one coalesced store per node)
 #pragma unroll 4
-    for (int q = 0; q < 32; ++q) {
-      const int nodeq = warp * 32 + q;
-      const int dq = s_cnt[nodeq];
-      if (lane < dq) eidx[b0 + s_ex[nodeq] + lane] = slots[lane * kSlotPitch + nodeq];
+      for (int q = 0; q < 32; ++q) {
+        const int nodeq = warp * 32 + q;
+        const int dq = s_cnt[nodeq];
+        if (lane < dq) eidx[b0 + s_ex[nodeq] + lane] = slots[lane * kSlotPitch + nodeq];
+      }
+    } else {
+      // short lists: thread i writes chunk output position i; its node by binary search in s_ex
+      for (int i = t; i < n; i += kChunkNodes) {
+        int lo = 0;
+#pragma unroll
+        for (int step = kChunkNodes / 2; step > 0; step >>= 1)
+          if (s_ex[lo + step] <= i) lo += step;
+        eidx[b0 + i] = slots[(i - s_ex[lo]) * kSlotPitch + lo];
+      }
     }
     return;
   }

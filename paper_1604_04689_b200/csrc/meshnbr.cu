@@ -1091,6 +1091,16 @@ static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, in
   int64_t *eoff = nullptr, *rawoff = nullptr;
   int32_t* eidx = nullptr;
   size_t head = 0;
+  // node / element outputs of a non-empty mesh: chunk-bucketed transpose (single read of the rings
+  // into fixed-capacity 128-node chunk buckets, guarded counted fallback; kernels.cuh / poly.cuh).
+  // The element-sharing adjacency needs per-node raw candidate counts: the counted per-node path.
+  const bool chunk = !wsh && M > 0 && N > 0;
+  const int64_t nch = tiles_of(N, kChunkNodes);
+  int32_t* ccur = nullptr;
+  unsigned int* ovf = nullptr;
+  int64_t* cbase = nullptr;
+  uint8_t* bnode = nullptr;
+  int ccap = 0;
   auto fill = [&](mn_csr* o, int64_t* offs, int32_t* ind, int64_t nnz) {
     o->num_nodes = N; o->nnz = nnz; o->offsets = offs; o->indices = ind; o->owner = mem.a;
   };
@@ -1117,7 +1127,9 @@ static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, in
       cinc = a.take<int32_t>((size_t)N + 1);
       cursor = a.take<int32_t>((size_t)N + 1);
       if (wsh) rawcnt = a.take<int32_t>((size_t)N + 1);
+      if (chunk) { ccur = a.take<int32_t>((size_t)nch + 1); ovf = a.take<unsigned int>(1); }
       head = a.off;
+      if (chunk) { cbase = a.take<int64_t>((size_t)nch + 1); bnode = a.take<uint8_t>((size_t)2 * L); }
       sgiants = a.take<uint32_t>((size_t)N + 1);
       giants = a.take<uint32_t>((size_t)N + 1);
       eoff = we ? elem_off : a.take<int64_t>((size_t)N + 1);
@@ -1136,7 +1148,45 @@ static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, in
   }
   MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
   MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
-  if (M == 0) {
+  if (chunk) {
+    // buckets: element ids in tempR (2 L entries; the ring-edge gather's raw region afterwards),
+    // local node bytes in bnode; capacity twice the mean chunk load
+    tempR = (uint32_t*)mem.get((size_t)2 * L * 4 + 16);
+    if (!tempR) { st = MN_ERR_OOM; goto done; }
+    int32_t* belem = reinterpret_cast<int32_t*>(tempR);
+    int64_t capl = (2 * L / nch) & ~(int64_t)31;
+    const int ovr = g_chunk_cap.load();
+    if (ovr > 0 && ovr < capl) capl = ovr;
+    if (capl > (int64_t)INT32_MAX - 4096) capl = (int64_t)INT32_MAX - 4096;
+    ccap = (int)capl;
+    MN_CUDA(launch("poly_scatter", 16.0 * M + 9.0 * L, s, [&] {
+      k_poly_chunk_scatter<true><<<hist_grid(M), 256, 0, s>>>(off, idx, M, L, N, ccap, nullptr, ccur, belem, bnode,
+                                                              errw, ovf);
+    }));
+    MN_CUDA(launch("scan_counts", 12.0 * nch, s, [&] {
+      k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nch, kScanTile), kScanThreads, 0, s>>>(
+          ccur, nch, cbase, sstatus, tickets + 29, 1);
+    }));
+    MN_CUDA(launch("count_fallback", 0.0, s, [&] {
+      k_poly_chunk_count<<<hist_grid(M), 256, 0, s>>>(off, idx, M, cinc, errw, ovf);
+    }));
+    MN_CUDA(launch("scan_fallback", 0.0, s, [&] {
+      k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nch, kScanTile), kScanThreads, 0, s>>>(
+          cinc, nch, cbase, sstatus, tickets + 28, 3, ovf);
+    }));
+    MN_CUDA(launch("scatter_fallback", 0.0, s, [&] {
+      k_poly_chunk_scatter<false><<<hist_grid(M), 256, 0, s>>>(off, idx, M, L, N, 0, cbase, cursor, belem, bnode,
+                                                               errw, ovf);
+    }));
+    MN_CUDA(launch("elem_segsort", 9.0 * L + 8.0 * (N + 1), s, [&] {
+      if (we)   // element lists sorted (R3); for the node adjacency alone the grouping suffices
+        k_chunk_sort<true><<<(unsigned)nch, kChunkNodes, 0, s>>>(cbase, N, belem, bnode, eoff, eidx, sgiants,
+                                                                  nsgiant, errw, ovf, ccap);
+      else
+        k_chunk_sort<false><<<(unsigned)nch, kChunkNodes, 0, s>>>(cbase, N, belem, bnode, eoff, eidx, sgiants,
+                                                                   nsgiant, errw, ovf, ccap);
+    }));
+  } else if (M == 0) {
     MN_CUDA(cudaMemsetAsync(eoff, 0, (size_t)(N + 1) * 8, s));
   } else {
     MN_CUDA(launch("poly_count", 16.0 * M + 4.0 * L, s, [&] {
@@ -1162,14 +1212,16 @@ static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, in
   if (st != MN_OK) goto done;
   rawtotal = (wsh && M > 0 && N > 0) ? (int64_t)host[1] : 0;
   if (M > 0) {
-    MN_CUDA(launch("poly_scatter", 16.0 * M + 16.0 * L, s, [&] {
-      k_poly_scatter<<<hist_grid(M), 256, 0, s>>>(off, idx, M, eoff, cursor, eidx, errw);
-    }));
-    if (we) {
-      MN_CUDA(launch("elem_segsort", 8.0 * L + 8.0 * (N + 1), s, [&] {
-        segsort_fn<<<(unsigned)tiles_of(N, kSegThreads), kSegThreads, 0, s>>>(eoff, N, eidx, sgiants, nsgiant,
-                                                                                 errw);
+    if (!chunk)
+      MN_CUDA(launch("poly_scatter", 16.0 * M + 16.0 * L, s, [&] {
+        k_poly_scatter<<<hist_grid(M), 256, 0, s>>>(off, idx, M, eoff, cursor, eidx, errw);
       }));
+    if (we) {
+      if (!chunk)
+        MN_CUDA(launch("elem_segsort", 8.0 * L + 8.0 * (N + 1), s, [&] {
+          segsort_fn<<<(unsigned)tiles_of(N, kSegThreads), kSegThreads, 0, s>>>(eoff, N, eidx, sgiants, nsgiant,
+                                                                                   errw);
+        }));
       static bool seg_attr = false;
       if (!seg_attr) {
         cudaFuncSetAttribute(k_segsort_giant, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
@@ -1186,7 +1238,7 @@ static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, in
       poly_attr = true;
     }
     if (wn) {   // ring-edge node adjacency: 2 raw candidates per incidence
-      tempR = L ? (uint32_t*)mem.get((size_t)2 * L * 4) : nullptr;
+      if (!tempR) tempR = L ? (uint32_t*)mem.get((size_t)2 * L * 4) : nullptr;
       if (L && !tempR) { st = MN_ERR_OOM; goto done; }
       MN_CUDA(launch("poly_gather", 8.0 * (N + 1) + 4.0 * L + 24.0 * L, s, [&] {
         k_poly_gather<false><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, off, idx, N, nullptr, 2, tempR, cntR, lofsR,

@@ -99,6 +99,97 @@ k_poly_scatter(const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
   }
 }
 
+// ---- chunk-bucketed polygon transpose (node / element outputs; the fixed types' scheme, kernels.cuh)
+// Validation of one ring (reading R18, the order of k_poly_count): returns -1 if valid, else the
+// error word's (kind, pos) packed as kind << 22 | pos.
+__device__ __forceinline__ int64_t poly_check(const int64_t* __restrict__ off, const int32_t* __restrict__ idx,
+                                              int64_t e, int64_t L, int64_t N) {
+  const int64_t b = off[e], k = off[e + 1] - b;
+  if (b < 0 || off[e + 1] > L || k > kPolyMaxArity) return (int64_t)3 << 22;
+  if (k < 3) return (int64_t)2 << 22;
+  const int32_t* row = idx + b;
+  for (int64_t p = 0; p < k; ++p)
+    if (row[p] < 0 || (int64_t)row[p] >= N) return p;
+  for (int64_t p = 1; p < k; ++p) {
+    const int32_t x = row[p];
+    for (int64_t q = 0; q < p; ++q)
+      if (row[q] == x) return ((int64_t)1 << 22) | p;
+  }
+  return -1;
+}
+
+// FIXED: single read, validation + append (element id, local node byte) to the node's 128-node
+// chunk bucket at [x * cap, (x + 1) * cap); an overflow sets *ovf (the guarded counted path then
+// replaces the result).  !FIXED (fallback, guarded by *ovf): counted buckets at cbase[x], cursors
+// `cur`.  Lane per element; the warp steps through ring positions together and lanes holding the
+// same chunk at a step reserve their slots with one returning atomic.
+template <bool FIXED>
+__global__ void __launch_bounds__(256)
+k_poly_chunk_scatter(const int64_t* __restrict__ off, const int32_t* __restrict__ idx, int64_t M, int64_t L,
+                     int64_t N, int cap, const int64_t* __restrict__ cbase, int32_t* __restrict__ cur,
+                     int32_t* __restrict__ belem, uint8_t* __restrict__ bnode, unsigned long long* __restrict__ err,
+                     unsigned int* __restrict__ ovf) {
+  if (!FIXED && *ovf == 0u) return;
+  if (!FIXED && *err != ERR_NONE) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < M; base += stride) {
+    const int64_t e = base + lane;
+    bool ok = e < M;
+    if (FIXED && ok) {
+      const int64_t c = poly_check(off, idx, e, L, N);
+      if (c >= 0) {
+        atomicMin(err, (unsigned long long)poly_err((uint64_t)e, (int)(c >> 22), c & 0x3FFFFF));
+        ok = false;
+      }
+    }
+    const int64_t b = ok ? off[e] : 0;
+    const int k = ok ? (int)(off[e + 1] - b) : 0;
+    const int kmax = (int)__reduce_max_sync(FULL, (unsigned)k);
+    for (int p = 0; p < kmax; ++p) {
+      const bool mine = p < k;
+      const int v = mine ? idx[b + p] : 0;
+      const int x = mine ? (v >> 7) : -1;   // one shared sentinel: match cost grows with distinct values
+      const unsigned peers = __match_any_sync(FULL, x);
+      const int leader = __ffs(peers) - 1;
+      int c = 0;
+      if (mine && lane == leader) {
+        c = atomicAdd(cur + x, (int)__popc(peers));
+        if (FIXED && c + (int)__popc(peers) > cap) *ovf = 1u;
+      }
+      c = __shfl_sync(FULL, c, leader) + __popc(peers & lanemask_lt());
+      if (mine && (!FIXED || c < cap)) {
+        const int64_t pos = (FIXED ? (int64_t)x * cap : cbase[x]) + c;
+        belem[pos] = (int32_t)e;
+        bnode[pos] = (uint8_t)(v & (kChunkNodes - 1));
+      }
+    }
+  }
+}
+
+// Fallback counts (guarded by *ovf): per-chunk incidence counts of the (already validated) rings.
+__global__ void __launch_bounds__(256)
+k_poly_chunk_count(const int64_t* __restrict__ off, const int32_t* __restrict__ idx, int64_t M,
+                   int32_t* __restrict__ ccnt, const unsigned long long* __restrict__ err,
+                   const unsigned int* __restrict__ ovf) {
+  if (*ovf == 0u || *err != ERR_NONE) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < M; base += stride) {
+    const int64_t e = base + lane;
+    const bool in = e < M;
+    const int64_t b = in ? off[e] : 0;
+    const int k = in ? (int)(off[e + 1] - b) : 0;
+    const int kmax = (int)__reduce_max_sync(FULL, (unsigned)k);
+    for (int p = 0; p < kmax; ++p) {
+      const bool mine = p < k;
+      const int x = mine ? (idx[b + p] >> 7) : -1;
+      const unsigned peers = __match_any_sync(FULL, x);
+      if (mine && lane == __ffs(peers) - 1) atomicAdd(ccnt + x, (int)__popc(peers));
+    }
+  }
+}
+
 // Raw candidate region of node a: rawoff ? [rawoff[a], rawoff[a+1]) : C * [eoff[a], eoff[a+1]).
 __device__ __forceinline__ int64_t poly_raw_base(const int64_t* eoff, const int64_t* rawoff, int C, int64_t a) {
   return rawoff ? rawoff[a] : (int64_t)C * eoff[a];

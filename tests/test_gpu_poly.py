@@ -65,6 +65,26 @@ def test_poly_parity(name, make):
     _eq(shared, oracle.poly_shared_csr(off, idx, N), name + " shared")
 
 
+@pytest.mark.parametrize("cap", [0, 32, 96])
+@pytest.mark.parametrize("name,make", CASES)
+def test_poly_chunk_path(name, make, cap):
+    """Node + element outputs (no element-sharing CSR) take the chunk-bucketed transpose: fixed
+    capacity buckets (cap 0 = auto), with small caps forcing the guarded counted fallback."""
+    off, idx, N = make()
+    mn().set_chunk_cap(cap)
+    try:
+        node, elem, _ = mn().find_poly_neighbors(off.cuda(), idx.cuda(), N, node=True, elem=True)
+        elem_only = mn().find_poly_neighbors(off.cuda(), idx.cuda(), N, node=False, elem=True)[1]
+        node_only = mn().find_poly_neighbors(off.cuda(), idx.cuda(), N, node=True, elem=False)[0]
+    finally:
+        mn().set_chunk_cap(0)
+    en, ee = oracle.poly_node_csr(off, idx, N), oracle.poly_elem_csr(off, idx, N)
+    _eq(node, en, f"{name} node cap {cap}")
+    _eq(node_only, en, f"{name} node-only cap {cap}")
+    _eq(elem, ee, f"{name} elem cap {cap}")
+    _eq(elem_only, ee, f"{name} elem-only cap {cap}")
+
+
 @pytest.mark.parametrize("sel", [(True, False, False), (False, True, False), (False, False, True),
                                  (True, False, True)])
 def test_output_selection(sel):
@@ -120,11 +140,12 @@ def test_validation_matches_oracle(rings, N):
     if code == oracle.OK:
         m.find_poly_neighbors(off.cuda(), idx.cuda(), N)
         return
-    with pytest.raises(m.MeshError) as ei:
-        m.find_poly_neighbors(off.cuda(), idx.cuda(), N, True, True, True)
     want = {oracle.ERR_RANGE: m.MN_ERR_INDEX_OUT_OF_RANGE, oracle.ERR_DEGENERATE: m.MN_ERR_DEGENERATE,
             oracle.ERR_ARITY: m.MN_ERR_ARITY}[code]
-    assert (ei.value.code, ei.value.elem, ei.value.pos) == (want, e, p)
+    for sel in ((True, True, True), (True, True, False), (False, True, False)):   # counted / chunk paths
+        with pytest.raises(m.MeshError) as ei:
+            m.find_poly_neighbors(off.cuda(), idx.cuda(), N, *sel)
+        assert (ei.value.code, ei.value.elem, ei.value.pos) == (want, e, p), sel
 
 
 def test_bad_offsets():
