@@ -272,6 +272,10 @@ mn_status mn_dist_finish(mn_elem_type type, const uint64_t* d_pairs, int64_t n, 
  *       first array of integers").
  *   2 = counting-sort transpose: per-node counts, scan, scatter, per-node sort of element ids
  *       (element CSR = transpose of the incidence matrix).
+ *   3 = MSD: one stable onesweep pass buckets the (node, element) pairs by node range (512
+ *       ranges), then one CTA per range counts, scans, scatters and sorts in shared memory
+ *       (SURVEY.md §8(f) row 1).  Needs ceil(N / 512) <= 49152; otherwise the LSD sort runs.
+ *       Not chosen by auto (measured slower than 1 on B200).
  * ------------------------------------------------------------------------------------------- */
 mn_status mn_set_elem_path(int mode);
 int mn_get_elem_path(void);

@@ -576,11 +576,11 @@ def dist_finish(etype, pairs: torch.Tensor, row_elems: torch.Tensor, rows: torch
 # ------------------------------------------------------------------------------------------------
 # instrumentation
 # ------------------------------------------------------------------------------------------------
-ELEM_PATHS = {"auto": 0, "radix": 1, "transpose": 2}
+ELEM_PATHS = {"auto": 0, "radix": 1, "transpose": 2, "msd": 3}
 
 
 def set_elem_path(mode="auto"):
-    """Element-CSR algorithm (process-wide): "auto" | "radix" | "transpose" (include/meshnbr.h)."""
+    """Element-CSR algorithm (process-wide): "auto" | "radix" | "transpose" | "msd" (include/meshnbr.h)."""
     _check(load().mn_set_elem_path(ELEM_PATHS[mode] if isinstance(mode, str) else int(mode)))
 
 

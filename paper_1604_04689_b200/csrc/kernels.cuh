@@ -38,7 +38,10 @@ struct PassDigit {   // digit(key) = OWNER ? (key >> shift) / div : (key >> shif
 
 template <typename KeyT, bool OWNER>
 __device__ __forceinline__ uint32_t digit_of(KeyT key, const PassDigit& pd, uint32_t maxbin) {
-  if (OWNER) {
+  if (OWNER && sizeof(KeyT) == 4) {   // 32-bit keys (node ids; div <= N < 2^31): 32-bit division
+    const uint32_t d = ((uint32_t)key >> pd.shift) / (uint32_t)pd.div;
+    return d > maxbin ? maxbin : d;
+  } else if (OWNER) {
     uint64_t d = ((uint64_t)key >> pd.shift) / pd.div;
     return d > maxbin ? maxbin : (uint32_t)d;
   } else {
@@ -100,7 +103,8 @@ k_hist_validate(const int32_t* __restrict__ conn, int64_t M, int64_t N, int64_t 
       if (ok) {
 #pragma unroll
         for (int p = 0; p < K; ++p) {
-          const uint64_t d = (uint64_t)v[p] / owner_div;
+          const uint64_t d = owner_div <= 0xFFFFFFFFull ? (uint64_t)((uint32_t)v[p] / (uint32_t)owner_div)
+                                                        : (uint64_t)v[p] / owner_div;
           atomicAdd(&sh[d < BINS ? d : BINS - 1], 1u);
         }
       }
@@ -1519,6 +1523,122 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
     if (wmax <= 8) sort_segment<8>(seg, dd);
     else if (wmax <= 16) sort_segment<16>(seg, dd);
     else sort_segment<32>(seg, dd);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// MSD element path for meshes without locality: one onesweep pass buckets the
+// (node, element) pairs stably by node range [g * R, (g + 1) * R) (owner digit node / R, 512
+// buckets), then one CTA per bucket finishes the transpose in shared memory instead of the
+// remaining LSD passes: per-node counts (shared atomics on R <= kRangeMax counters), block scan ->
+// element-CSR offsets, scatter of the element ids into their node segments (the bucket's output
+// range, L2-resident), and a register sort per segment (lists > kSegMax go to k_segsort_giant).
+// ------------------------------------------------------------------------------------------------
+constexpr int kRangeThreads = 1024;
+constexpr int kRangeMax = 48 * 1024;   // nodes per bucket (192 KB of counters)
+
+template <bool SORT>
+__global__ void __launch_bounds__(kRangeThreads, 1)
+k_range_transpose(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                  const uint64_t* __restrict__ bases, int nb, int R, int64_t N, int64_t total,
+                  int64_t* __restrict__ eoff, int32_t* __restrict__ eidx, uint32_t* __restrict__ giants,
+                  unsigned int* __restrict__ ngiant, const unsigned long long* __restrict__ err) {
+  extern __shared__ int32_t scnt[];
+  __shared__ int s_ws[kRangeThreads / 32];
+  if (err && *err != ERR_NONE) return;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  // persistent: a grid smaller than nb keeps the CTAs' random-write windows (one bucket's element
+  // ids each) inside L2
+  for (int g = blockIdx.x; g < nb; g += gridDim.x) {
+  __syncthreads();
+  const int64_t lo = (int64_t)g * R;
+  if (lo >= N) continue;
+  const int nr = (int)(lo + R < N ? R : N - lo);
+  const int64_t b0 = (int64_t)bases[g], b1 = g + 1 < nb ? (int64_t)bases[g + 1] : total;
+  for (int j = t; j < nr; j += kRangeThreads) scnt[j] = 0;
+  __syncthreads();
+  constexpr int U = 8;   // loads in flight per thread (each pass is otherwise one round trip per entry)
+  for (int64_t i0 = b0 + t; i0 < b1; i0 += (int64_t)U * kRangeThreads) {
+    uint32_t k[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + (int64_t)u * kRangeThreads;
+      k[u] = i < b1 ? __ldg(keys + i) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k[u] != 0xFFFFFFFFu) atomicAdd(&scnt[(int)(k[u] - lo)], 1);
+  }
+  __syncthreads();
+  // exclusive scan of scnt[0, nr) in place: a contiguous piece per thread + block scan of the sums
+  {
+    const int per = (nr + kRangeThreads - 1) / kRangeThreads;
+    const int j0 = t * per, j1 = j0 + per < nr ? j0 + per : nr;
+    int sum = 0;
+    for (int j = j0; j < j1; ++j) sum += scnt[j];
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_ws[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int x = s_ws[lane];
+      int xi = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, xi, o);
+        if (lane >= o) xi += y;
+      }
+      s_ws[lane] = xi - x;
+    }
+    __syncthreads();
+    int run = s_ws[warp] + incl - sum;
+    for (int j = j0; j < j1; ++j) {
+      const int c = scnt[j];
+      scnt[j] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int j = t; j < nr; j += kRangeThreads) eoff[lo + j] = b0 + scnt[j];
+  if (lo + nr == N && t == 0) eoff[N] = b1;
+  __syncthreads();
+  for (int64_t i0 = b0 + t; i0 < b1; i0 += (int64_t)U * kRangeThreads) {
+    uint32_t k[U], v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + (int64_t)u * kRangeThreads;
+      k[u] = i < b1 ? __ldg(keys + i) : 0xFFFFFFFFu;
+      v[u] = i < b1 ? __ldg(vals + i) : 0u;
+    }
+    int p[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) p[u] = k[u] != 0xFFFFFFFFu ? atomicAdd(&scnt[(int)(k[u] - lo)], 1) : -1;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (p[u] >= 0) eidx[b0 + p[u]] = (int32_t)v[u];
+  }
+  __syncthreads();   // scnt[j] = end of node j's segment; the CTA's global writes are visible to it
+  if (!SORT) continue;
+  for (int j0 = 0; j0 < nr; j0 += kRangeThreads) {
+    const int j = j0 + t;
+    const bool in = j < nr;
+    const int st = in ? (j ? scnt[j - 1] : 0) : 0;
+    const int d = in ? scnt[j] - st : 0;
+    const bool big = d > kSegMax;
+    if (big) giants[atomicAdd(ngiant, 1u)] = (uint32_t)(lo + j);
+    const int dd = big ? 0 : d;
+    const int wmax = __reduce_max_sync(FULL, (unsigned)dd);
+    if (wmax > 1) {
+      int32_t* seg = eidx + b0 + st;
+      if (wmax <= 8) sort_segment<8>(seg, dd);
+      else if (wmax <= 16) sort_segment<16>(seg, dd);
+      else sort_segment<32>(seg, dd);
+    }
+  }
   }
 }
 

@@ -184,7 +184,7 @@ def test_row_a5_exclusive_scan(n):
 # ------------------------------------------------------------------------------------------------
 # whole path vs the std::set oracle
 # ------------------------------------------------------------------------------------------------
-@pytest.fixture(params=["radix", "transpose"])
+@pytest.fixture(params=["radix", "transpose", "msd"])
 def elem_path(request):
     mn().set_elem_path(request.param)
     yield request.param
