@@ -206,8 +206,10 @@ def run_reference(args):
         return run_reference_poly(args)
     if args.config == 5:   # only the leading cell layers are ever sampled: build just those
         et, conn = meshgen.TET4, meshgen.kuhn_tets(320, cell_begin=0, cell_end=320 * 320 * 48)[0]
+        M_total, N_total = 6 * 320 ** 3, 321 ** 3
     else:
-        et, conn, _ = meshgen.make_config(args.config, device="cpu")
+        et, conn, N_total = meshgen.make_config(args.config, device="cpu")
+        M_total = int(conn.shape[0])
     conn = conn.numpy()
     # size the per-step sample for ~ (few minutes) / (steps + warmup)
     per_step = max(1.0, min(20.0, 150.0 / (args.steps + args.warmup)))
@@ -240,8 +242,9 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": meshgen.CONFIGS[args.config]["name"], "sample_elements": ms,
-                       "parallelism": "host, 1 thread"},
+            "config": {"workload": f"config {args.config}: {meshgen.CONFIGS[args.config]['desc']}",
+                       "elements": M_total, "nodes": N_total, "parallelism": "host, 1 thread (oracle)",
+                       "outputs": "node + element CSR", "sample_elements": ms},
             "cpu_baseline": {"value": v, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
@@ -253,7 +256,7 @@ def run_reference_poly(args):
     """Reference arm on a polygon workload: the oracle's polygon functions on a prefix sample."""
     import meshgen
     import oracle
-    off_t, idx_t, _ = meshgen.make_poly_config(args.config, device="cpu")
+    off_t, idx_t, N_total = meshgen.make_poly_config(args.config, device="cpu")
     off_all, idx_all = off_t.numpy(), idx_t.numpy()
     M = off_all.shape[0] - 1
     per_step = max(1.0, min(20.0, 150.0 / (args.steps + args.warmup)))
@@ -290,8 +293,10 @@ def run_reference_poly(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": meshgen.POLY_CONFIGS[args.config]["name"], "sample_elements": ms,
-                       "parallelism": "host, 1 thread"},
+            "config": {"workload": f"config {args.config}: {meshgen.POLY_CONFIGS[args.config]['desc']}",
+                       "elements": M, "nodes": int(N_total),
+                       "parallelism": "host, 1 thread (oracle)", "outputs": "node + element CSR",
+                       "sample_elements": ms},
             "cpu_baseline": {"value": v, "unit": "elements/s", "cores": 1, "kind": "oracle",
                              "sample": sample_desc},
             "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -490,7 +495,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int32" if poly else "u64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": f"config {args.config}: {info['desc']}", "elements": M_total, "nodes": N,
                        **({"conn_entries": int(conn[1].numel())} if poly else {}),
                        "parallelism": "single GPU" if world == 1 else
