@@ -1915,6 +1915,56 @@ k_pairs_scatter(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, const
   }
 }
 
+// Chunk-bucketed transpose of received (node << 32 | element) pairs (the multi-GPU finish; the
+// scheme of k_chunk_scatter_fixed / k_chunk_sort on the owner's local node ids a - lo).
+// FIXED: fixed-capacity buckets [x * cap, (x + 1) * cap), overflow -> *ovf; else (fallback, guarded
+// by *ovf) counted buckets at cbase[x] with cursors `cur`.
+template <bool FIXED>
+__global__ void __launch_bounds__(256)
+k_pairs_chunk_scatter(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, int cap,
+                      const int64_t* __restrict__ cbase, int32_t* __restrict__ cur, int32_t* __restrict__ belem,
+                      uint8_t* __restrict__ bnode, unsigned int* __restrict__ ovf) {
+  if (!FIXED && *ovf == 0u) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
+    const int64_t j = base + lane;
+    const bool in = j < n;
+    const uint64_t p = in ? pairs[j] : 0;
+    const int a = in ? (int)((int64_t)(p >> 32) - lo) : 0;
+    const int x = in ? (a >> 7) : -1;   // one shared sentinel: match cost grows with distinct values
+    const unsigned peers = __match_any_sync(FULL, x);
+    const int leader = __ffs(peers) - 1;
+    int c = 0;
+    if (in && lane == leader) {
+      c = atomicAdd(cur + x, (int)__popc(peers));
+      if (FIXED && c + (int)__popc(peers) > cap) *ovf = 1u;
+    }
+    c = __shfl_sync(FULL, c, leader) + __popc(peers & lanemask_lt());
+    if (in && (!FIXED || c < cap)) {
+      const int64_t pos = (FIXED ? (int64_t)x * cap : cbase[x]) + c;
+      belem[pos] = (int32_t)(p & 0xffffffffull);
+      bnode[pos] = (uint8_t)(a & (kChunkNodes - 1));
+    }
+  }
+}
+
+// Fallback chunk counts of received pairs (guarded by *ovf).
+__global__ void __launch_bounds__(256)
+k_pairs_chunk_count(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, int32_t* __restrict__ ccnt,
+                    const unsigned int* __restrict__ ovf) {
+  if (*ovf == 0u) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
+    const int64_t j = base + lane;
+    const bool in = j < n;
+    const int x = in ? (int)(((int64_t)(pairs[j] >> 32) - lo) >> 7) : -1;
+    const unsigned peers = __match_any_sync(FULL, x);
+    if (in && lane == __ffs(peers) - 1) atomicAdd(ccnt + x, (int)__popc(peers));
+  }
+}
+
 // Multi-GPU finish: local node key and element-id payload of every received pair.
 __global__ void __launch_bounds__(256)
 k_local_keys(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, uint32_t* __restrict__ keys,

@@ -1676,6 +1676,9 @@ static mn_status dist_finish_impl(const uint64_t* pairs, int64_t n, const int32_
     uint64_t* sstatus = ar.take<uint64_t>((size_t)tiles_of(nloc, kScanTile) + 1);
     int32_t* cnt = ar.take<int32_t>((size_t)nloc + 1);    // zeroed: counts of the transpose
     int32_t* lofs = ar.take<int32_t>((size_t)nloc + 1);   // zeroed: cursors of the transpose
+    const int64_t nch = tiles_of(nloc, kChunkNodes);
+    int32_t* ccur = ar.take<int32_t>((size_t)nch + 1);     // zeroed: fixed chunk-bucket cursors
+    unsigned int* ovf = ar.take<unsigned int>(1);          // zeroed: a fixed bucket overflowed
     const size_t head = ar.off;
     uint32_t* keys = ar.take<uint32_t>((size_t)n);
     uint32_t* temp = ar.take<uint32_t>((size_t)C * n);
@@ -1687,6 +1690,7 @@ static mn_status dist_finish_impl(const uint64_t* pairs, int64_t n, const int32_
       auto fix = [&](auto* q) { return (decltype(q))(bb + (size_t)q); };
       errw = fix(errw); smp = fix(smp); tickets = fix(tickets); ngiant = fix(ngiant); sstatus = fix(sstatus);
       keys = fix(keys); temp = fix(temp); cnt = fix(cnt); lofs = fix(lofs); giants = fix(giants);
+      ccur = fix(ccur); ovf = fix(ovf);
       uint32_t* elems = reinterpret_cast<uint32_t*>(eidx);
       MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
       MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
@@ -1701,17 +1705,38 @@ static mn_status dist_finish_impl(const uint64_t* pairs, int64_t n, const int32_
       }
       if (transpose) {
         if (nloc > 0) {
-          MN_CUDA(launch("elem_count", 8.0 * n, s, [&] { k_pairs_count<<<stream_grid(n), 256, 0, s>>>(pairs, n, lo, cnt); }));
-          MN_CUDA(launch("scan_counts", 12.0 * nloc, s, [&] {
-            k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kScanThreads, 0, s>>>(
-                cnt, nloc, eoff, sstatus, tickets + 2, 1);
+          // chunk-bucketed: the pairs into fixed-capacity 128-node chunk buckets (element ids in temp,
+          // node bytes in keys; both dead until the node pass), guarded counted fallback, chunk sort
+          int32_t* belem = reinterpret_cast<int32_t*>(temp);
+          uint8_t* bnode = reinterpret_cast<uint8_t*>(keys);
+          int64_t* cbase = noff;   // scratch until the node scan writes the node offsets
+          int64_t capl = (2 * n / nch) & ~(int64_t)31;
+          const int ovr = g_chunk_cap.load();
+          if (ovr > 0 && ovr < capl) capl = ovr;
+          if (capl > (int64_t)INT32_MAX - 4096) capl = (int64_t)INT32_MAX - 4096;
+          const int cap = (int)capl;
+          MN_CUDA(launch("elem_scatter", 8.0 * n + 5.0 * n, s, [&] {
+            k_pairs_chunk_scatter<true><<<stream_grid(n), 256, 0, s>>>(pairs, n, lo, cap, nullptr, ccur, belem,
+                                                                        bnode, ovf);
           }));
-          MN_CUDA(launch("elem_scatter", 16.0 * n, s, [&] {
-            k_pairs_scatter<<<stream_grid(n), 256, 0, s>>>(pairs, n, lo, eoff, lofs, eidx);
+          MN_CUDA(launch("scan_counts", 12.0 * nch, s, [&] {
+            k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nch, kScanTile), kScanThreads, 0, s>>>(
+                ccur, nch, cbase, sstatus, tickets + 2, 1);
           }));
-          MN_CUDA(launch("elem_segsort", 8.0 * n + 8.0 * (nloc + 1), s, [&] {
-            segsort_fn<<<(unsigned)tiles_of(nloc, kSegThreads), kSegThreads, 0, s>>>(eoff, nloc, eidx, giants,
-                                                                                      ngiant, errw);
+          MN_CUDA(launch("count_fallback", 0.0, s, [&] {
+            k_pairs_chunk_count<<<stream_grid(n), 256, 0, s>>>(pairs, n, lo, cnt, ovf);
+          }));
+          MN_CUDA(launch("scan_fallback", 0.0, s, [&] {
+            k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nch, kScanTile), kScanThreads, 0, s>>>(
+                cnt, nch, cbase, sstatus, tickets + 3, 3, ovf);
+          }));
+          MN_CUDA(launch("scatter_fallback", 0.0, s, [&] {
+            k_pairs_chunk_scatter<false><<<stream_grid(n), 256, 0, s>>>(pairs, n, lo, 0, cbase, lofs, belem, bnode,
+                                                                         ovf);
+          }));
+          MN_CUDA(launch("elem_segsort", 9.0 * n + 8.0 * (nloc + 1), s, [&] {
+            k_chunk_sort<true><<<(unsigned)nch, kChunkNodes, 0, s>>>(cbase, nloc, belem, bnode, eoff, eidx, giants,
+                                                                      ngiant, errw, ovf, cap);
           }));
           const int scap = 48 * 1024;
           cudaFuncSetAttribute(k_segsort_giant, cudaFuncAttributeMaxDynamicSharedMemorySize, scap * 4);

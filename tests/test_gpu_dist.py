@@ -83,6 +83,26 @@ def test_virtual_ranks_match_oracle(G, name, et, make, elem_path):
     assert np.array_equal(eo.cpu().numpy(), so) and np.array_equal(ei.cpu().numpy(), si)
 
 
+@pytest.mark.parametrize("cap", [32, 96])
+@pytest.mark.parametrize("G", [2, 3])
+def test_virtual_ranks_chunk_bucket_fallback(G, cap):
+    """The finish's chunk-bucketed transpose with small fixed capacities: overflowing buckets take
+    the guarded counted path; the slices still concatenate to the oracle's CSRs."""
+    import paper_1604_04689_b200 as mn
+    conn, N = meshgen.kuhn_tets(12)
+    mn.set_elem_path("transpose")
+    mn.set_chunk_cap(cap)
+    try:
+        (no, ni), (eo, ei) = _virtual_ranks(conn.cuda(), meshgen.TET4, N, G)
+    finally:
+        mn.set_chunk_cap(0)
+        mn.set_elem_path("auto")
+    ro, ri = oracle.node_csr(meshgen.TET4, conn, N)
+    so, si = oracle.elem_csr(meshgen.TET4, conn, N)
+    assert np.array_equal(no.cpu().numpy(), ro) and np.array_equal(ni.cpu().numpy(), ri)
+    assert np.array_equal(eo.cpu().numpy(), so) and np.array_equal(ei.cpu().numpy(), si)
+
+
 def test_virtual_ranks_config5_shape_small(elem_path):
     """Config 5's recipe (Kuhn, natural order) at 40^3, 8 ranks: equals the 1-GPU CSR."""
     import paper_1604_04689_b200 as mn
