@@ -683,25 +683,44 @@ __device__ __forceinline__ uint32_t pick(const int (&row)[Elem<T>::K], int idx) 
 constexpr int kSegThreads = 128;
 constexpr int kSegMax = 32;   // longer element lists are sorted by k_segsort_giant
 
-// Bitonic sorting network on NET registers (ascending); every index is a compile-time constant
-// after unrolling, so v[] stays in registers.
+constexpr int next_pow2(int n) { return n <= 1 ? 1 : 2 * next_pow2((n + 1) / 2); }
+
+// Batcher's odd-even merge sort on NET registers (ascending; NET need not be a power of two).
+// The network for P = next_pow2(NET) inputs has only "min to the lower index" comparators, so
+// +inf padding at positions >= NET stays there and every comparator touching those positions is a
+// no-op: dropping them sorts NET values (24: 123 comparators vs 191 for 32; 32 vs bitonic: 191 vs
+// 240).  Every index is a compile-time constant after unrolling, so v[] stays in registers.
+struct CmpNet {
+  int n;
+  unsigned char a[256], b[256];
+};
+template <int NET>
+constexpr CmpNet make_oem() {
+  CmpNet t{};
+  constexpr int P = next_pow2(NET);
+  for (int p = 1; p < P; p <<= 1)
+    for (int k = p; k >= 1; k >>= 1)
+      for (int j = k % p; j + k < P; j += 2 * k)
+        for (int i = 0; i < k; ++i) {
+          const int a = i + j, b = i + j + k;
+          if (b < NET && a / (2 * p) == b / (2 * p)) {
+            t.a[t.n] = (unsigned char)a;
+            t.b[t.n] = (unsigned char)b;
+            ++t.n;
+          }
+        }
+  return t;
+}
+
 template <int NET>
 __device__ __forceinline__ void oddeven_sort(int32_t (&v)[NET]) {
+  constexpr CmpNet T = make_oem<NET>();
+  static_assert(T.n <= 256, "network too large");
 #pragma unroll
-  for (int k = 2; k <= NET; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-#pragma unroll
-      for (int i = 0; i < NET; ++i) {
-        const int l = i ^ j;
-        if (l > i) {
-          const int32_t a = v[i], b = v[l];
-          const bool asc = (i & k) == 0;
-          v[i] = asc ? min(a, b) : max(a, b);
-          v[l] = asc ? max(a, b) : min(a, b);
-        }
-      }
-    }
+  for (int c = 0; c < T.n; ++c) {
+    const int32_t x = v[T.a[c]], y = v[T.b[c]];
+    v[T.a[c]] = min(x, y);
+    v[T.b[c]] = max(x, y);
   }
 }
 
@@ -892,6 +911,7 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
   const int lmax = __reduce_max_sync(__activemask(), (unsigned)L);
   if (lmax <= 8) sort_small<8, HS>(tab, t, L, out);
   else if (lmax <= 16) sort_small<16, HS>(tab, t, L, out);
+  else if (lmax <= 24) sort_small<24, HS>(tab, t, L, out);
   else if (lmax <= 32) sort_small<32, HS>(tab, t, L, out);
   else {
     for (int i = 1; i < L; ++i) {
@@ -1197,6 +1217,7 @@ k_elem_segsort(const int64_t* __restrict__ eoff, int64_t N, int32_t* __restrict_
   if (wmax > 1) {
     if (wmax <= 8) sort_segment<8>(seg, dd);
     else if (wmax <= 16) sort_segment<16>(seg, dd);
+    else if (wmax <= 24) sort_segment<24>(seg, dd);
     else sort_segment<32>(seg, dd);
   }
   if (staged) {
@@ -1480,6 +1501,7 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
     if (wmax > 1) {
       if (wmax <= 8) sort_slot_column<8>(slots, t, dd);
       else if (wmax <= 16) sort_slot_column<16>(slots, t, dd);
+      else if (wmax <= 24) sort_slot_column<24>(slots, t, dd);
       else sort_slot_column<32>(slots, t, dd);
     }
     __syncthreads();
@@ -1522,6 +1544,7 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
     int32_t* seg = eidx + b0 + excl;
     if (wmax <= 8) sort_segment<8>(seg, dd);
     else if (wmax <= 16) sort_segment<16>(seg, dd);
+    else if (wmax <= 24) sort_segment<24>(seg, dd);
     else sort_segment<32>(seg, dd);
   }
 }
@@ -1636,6 +1659,7 @@ k_range_transpose(const uint32_t* __restrict__ keys, const uint32_t* __restrict_
       int32_t* seg = eidx + b0 + st;
       if (wmax <= 8) sort_segment<8>(seg, dd);
       else if (wmax <= 16) sort_segment<16>(seg, dd);
+      else if (wmax <= 24) sort_segment<24>(seg, dd);
       else sort_segment<32>(seg, dd);
     }
   }
