@@ -1239,7 +1239,14 @@ k_elem_segsort(const int64_t* __restrict__ eoff, int64_t N, int32_t* __restrict_
 //                    node's list sorted in registers (warp-uniform network), element CSR range and
 //                    the chunk's offsets written coalesced; lists > kSegMax go to k_segsort_giant
 // ------------------------------------------------------------------------------------------------
-constexpr int kChunkNodes = 128;
+#ifndef MN_CHUNK_SHIFT
+#define MN_CHUNK_SHIFT 7
+#endif
+// log2 of the nodes per chunk (local node ids fit a byte).  256-node chunks (-DMN_CHUNK_SHIFT=8),
+// config 5: scatter 2.12 vs 2.15 ms, chunk sort 2.53 vs 2.37 -> 128 kept
+constexpr int kChunkShift = MN_CHUNK_SHIFT;
+constexpr int kChunkNodes = 1 << kChunkShift;
+static_assert(kChunkNodes <= 256, "local node ids are bytes");
 constexpr int kChunkCap = 4096;   // bucket entries staged in shared memory (Kuhn tets: 3072)
 
 // RANGE: only nodes of [lo, hi) (the memory-bounded mode); compiled out of the whole-path kernels
@@ -1277,7 +1284,7 @@ k_chunk_count(const int32_t* __restrict__ conn, int64_t M, int64_t N, int32_t* _
 #pragma unroll
     for (int p = 0; p < K; ++p) {   // only nodes of [lo, hi) (the memory-bounded mode's range)
       const bool mine = ok && (!RANGE || (v[p] >= lo && v[p] < hi));
-      const int x = mine ? (RANGE ? (int)((v[p] - lo) >> 7) : (v[p] >> 7)) : -1;   // one shared sentinel
+      const int x = mine ? (RANGE ? (int)((v[p] - lo) >> kChunkShift) : (v[p] >> kChunkShift)) : -1;   // one shared sentinel
       const unsigned peers = __match_any_sync(FULL, x);   // (match cost grows with distinct values)
       if (mine && lane == __ffs(peers) - 1) atomicAdd(ccnt + x, (int)__popc(peers));
     }
@@ -1303,7 +1310,7 @@ k_chunk_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __re
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       const bool mine = in && (!RANGE || (v[p] >= lo && v[p] < hi));
-      const int x = mine ? (RANGE ? (int)((v[p] - lo) >> 7) : (v[p] >> 7)) : -1;   // one shared sentinel
+      const int x = mine ? (RANGE ? (int)((v[p] - lo) >> kChunkShift) : (v[p] >> kChunkShift)) : -1;   // one shared sentinel
       const unsigned peers = __match_any_sync(FULL, x);
       const int leader = __ffs(peers) - 1;
       int b = 0;
@@ -1367,7 +1374,7 @@ k_chunk_scatter_fixed(const int32_t* __restrict__ conn, int64_t M, int64_t N, in
     unsigned peers[K];
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      x[p] = ok ? (v[p] >> 7) : -1;   // one shared sentinel (match cost grows with distinct values)
+      x[p] = ok ? (v[p] >> kChunkShift) : -1;   // one shared sentinel (match cost grows with distinct values)
       peers[p] = __match_any_sync(FULL, x[p]);
       b[p] = 0;
       if (ok && lane == __ffs(peers[p]) - 1) b[p] = atomicAdd(ccur + x[p], (int)__popc(peers[p]));
@@ -1407,7 +1414,7 @@ __device__ __forceinline__ void sort_slot_column(int32_t* slots, int t, int d) {
     if (i < d) slots[i * kSlotPitch + t] = v[i];
 }
 
-template <bool SORT, int MINB = 8>
+template <bool SORT, int MINB = 1024 / kChunkNodes>
 __global__ void __launch_bounds__(kChunkNodes, MINB)
 k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __restrict__ belem,
               const uint8_t* __restrict__ bnode, int64_t* __restrict__ eoff, int32_t* __restrict__ eidx,
@@ -1956,7 +1963,7 @@ k_pairs_chunk_scatter(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo,
     const bool in = j < n;
     const uint64_t p = in ? pairs[j] : 0;
     const int a = in ? (int)((int64_t)(p >> 32) - lo) : 0;
-    const int x = in ? (a >> 7) : -1;   // one shared sentinel: match cost grows with distinct values
+    const int x = in ? (a >> kChunkShift) : -1;   // one shared sentinel: match cost grows with distinct values
     const unsigned peers = __match_any_sync(FULL, x);
     const int leader = __ffs(peers) - 1;
     int c = 0;
@@ -1983,7 +1990,7 @@ k_pairs_chunk_count(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, i
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
     const int64_t j = base + lane;
     const bool in = j < n;
-    const int x = in ? (int)(((int64_t)(pairs[j] >> 32) - lo) >> 7) : -1;
+    const int x = in ? (int)(((int64_t)(pairs[j] >> 32) - lo) >> kChunkShift) : -1;
     const unsigned peers = __match_any_sync(FULL, x);
     if (in && lane == __ffs(peers) - 1) atomicAdd(ccnt + x, (int)__popc(peers));
   }

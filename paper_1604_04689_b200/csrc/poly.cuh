@@ -149,7 +149,7 @@ k_poly_chunk_scatter(const int64_t* __restrict__ off, const int32_t* __restrict_
     for (int p = 0; p < kmax; ++p) {
       const bool mine = p < k;
       const int v = mine ? idx[b + p] : 0;
-      const int x = mine ? (v >> 7) : -1;   // one shared sentinel: match cost grows with distinct values
+      const int x = mine ? (v >> kChunkShift) : -1;   // one shared sentinel: match cost grows with distinct values
       const unsigned peers = __match_any_sync(FULL, x);
       const int leader = __ffs(peers) - 1;
       int c = 0;
@@ -183,7 +183,7 @@ k_poly_chunk_count(const int64_t* __restrict__ off, const int32_t* __restrict__ 
     const int kmax = (int)__reduce_max_sync(FULL, (unsigned)k);
     for (int p = 0; p < kmax; ++p) {
       const bool mine = p < k;
-      const int x = mine ? (idx[b + p] >> 7) : -1;
+      const int x = mine ? (idx[b + p] >> kChunkShift) : -1;
       const unsigned peers = __match_any_sync(FULL, x);
       if (mine && lane == __ffs(peers) - 1) atomicAdd(ccnt + x, (int)__popc(peers));
     }
