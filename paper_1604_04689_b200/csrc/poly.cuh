@@ -238,23 +238,61 @@ k_poly_gather(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx
 #pragma unroll
     for (int i = 0; i < HS; ++i) tab[i][t] = EMPTY;
     const int64_t s0 = eoff[a], s1 = eoff[a + 1];
-    for (int64_t i = s0; i < s1 && L <= MU; ++i) {
-      const int32_t e = eidx[i];
-      const int64_t b = off[e];
-      poly_candidates<SHARED>(idx + b, (int)(off[e + 1] - b), (int32_t)a, [&](uint32_t v) {
-        uint32_t h = (v * 0x9E3779B1u) >> (32 - HB);
-        while (L <= MU) {
-          const uint32_t x = tab[h][t];
-          if (x == v) break;
-          if (x == EMPTY) {
-            tab[h][t] = v;
-            used |= 1u << h;
-            ++L;
-            break;
-          }
-          h = (h + 1) & (HS - 1);
+    auto insert = [&](uint32_t v) {
+      uint32_t h = (v * 0x9E3779B1u) >> (32 - HB);
+      while (L <= MU) {
+        const uint32_t x = tab[h][t];
+        if (x == v) break;
+        if (x == EMPTY) {
+          tab[h][t] = v;
+          used |= 1u << h;
+          ++L;
+          break;
         }
-      });
+        h = (h + 1) & (HS - 1);
+      }
+    };
+    if (SHARED) {
+      for (int64_t i = s0; i < s1 && L <= MU; ++i) {
+        const int32_t e = eidx[i];
+        const int64_t b = off[e];
+        poly_candidates<SHARED>(idx + b, (int)(off[e + 1] - b), (int32_t)a, insert);
+      }
+    } else {
+      // ring-edge candidates, B incidences in flight: element ids, ring bounds and the first four
+      // ring entries are independent loads; rings of arity <= 4 are resolved in registers
+      constexpr int B = 4;
+      for (int64_t i0 = s0; i0 < s1 && L <= MU; i0 += B) {
+        int32_t e[B];
+#pragma unroll
+        for (int q = 0; q < B; ++q) e[q] = i0 + q < s1 ? __ldg(eidx + i0 + q) : -1;
+        int64_t rb[B];
+        int rk[B];
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+          rb[q] = e[q] >= 0 ? __ldg(off + e[q]) : 0;
+          rk[q] = e[q] >= 0 ? (int)(__ldg(off + e[q] + 1) - rb[q]) : 0;
+        }
+        int32_t r[B][4];
+#pragma unroll
+        for (int q = 0; q < B; ++q)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) r[q][j] = j < rk[q] ? __ldg(idx + rb[q] + j) : -1;
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+          if (e[q] < 0) continue;
+          const int k = rk[q];
+          if (k <= 4) {
+            const int32_t* x = r[q];
+            const int p = x[0] == (int32_t)a ? 0 : x[1] == (int32_t)a ? 1 : x[2] == (int32_t)a ? 2 : 3;
+            const int pp = p == 0 ? k - 1 : p - 1, pn = p == k - 1 ? 0 : p + 1;
+            insert((uint32_t)(pp == 0 ? x[0] : pp == 1 ? x[1] : pp == 2 ? x[2] : x[3]));
+            insert((uint32_t)(pn == 0 ? x[0] : pn == 1 ? x[1] : pn == 2 ? x[2] : x[3]));
+          } else {
+            poly_candidates<false>(idx + rb[q], k, (int32_t)a, insert);
+          }
+        }
+      }
     }
   }
   const bool giant = valid && L > MU;
