@@ -617,13 +617,21 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       if (ovr > 0 && ovr < capl) capl = ovr;
       if (capl > (int64_t)INT32_MAX - 4096) capl = (int64_t)INT32_MAX - 4096;
       const int cap = (int)capl;
+      // one resident wave (grid-stride): the occupancy of this instantiation x the SM count
+      static int fixed_wave = 0;
+      if (!fixed_wave) {
+        int occ = 0, dev = 0, sms = 148;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chunk_scatter_fixed<T, true>, 256, 0);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        fixed_wave = (occ > 0 ? occ : 4) * sms;
+      }
+      const int fgrid = (int)std::min<int64_t>(fixed_wave, (P.M + 255) / 256 > 0 ? (P.M + 255) / 256 : 1);
       MN_CUDA(launch("elem_scatter", 4.0 * P.K * P.M + 5.0 * P.Pe, s, [&] {
         if (aligned)
-          k_chunk_scatter_fixed<T, true><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, cap, ccur, belem, bnode,
-                                                                         errw, ovf);
+          k_chunk_scatter_fixed<T, true><<<fgrid, 256, 0, s>>>(conn, P.M, P.N, cap, ccur, belem, bnode, errw, ovf);
         else
-          k_chunk_scatter_fixed<T, false><<<hist_grid(P.M), 256, 0, s>>>(conn, P.M, P.N, cap, ccur, belem, bnode,
-                                                                          errw, ovf);
+          k_chunk_scatter_fixed<T, false><<<fgrid, 256, 0, s>>>(conn, P.M, P.N, cap, ccur, belem, bnode, errw, ovf);
       }));
       if (nchunks > 0)
         MN_CUDA(launch("scan_counts", 12.0 * nchunks, s, [&] {
