@@ -2020,6 +2020,11 @@ mn_status mn_workspace_bytes(mn_elem_type t, int64_t M, int64_t N, int modes, si
   a.take<int32_t>(nch + 1);
   a.take<int32_t>(nch + 1);
   a.take<unsigned int>(1);
+  if (g_elem_path.load() == 3) {   // MSD element path (forced only): range histogram, status, bases
+    a.take<unsigned long long>(kMsdBins);
+    a.take<uint64_t>((size_t)(tiles_of(P.Pe, kTile) ? tiles_of(P.Pe, kTile) : 1) * kMsdBins);
+    a.take<uint64_t>(kMsdBins);
+  }
   a.take<uint32_t>((size_t)P.N + 1);
   a.take<int64_t>(nch + 1);
   for (int i = 0; i < 4; ++i) a.take<uint32_t>((size_t)P.Pe);
