@@ -660,12 +660,11 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       }));
       if (nchunks > 0)
         MN_CUDA(launch("elem_segsort", 9.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
-          if (want_elem)
-            k_chunk_sort<true><<<(unsigned)nchunks, kChunkNodes, 0, s>>>(cbase, P.N, belem, bnode, eoff, eidx,
-                                                                          sgiants, nsgiant, errw, ovf, cap);
-          else
-            k_chunk_sort<false><<<(unsigned)nchunks, kChunkNodes, 0, s>>>(cbase, P.N, belem, bnode, eoff, eidx,
-                                                                           sgiants, nsgiant, errw, ovf, cap);
+          // sorted even for node-only calls: the gather then visits each node's element rows in
+          // ascending order (L1 reuse; config 5 element-sharing CSR: gather 5.38 -> 4.13 ms for
+          // +0.77 ms of sorting, step 10.28 -> 9.78 ms)
+          k_chunk_sort<true><<<(unsigned)nchunks, kChunkNodes, 0, s>>>(cbase, P.N, belem, bnode, eoff, eidx,
+                                                                        sgiants, nsgiant, errw, ovf, cap);
         }));
       if (want_elem)
         MN_CUDA(launch("segsort_giant", 0.0, s, [&] {
@@ -1260,12 +1259,9 @@ static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, in
                                                                errw, ovf);
     }));
     MN_CUDA(launch("elem_segsort", 9.0 * L + 8.0 * (N + 1), s, [&] {
-      if (we)   // element lists sorted (R3); for the node adjacency alone the grouping suffices
-        k_chunk_sort<true><<<(unsigned)nch, kChunkNodes, 0, s>>>(cbase, N, belem, bnode, eoff, eidx, sgiants,
-                                                                  nsgiant, errw, ovf, ccap);
-      else
-        k_chunk_sort<false><<<(unsigned)nch, kChunkNodes, 0, s>>>(cbase, N, belem, bnode, eoff, eidx, sgiants,
-                                                                   nsgiant, errw, ovf, ccap);
+      // element lists sorted (R3), also for node-only calls (ascending row visits in the gather)
+      k_chunk_sort<true><<<(unsigned)nch, kChunkNodes, 0, s>>>(cbase, N, belem, bnode, eoff, eidx, sgiants,
+                                                                nsgiant, errw, ovf, ccap);
     }));
   } else if (M == 0) {
     MN_CUDA(cudaMemsetAsync(eoff, 0, (size_t)(N + 1) * 8, s));
