@@ -705,7 +705,6 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       static bool rattr = false;
       if (!rattr) {
         cudaFuncSetAttribute(k_range_transpose<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeMax * 4);
-        cudaFuncSetAttribute(k_range_transpose<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeMax * 4);
         rattr = true;
       }
       // persistent grid of 96 CTAs (one per SM at most): their random-write windows (one bucket's
@@ -713,12 +712,9 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       // 148, 2.67 with 96, 3.00 with 64, 4.65 with 40.
       const unsigned rgrid = 96;
       MN_CUDA(launch("range_transpose", 8.0 * P.Pe + 4.0 * P.Pe + 8.0 * (P.N + 1), s, [&] {
-        if (want_elem)
-          k_range_transpose<true><<<rgrid, kRangeThreads, rsm, s>>>(ekA, epA, mbases, kMsdBins, (int)msd_R, P.N,
-                                                                       P.Pe, eoff, eidx, sgiants, nsgiant, errw);
-        else
-          k_range_transpose<false><<<rgrid, kRangeThreads, rsm, s>>>(ekA, epA, mbases, kMsdBins, (int)msd_R, P.N,
-                                                                        P.Pe, eoff, eidx, sgiants, nsgiant, errw);
+        // sorted also for node-only calls (ascending element-row visits in the gather)
+        k_range_transpose<true><<<rgrid, kRangeThreads, rsm, s>>>(ekA, epA, mbases, kMsdBins, (int)msd_R, P.N,
+                                                                     P.Pe, eoff, eidx, sgiants, nsgiant, errw);
       }));
       if (want_elem)
         MN_CUDA(launch("segsort_giant", 0.0, s, [&] {
