@@ -1084,12 +1084,11 @@ k_node_compact(const int64_t* __restrict__ eoff, int C, const uint32_t* __restri
 // Element CSR as a counting-sort transpose, used when the mesh numbering has
 // locality: the element CSR is the transpose of the incidence matrix B.
 //   k_locality_sample  distinct (slot, node) groups per warp window of 32 consecutive elements
-//   k_elem_count       validation + per-node incidence counts, one atomic per group of lanes that
-//                      hold the same node in the same local slot (__match_any_sync aggregation)
-//   k_elem_scatter     each group reserves its slots with one returning atomic, lanes write their
-//                      element ids (order inside a node is arbitrary here)
-//   k_elem_segsort     per-node insertion sort restores ascending element ids (canonical, R3)
+//                      (chooses the transpose; the transpose itself is the chunk-bucketed one below)
+//   k_elem_segsort     per-node register sort of element-id segments (the polygon sharing path)
 //   k_segsort_giant    block bitonic sort for segments longer than kSegMax
+// (the per-node count / scatter kernels this path started with -- 7.1 ms on config 5 against
+// 4.6 ms for the chunk buckets -- were removed once every mode moved to the chunk buckets)
 // ================================================================================================
 template <int T, bool ALIGNED>
 __global__ void __launch_bounds__(256)
@@ -1118,70 +1117,7 @@ k_locality_sample(const int32_t* __restrict__ conn, int64_t M, unsigned long lon
   }
 }
 
-template <int T, bool ALIGNED>
-__global__ void __launch_bounds__(256)
-k_elem_count(const int32_t* __restrict__ conn, int64_t M, int64_t N, int32_t* __restrict__ cnt,
-             unsigned long long* __restrict__ err, int64_t lo = 0, int64_t hi = INT64_MAX) {
-  constexpr int K = Elem<T>::K;
-  const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < M; base += stride) {
-    const int64_t e = base + lane;
-    const bool in = e < M;
-    int v[K];
-    if (in) load_row<T, ALIGNED>(conn, e, v);
-    int bad = -1, kind = 0;
-    if (in) {
-#pragma unroll
-      for (int p = K - 1; p >= 0; --p)
-        if (v[p] < 0 || (int64_t)v[p] >= N) bad = p;
-      if (bad < 0) {
-#pragma unroll
-        for (int p = K - 1; p >= 1; --p) {
-          bool dup = false;
-#pragma unroll
-          for (int q = 0; q < p; ++q) dup |= (v[q] == v[p]);
-          if (dup) { bad = p; kind = 1; }
-        }
-      }
-      if (bad >= 0) atomicMin(err, (unsigned long long)err_encode((uint64_t)e, kind, bad));
-    }
-    const bool ok = in && bad < 0;
-    if (ok) {
-#pragma unroll
-      for (int p = 0; p < K; ++p)   // fire-and-forget RED; only nodes of the range [lo, hi)
-        if (v[p] >= lo && v[p] < hi) atomicAdd(cnt + (v[p] - lo), 1);
-    }
-  }
-}
 
-template <int T, bool ALIGNED>
-__global__ void __launch_bounds__(256)
-k_elem_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __restrict__ eoff,
-               int32_t* __restrict__ cursor, int32_t* __restrict__ eidx, const unsigned long long* __restrict__ err,
-               int64_t lo = 0, int64_t hi = INT64_MAX) {
-  constexpr int K = Elem<T>::K;
-  if (*err != ERR_NONE) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < M; base += stride) {
-    const int64_t e = base + lane;
-    const bool in = e < M;
-    int v[K];
-    if (in) load_row<T, ALIGNED>(conn, e, v);
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const bool mine = in && v[p] >= lo && v[p] < hi;
-      const int x = mine ? (int)(v[p] - lo) : -1;   // one shared sentinel: match cost grows with distinct values
-      const unsigned peers = __match_any_sync(FULL, x);
-      const int leader = __ffs(peers) - 1;
-      int b = 0;
-      if (mine && lane == leader) b = atomicAdd(cursor + x, (int)__popc(peers));
-      b = __shfl_sync(FULL, b, leader);
-      if (mine) eidx[eoff[x] + b + __popc(peers & lanemask_lt())] = (int32_t)e;
-    }
-  }
-}
 
 
 constexpr int kSegSmem = 8192;   // elements of a 128-node chunk staged in shared memory
@@ -1921,30 +1857,7 @@ k_pairs_locality(const uint64_t* __restrict__ pairs, int64_t n, unsigned long lo
   }
 }
 
-__global__ void __launch_bounds__(256)
-k_pairs_count(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, int32_t* __restrict__ cnt) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(cnt + ((int64_t)(pairs[j] >> 32) - lo), 1);
-}
 
-__global__ void __launch_bounds__(256)
-k_pairs_scatter(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, const int64_t* __restrict__ eoff,
-                int32_t* __restrict__ cursor, int32_t* __restrict__ eidx) {
-  const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
-    const int64_t j = base + lane;
-    const bool in = j < n;
-    const uint64_t p = in ? pairs[j] : 0;
-    const int64_t a = in ? (int64_t)(p >> 32) - lo : -1;   // one shared sentinel: match cost grows with distinct values
-    const unsigned peers = __match_any_sync(FULL, (unsigned long long)a);
-    const int leader = __ffs(peers) - 1;
-    int b = 0;
-    if (in && lane == leader) b = atomicAdd(cursor + a, (int)__popc(peers));
-    b = __shfl_sync(FULL, b, leader);
-    if (in) eidx[eoff[a] + b + __popc(peers & lanemask_lt())] = (int32_t)(p & 0xffffffffull);
-  }
-}
 
 // Chunk-bucketed transpose of received (node << 32 | element) pairs (the multi-GPU finish; the
 // scheme of k_chunk_scatter_fixed / k_chunk_sort on the owner's local node ids a - lo).
