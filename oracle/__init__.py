@@ -31,7 +31,7 @@ OK, ERR_ARG, ERR_RANGE, ERR_DEGENERATE, ERR_ARITY = 0, 1, 2, 3, 4
 def build(force: bool = False) -> str:
     """Compile oracle.cpp with plain g++ (no CUDA)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", _SRC, "-o", _SO])
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-pthread", _SRC, "-o", _SO])
     return _SO
 
 
@@ -59,6 +59,12 @@ def _load():
         lib.oracle_poly_csr.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                         ctypes.c_int64, pp64, pp32, p64, p64, p32]
         lib.oracle_poly_csr.restype = ctypes.c_int
+        lib.oracle_csr_range.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                         ctypes.c_int64, ctypes.c_int64, pp64, pp32, p64, p64, p32]
+        lib.oracle_csr_range.restype = ctypes.c_int
+        lib.oracle_csr_mt.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                      ctypes.c_int, pp64, pp32, p64, p64, p32, p32]
+        lib.oracle_csr_mt.restype = ctypes.c_int
         lib.oracle_free.argtypes = [ctypes.c_void_p]
         lib.oracle_free.restype = None
         _lib = lib
@@ -121,6 +127,64 @@ def node_shared_csr(etype: int, conn, num_nodes: int):
 def elem_csr(etype: int, conn, num_nodes: int):
     """One-ring neighbouring elements of every vertex as CSR (int64 offsets, int32 indices)."""
     return _csr(_load().oracle_elem_csr, etype, conn, num_nodes)
+
+
+# ---- node-range mode (SURVEY §8(c)): the same loops restricted to vertices [lo, hi) -----------------
+NODE, ELEM, SHARED = 0, 1, 2
+
+
+def _take(off, idx, nnz, rows):
+    offsets = np.ctypeslib.as_array(off, shape=(rows + 1,)).copy()
+    indices = (np.ctypeslib.as_array(idx, shape=(nnz,)).copy() if nnz else np.zeros(0, np.int32))
+    lib = _load()
+    lib.oracle_free(ctypes.cast(off, ctypes.c_void_p))
+    lib.oracle_free(ctypes.cast(idx, ctypes.c_void_p))
+    return offsets, indices
+
+
+def csr_range(mode: int, etype: int, conn, num_nodes: int, lo: int, hi: int):
+    """CSR slice of vertices [lo, hi): offsets relative to the slice (hi - lo + 1 entries), indices.
+    mode NODE (edge adjacency), ELEM (incidence) or SHARED (element-sharing adjacency)."""
+    lib = _load()
+    c = _as_conn(conn)
+    M = c.shape[0] if c.size else 0
+    off = ctypes.POINTER(ctypes.c_int64)()
+    idx = ctypes.POINTER(ctypes.c_int32)()
+    nnz = ctypes.c_int64(0)
+    ee, ep = ctypes.c_int64(-1), ctypes.c_int32(-1)
+    rc = lib.oracle_csr_range(mode, etype, c.ctypes.data, M, num_nodes, lo, hi, ctypes.byref(off),
+                              ctypes.byref(idx), ctypes.byref(nnz), ctypes.byref(ee), ctypes.byref(ep))
+    if rc != OK:
+        raise OracleMeshError(rc, ee.value, ep.value)
+    return _take(off, idx, nnz.value, hi - lo)
+
+
+def csr_mt(mode: int, etype: int, conn, num_nodes: int, threads: int):
+    """Whole CSR from ``threads`` threads, thread t owning vertices [t*N/T, (t+1)*N/T) and scanning
+    every element.  -> (offsets, indices, threads actually used)."""
+    lib = _load()
+    c = _as_conn(conn)
+    M = c.shape[0] if c.size else 0
+    off = ctypes.POINTER(ctypes.c_int64)()
+    idx = ctypes.POINTER(ctypes.c_int32)()
+    nnz = ctypes.c_int64(0)
+    ee, ep = ctypes.c_int64(-1), ctypes.c_int32(-1)
+    used = ctypes.c_int32(0)
+    rc = lib.oracle_csr_mt(mode, etype, c.ctypes.data, M, num_nodes, int(threads), ctypes.byref(off),
+                           ctypes.byref(idx), ctypes.byref(nnz), ctypes.byref(ee), ctypes.byref(ep),
+                           ctypes.byref(used))
+    if rc != OK:
+        raise OracleMeshError(rc, ee.value, ep.value)
+    o, i = _take(off, idx, nnz.value, num_nodes)
+    return o, i, used.value
+
+
+def host_threads() -> int:
+    """Host cores this process may run on (the T of the all-core oracle)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
 
 
 # ---- polygon / mixed-arity meshes: (off int64[M+1], idx int32[off[M]]), ring edges ----

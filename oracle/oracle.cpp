@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <set>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -190,6 +191,111 @@ int oracle_poly_csr(int mode, const int64_t* off, const int32_t* idx, int64_t M,
     }
   }
   flatten(S, N, offsets, indices, nnz);
+  return OK;
+}
+
+// ---- node-range mode ("an optional T-thread mode where thread t owns node range t
+// and scans all elements; the output is identical") ----
+// The same two loops as oracle_node_csr / oracle_elem_csr, restricted to the vertices v with
+// lo <= v < hi: every element is still visited in ascending order, and a pair / incidence is kept
+// only when its first node lies in the range.  The slice's offsets are relative to its first
+// entry (offsets[0] = 0, hi - lo + 1 entries).  Validation is the caller's (it is global).
+namespace {
+
+struct Slice {
+  int64_t* off = nullptr;
+  int32_t* idx = nullptr;
+  int64_t nnz = 0;
+};
+
+// mode 0: edge node adjacency; 1: element incidence; 2: element-sharing node adjacency
+void range_csr(int mode, int etype, const int32_t* conn, int64_t M, int64_t lo, int64_t hi, Slice* out) {
+  const EdgeTable& t = kTables[etype];
+  const int k = t.arity;
+  const int64_t R = hi - lo;
+  if (mode == 1) {
+    std::vector<std::vector<int32_t>> L((size_t)R);
+    for (int64_t e = 0; e < M; ++e)
+      for (int p = 0; p < k; ++p) {
+        const int64_t n = conn[e * k + p];
+        if (n >= lo && n < hi) L[(size_t)(n - lo)].push_back((int32_t)e);
+      }
+    flatten(L, R, &out->off, &out->idx, &out->nnz);
+    return;
+  }
+  std::vector<std::set<int32_t>> S((size_t)R);
+  for (int64_t e = 0; e < M; ++e) {
+    const int32_t* row = conn + e * k;
+    if (mode == 0) {
+      for (int j = 0; j < t.nedges; ++j) {
+        const int32_t a = row[t.a[j]], b = row[t.b[j]];
+        if (a >= lo && a < hi) S[(size_t)(a - lo)].insert(b);
+        if (b >= lo && b < hi) S[(size_t)(b - lo)].insert(a);
+      }
+    } else {
+      for (int i = 0; i < k; ++i)
+        if (row[i] >= lo && row[i] < hi)
+          for (int j = 0; j < k; ++j)
+            if (i != j) S[(size_t)(row[i] - lo)].insert(row[j]);
+    }
+  }
+  flatten(S, R, &out->off, &out->idx, &out->nnz);
+}
+
+}  // namespace
+
+// The CSR slice of vertices [lo, hi) (0 <= lo <= hi <= N), after validating the whole mesh.
+int oracle_csr_range(int mode, int etype, const int32_t* conn, int64_t M, int64_t N, int64_t lo, int64_t hi,
+                     int64_t** offsets, int32_t** indices, int64_t* nnz, int64_t* err_elem, int32_t* err_pos) {
+  if (mode < 0 || mode > 2 || lo < 0 || hi < lo || hi > N) return ERR_ARG;
+  int rc = oracle_validate(etype, conn, M, N, err_elem, err_pos);
+  if (rc != OK) return rc;
+  Slice s;
+  range_csr(mode, etype, conn, M, lo, hi, &s);
+  *offsets = s.off;
+  *indices = s.idx;
+  *nnz = s.nnz;
+  return OK;
+}
+
+// T threads: thread t owns vertices [t*N/T, (t+1)*N/T) and scans all elements; the slices are
+// concatenated in t order, shifting each slice's offsets by the nnz before it.  Identical to the
+// one-thread oracle by construction (each vertex's list is built by exactly one thread from the
+// same ascending element scan).  *threads_used reports T after clamping to [1, max(N, 1)].
+int oracle_csr_mt(int mode, int etype, const int32_t* conn, int64_t M, int64_t N, int T, int64_t** offsets,
+                  int32_t** indices, int64_t* nnz, int64_t* err_elem, int32_t* err_pos, int* threads_used) {
+  if (mode < 0 || mode > 2) return ERR_ARG;
+  int rc = oracle_validate(etype, conn, M, N, err_elem, err_pos);
+  if (rc != OK) return rc;
+  if (T < 1) T = 1;
+  if ((int64_t)T > N && N > 0) T = (int)N;
+  if (threads_used) *threads_used = T;
+  std::vector<Slice> slices((size_t)T);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t) {
+    const int64_t lo = N * t / T, hi = N * (t + 1) / T;
+    pool.emplace_back(range_csr, mode, etype, conn, M, lo, hi, &slices[(size_t)t]);
+  }
+  for (auto& th : pool) th.join();
+  int64_t total = 0;
+  for (const Slice& s : slices) total += s.nnz;
+  int64_t* off = (int64_t*)std::malloc(sizeof(int64_t) * (size_t)(N + 1));
+  int32_t* idx = (int32_t*)std::malloc(sizeof(int32_t) * (size_t)(total > 0 ? total : 1));
+  off[0] = 0;
+  int64_t v = 0, base = 0;
+  for (int t = 0; t < T; ++t) {
+    const Slice& s = slices[(size_t)t];
+    const int64_t R = N * (t + 1) / T - N * t / T;
+    for (int64_t i = 0; i < R; ++i) off[v + i + 1] = base + s.off[i + 1];
+    if (s.nnz) std::memcpy(idx + base, s.idx, sizeof(int32_t) * (size_t)s.nnz);
+    v += R;
+    base += s.nnz;
+    std::free(s.off);
+    std::free(s.idx);
+  }
+  *offsets = off;
+  *indices = idx;
+  *nnz = total;
   return OK;
 }
 
