@@ -43,7 +43,8 @@ def parse():
                     help="memory-bounded mode (SURVEY §8(f) row 4): node ranges whose workspace fits this budget")
     ap.add_argument("--elem-path", default="auto", choices=["auto", "radix", "transpose"],
                     help="element-CSR algorithm (auto = locality test; see DESIGN.md §3.5)")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
+    ap.add_argument("--cpu-seconds", type=float, default=16.0, help="target oracle sample time")
+    ap.add_argument("--no-parity", action="store_true", help="skip the pre-timing parity gate (profiling only)")
     return ap.parse_args()
 
 
@@ -145,13 +146,29 @@ def workload(cfg, rank, world, device):
     return et, conn, 0, M, N, info
 
 
-def oracle_sample(conn_full_dev, et, target_s, k_layers_hint=None, outputs="both"):
-    """Time the oracle (std::set serial baseline, 1 thread) on a bounded prefix of the workload:
-    the first Ms elements with N trimmed to the largest node id + 1.  Returns (elements/s,
-    description, seconds)."""
+def oracle_sample(conn_full_dev, et, target_s, k_layers_hint=None, outputs="both", threads=1):
+    """Time the oracle (std::set serial baseline; with threads > 1 its T-thread node-range mode,
+    SURVEY §8(c)) on a bounded prefix of the workload: the first Ms elements with N trimmed to the
+    largest node id + 1.  Returns (elements/s, description, seconds, Ms)."""
     import numpy as np
 
     import oracle
+    if et is not None and threads > 1:
+        M = conn_full_dev.shape[0]
+        ms = min(M, 500_000)
+        modes = [oracle.SHARED] if outputs == "shared" else [oracle.NODE, oracle.ELEM]
+        while True:
+            sub = conn_full_dev[:ms].cpu().numpy()
+            n_s = int(sub.max()) + 1 if sub.size else 0
+            t0 = time.perf_counter()
+            for m in modes:
+                _, _, used = oracle.csr_mt(m, et, sub, n_s, threads)
+            dt = time.perf_counter() - t0
+            what = "element-sharing node CSR" if outputs == "shared" else "node + element CSR"
+            if dt >= 0.6 * target_s or ms >= M:
+                return ms / dt, (f"first {ms:,} of {M:,} elements (node ids < {n_s:,}), {what}, "
+                                 f"{used} threads (node-range mode), {dt:.1f} s"), dt, ms
+            ms = min(M, int(ms * max(1.5, min(8.0, target_s / max(dt, 1e-3)))))
     if et is None:   # polygon workload
         off_d, idx_d = conn_full_dev
         M = off_d.numel() - 1
@@ -191,6 +208,60 @@ def oracle_sample(conn_full_dev, et, target_s, k_layers_hint=None, outputs="both
         ms = min(M, int(ms * max(1.5, min(8.0, target_s / max(dt, 1e-3)))))
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _slice(csr, lo, a, b):
+    """Rows [a, b) of a device CSR whose first row is vertex lo -> host (relative offsets, indices)."""
+    off, idx = csr
+    o = off[a - lo:b - lo + 1].cpu().numpy()
+    i = idx[int(o[0]):int(o[-1])].cpu().numpy() if o.size else idx[:0].cpu().numpy()
+    return o - (o[0] if o.size else 0), i
+
+
+def parity_gate(et, conn_cpu, N, outs, lo=0, hi=None, rows=1 << 15):
+    """Bit-exact comparison of the timed call's outputs with the oracle's node-range mode (SURVEY
+    §8(c)) on three vertex ranges (first, middle, last of [lo, hi)), before any timing is printed
+    (SPEC S:L418, L435).  outs: {oracle mode: device CSR whose first row is vertex lo}.
+    Raises SystemExit on a mismatch.  -> description of what was checked."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    import oracle
+    hi = N if hi is None else hi
+    R = min(rows, hi - lo)
+    ranges = sorted({(lo, lo + R), ((lo + hi - R) // 2, (lo + hi + R) // 2), (hi - R, hi)})
+    jobs = []
+    with ThreadPoolExecutor(max_workers=len(ranges) * len(outs)) as ex:   # ctypes releases the GIL
+        for mode, csr in outs.items():
+            for a, b in ranges:
+                if et is None:
+                    fut = ex.submit(oracle.poly_csr_range, mode, conn_cpu[0], conn_cpu[1], N, a, b)
+                else:
+                    fut = ex.submit(oracle.csr_range, mode, et, conn_cpu, N, a, b)
+                jobs.append((mode, a, b, csr, fut))
+        nv = 0
+        for mode, a, b, csr, fut in jobs:
+            ro, ri = fut.result()
+            go, gi = _slice(csr, lo, a, b)
+            if not (np.array_equal(go, ro) and np.array_equal(gi, ri)):
+                raise SystemExit(f"parity gate FAILED: mode {mode}, vertices [{a}, {b}) differ from the oracle; "
+                                 "no timing reported")
+            nv += b - a
+    names = {0: "node", 1: "elem", 2: "shared"}
+    return {"ok": True, "oracle": "node-range mode (oracle/oracle.cpp oracle_csr_range)",
+            "outputs": [names[m] for m in outs], "vertex_ranges": [list(r) for r in ranges],
+            "vertices_checked_per_output": sum(b - a for a, b in ranges), "compare": "bit-exact (memcmp)"}
+
+
 # ------------------------------------------------------------------------------------------------
 # reference arm: the oracle, timed as it stands on the host cores
 # ------------------------------------------------------------------------------------------------
@@ -205,12 +276,18 @@ def run_reference(args):
     if args.config in meshgen.POLY_CONFIGS:
         return run_reference_poly(args)
     if args.config == 5:   # only the leading cell layers are ever sampled: build just those
-        et, conn = meshgen.TET4, meshgen.kuhn_tets(320, cell_begin=0, cell_end=320 * 320 * 48)[0]
+        et, conn = meshgen.TET4, meshgen.kuhn_tets(320, cell_begin=0, cell_end=320 * 320 * 128)[0]
         M_total, N_total = 6 * 320 ** 3, 321 ** 3
     else:
         et, conn, N_total = meshgen.make_config(args.config, device="cpu")
         M_total = int(conn.shape[0])
     conn = conn.numpy()
+    T = oracle.host_threads()   # the oracle's T-thread node-range mode on all host cores
+
+    def one(sub, n_s):
+        oracle.csr_mt(oracle.NODE, et, sub, n_s, T)
+        oracle.csr_mt(oracle.ELEM, et, sub, n_s, T)
+
     # size the per-step sample for ~ (few minutes) / (steps + warmup)
     per_step = max(1.0, min(20.0, 150.0 / (args.steps + args.warmup)))
     ms = min(conn.shape[0], 100_000)
@@ -218,8 +295,7 @@ def run_reference(args):
         sub = conn[:ms]
         n_s = int(sub.max()) + 1
         t0 = time.perf_counter()
-        oracle.node_csr(et, sub, n_s)
-        oracle.elem_csr(et, sub, n_s)
+        one(sub, n_s)
         dt = time.perf_counter() - t0
         if dt >= 0.6 * per_step or ms >= conn.shape[0]:
             break
@@ -227,25 +303,24 @@ def run_reference(args):
     sub = conn[:ms]
     n_s = int(sub.max()) + 1
     for _ in range(args.warmup):
-        oracle.node_csr(et, sub, n_s)
-        oracle.elem_csr(et, sub, n_s)
+        one(sub, n_s)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.node_csr(et, sub, n_s)
-        oracle.elem_csr(et, sub, n_s)
+        one(sub, n_s)
         times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
     v = ms / t
     sample = (f"first {ms:,} elements of config {args.config} ({meshgen.CONFIGS[args.config]['name']}), "
-              f"node ids < {n_s:,}; std::set oracle, node + element CSR, 1 thread")
+              f"node ids < {n_s:,}; std::set oracle, node + element CSR, {T} threads (node-range mode, "
+              f"{cpu_model()})")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": f"config {args.config}: {meshgen.CONFIGS[args.config]['desc']}",
-                       "elements": M_total, "nodes": N_total, "parallelism": "host, 1 thread (oracle)",
+                       "elements": M_total, "nodes": N_total, "parallelism": f"host, {T} threads (oracle)",
                        "outputs": "node + element CSR", "sample_elements": ms},
-            "cpu_baseline": {"value": v, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "elements/s", "cores": T, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
@@ -385,6 +460,43 @@ def run_ours(args):
         del r
     torch.cuda.synchronize()
 
+    # ---- parity gate: one more call, its outputs compared with the oracle's
+    # node-range mode before anything is timed; also gives the output sizes for B_min ----
+    r = step()
+    torch.cuda.synchronize()
+    parity = None
+    nnz = {}
+    if poly:
+        node_r, elem_r, shared_r = r
+        outs = {m: c for m, c in ((0, node_r), (1, elem_r), (2, shared_r)) if c is not None}
+    elif args.outputs == "shared":
+        outs = {2: r}
+    elif world > 1:
+        outs = {0: r.node, 1: r.elem}
+    else:
+        outs = {0: r[0], 1: r[1]}
+    for m, c in outs.items():
+        nnz[m] = int(c[1].numel())
+    if world > 1:   # slices: total nnz over ranks
+        tot = torch.tensor([nnz.get(0, 0), nnz.get(1, 0)], dtype=torch.int64,
+                           device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(tot)
+        nnz = {0: int(tot[0]), 1: int(tot[1])}
+    if not args.no_parity and rank == 0:
+        if world > 1:   # rank 0 checks its own slice against the whole mesh (built on the host)
+            import meshgen
+            _, conn_full, _ = meshgen.make_config(args.config, device="cpu")
+            parity = parity_gate(et, conn_full.numpy(), N, outs, lo=r.lo, hi=r.hi)
+            del conn_full
+        elif poly:
+            parity = parity_gate(None, (conn[0].cpu().numpy(), conn[1].cpu().numpy()), N, outs)
+        else:
+            parity = parity_gate(et, conn.cpu().numpy(), N, outs)
+    if world > 1:
+        dist.barrier()
+    del r, outs
+    torch.cuda.synchronize()
+
     # ---- device-timed region ----
     s = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -433,6 +545,15 @@ def run_ours(args):
     step_roof = {"alg_bytes_per_step": step_bytes, "achieved_GBps": step_bytes / (ms_local / 1e3) / 1e9,
                  "frac_of_peak": step_bytes / (ms_local / 1e3) / 1e9 / peak,
                  "kernel_ms_per_step": tot_ms / args.steps}
+    # compulsory floor: connectivity read once, every output written once
+    if poly:
+        conn_bytes = conn[0].numel() * 8 + conn[1].numel() * 4
+    else:
+        conn_bytes = conn.numel() * 4 * (world if world > 1 else 1)   # (shards: approximately the mesh)
+    b_min = conn_bytes + sum(4 * v + 8 * (N + 1) for v in nnz.values())
+    step_roof.update({"B_min_bytes": b_min, "B_min_GBps": b_min / (ms / 1e3) / 1e9,
+                      "frac_vs_B_min": b_min / (ms / 1e3) / 1e9 / peak,
+                      "B_min_def": "connectivity once + each output CSR once (int32 indices, int64 offsets)"})
 
     # ---- end to end through the public host-buffer API ----
     e2e = None
@@ -488,8 +609,18 @@ def run_ours(args):
     # ---- CPU baseline: the oracle on a bounded sample, rank 0 at N=1 only ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, desc, dt, ms_s = oracle_sample(conn, et, args.cpu_seconds, outputs=args.outputs)
-        cpu = {"value": v, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": desc}
+        import oracle
+        T = oracle.host_threads()
+        v1, desc1, _, _ = oracle_sample(conn, et, args.cpu_seconds / 2, outputs=args.outputs)
+        if poly or T <= 1:
+            v, desc, cores = v1, desc1, 1
+        else:
+            v, desc, _, _ = oracle_sample(conn, et, args.cpu_seconds / 2, outputs=args.outputs, threads=T)
+            cores = T
+        cpu = {"value": v, "unit": "elements/s", "cores": cores, "kind": "oracle", "sample": desc,
+               "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+               "serial": {"value": v1, "cores": 1, "sample": desc1,
+                          "note": "the paper's serial baseline (P:L288-290)"}}
 
     if rank == 0:
         line = {
@@ -506,7 +637,7 @@ def run_ours(args):
                        **({"max_workspace_gb": args.max_workspace_gb, "node_ranges": chunks_used[-1]}
                           if args.max_workspace_gb and not poly and world == 1 else {})},
             "roofline": roofline, "step_roofline": step_roof, "kernels": kernels,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "parity": parity,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -14,14 +14,28 @@
  *   - Pointers named d_* are CUDA device pointers, h_* host pointers.  Connectivity is
  *     int32 conn[num_elems][arity] row-major, 0-based, owned by the caller, read-only here.
  *   - All work is stream-ordered on `stream` (a cudaStream_t passed as void*; NULL = legacy
- *     default stream).  The mn_find_* calls block the calling thread exactly once (to read the
- *     validation word and nnz: the output size is data-dependent) and return with the outputs
- *     complete on `stream`.  Stage primitives (mn_emit_*, mn_radix_sort_*, ...) do not block
- *     unless stated.
+ *     default stream) on the calling thread's current device, and the mn_find_* calls return
+ *     with the outputs complete on `stream`.  They block the calling thread to read device
+ *     words whose values size the outputs or choose the algorithm:
+ *       - mn_find_{node,elem}_neighbors, _both, _shared: once (validation word + nnz), plus once
+ *         before it on meshes of >= 2^20 elements with the automatic element path (the locality
+ *         sample that picks the element-CSR algorithm);
+ *       - mn_find_poly_neighbors: three times (offset bounds; validation + element offsets; node nnz);
+ *       - mn_find_neighbors_both_chunked: once per node range, plus once;
+ *       - mn_find_neighbors_both_host: as _both, plus the final D2H;
+ *       - mn_find_neighbors_dist: as _both, plus the exchange's count step (see there).
+ *     Stage primitives (mn_emit_*, mn_radix_sort_*, ...) do not block unless stated.
  *   - Memory: outputs and workspace come from the caller's mn_allocator (NULL = the library's
- *     cudaMallocAsync on `stream`).  Outputs are owned by the caller; release them with
- *     mn_csr_release.  Workspace is released before return.  No global state except the
- *     optional profiler (not thread-safe; bench only).
+ *     cudaMallocAsync on `stream`); the library allocates and releases on `stream` only.  Outputs
+ *     are owned by the caller; release them with mn_csr_release.  Workspace is released before
+ *     return (stream-ordered: an allocator must not hand a released block to another stream
+ *     before `stream` has passed the release point).
+ *   - Global state: (1) the optional profiler (mn_profile_*; not thread-safe; bench only);
+ *     (2) two process-wide test knobs, mn_set_elem_path and mn_set_chunk_cap (defaults: auto,
+ *     0), which change the algorithm but never the result; (3) per-device one-time setup
+ *     (kernel shared-memory attributes, an occupancy-derived grid size), guarded per device, so
+ *     one process may drive several GPUs and several threads may call concurrently; (4) per
+ *     thread and device: a pinned staging word pair and the host path's side stream + event.
  *   - Errors: invalid input is reported as the LOWEST offending element id, then the lowest
  *     position in it; an index outside [0, N) is reported before a repeated node of the same
  *     element (reading R8).  On any error no output is returned (out->offsets == NULL).

@@ -65,6 +65,10 @@ def _load():
         lib.oracle_csr_mt.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                       ctypes.c_int, pp64, pp32, p64, p64, p32, p32]
         lib.oracle_csr_mt.restype = ctypes.c_int
+        lib.oracle_poly_csr_range.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                              ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, pp64, pp32, p64,
+                                              p64, p32]
+        lib.oracle_poly_csr_range.restype = ctypes.c_int
         lib.oracle_free.argtypes = [ctypes.c_void_p]
         lib.oracle_free.restype = None
         _lib = lib
@@ -237,6 +241,22 @@ def poly_elem_csr(off, idx, num_nodes: int):
 def poly_shared_csr(off, idx, num_nodes: int):
     """Element-sharing node adjacency of a polygon mesh as CSR."""
     return _poly(2, off, idx, num_nodes)
+
+
+def poly_csr_range(mode: int, off, idx, num_nodes: int, lo: int, hi: int):
+    """Polygon CSR slice of vertices [lo, hi) (mode NODE / ELEM / SHARED), offsets relative."""
+    lib = _load()
+    o, i = _as_poly(off, idx)
+    po = ctypes.POINTER(ctypes.c_int64)()
+    pi = ctypes.POINTER(ctypes.c_int32)()
+    nnz = ctypes.c_int64(0)
+    ee, ep = ctypes.c_int64(-1), ctypes.c_int32(-1)
+    rc = lib.oracle_poly_csr_range(mode, o.ctypes.data, i.ctypes.data, o.shape[0] - 1, num_nodes, lo, hi,
+                                   ctypes.byref(po), ctypes.byref(pi), ctypes.byref(nnz), ctypes.byref(ee),
+                                   ctypes.byref(ep))
+    if rc != OK:
+        raise OracleMeshError(rc, ee.value, ep.value)
+    return _take(po, pi, nnz.value, hi - lo)
 
 
 from . import stages  # noqa: E402,F401  (numpy step-by-step oracle)

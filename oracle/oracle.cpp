@@ -299,6 +299,41 @@ int oracle_csr_mt(int mode, int etype, const int32_t* conn, int64_t M, int64_t N
   return OK;
 }
 
+// Polygon meshes, node-range mode: oracle_poly_csr's loops restricted to vertices [lo, hi).
+int oracle_poly_csr_range(int mode, const int64_t* off, const int32_t* idx, int64_t M, int64_t N, int64_t lo,
+                          int64_t hi, int64_t** offsets, int32_t** indices, int64_t* nnz, int64_t* err_elem,
+                          int32_t* err_pos) {
+  if (mode < 0 || mode > 2 || lo < 0 || hi < lo || hi > N) return ERR_ARG;
+  int rc = oracle_poly_validate(off, idx, M, N, err_elem, err_pos);
+  if (rc != OK) return rc;
+  const int64_t R = hi - lo;
+  if (mode == 1) {
+    std::vector<std::vector<int32_t>> L((size_t)R);
+    for (int64_t e = 0; e < M; ++e)
+      for (int64_t p = off[e]; p < off[e + 1]; ++p)
+        if (idx[p] >= lo && idx[p] < hi) L[(size_t)(idx[p] - lo)].push_back((int32_t)e);
+    flatten(L, R, offsets, indices, nnz);
+    return OK;
+  }
+  std::vector<std::set<int32_t>> S((size_t)R);
+  for (int64_t e = 0; e < M; ++e) {
+    const int64_t k = off[e + 1] - off[e];
+    const int32_t* row = idx + off[e];
+    for (int64_t i = 0; i < k; ++i) {
+      if (mode == 0) {
+        const int32_t a = row[i], b = row[(i + 1) % k];
+        if (a >= lo && a < hi) S[(size_t)(a - lo)].insert(b);
+        if (b >= lo && b < hi) S[(size_t)(b - lo)].insert(a);
+      } else if (row[i] >= lo && row[i] < hi) {
+        for (int64_t j = 0; j < k; ++j)
+          if (i != j) S[(size_t)(row[i] - lo)].insert(row[j]);
+      }
+    }
+  }
+  flatten(S, R, offsets, indices, nnz);
+  return OK;
+}
+
 void oracle_free(void* p) { std::free(p); }
 
 }  // extern "C"

@@ -157,8 +157,12 @@ def load():
 class _TorchAllocator:
     """Hands out torch uint8 CUDA tensors; keeps them alive until released or adopted."""
 
-    def __init__(self, device):
+    def __init__(self, device, stream=None):
         self.device = device
+        # Blocks come from the caching allocator's pool of the stream the library runs on, so a
+        # workspace the library releases while its kernels still read it is only reused by later
+        # work on that same stream (stream order), never by the caller's current stream.
+        self.stream = stream
         self.live = {}
         self._a = _ALLOC_FN(self._alloc)
         self._r = _RELEASE_FN(self._release)
@@ -166,7 +170,11 @@ class _TorchAllocator:
 
     def _alloc(self, ctx, nbytes, stream):
         try:
-            t = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+            if self.stream is not None:
+                with torch.cuda.stream(self.stream):
+                    t = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+            else:
+                t = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
         except RuntimeError:
             return None
         p = t.data_ptr()
@@ -256,7 +264,7 @@ def find_node_neighbors(conn: torch.Tensor, etype, num_nodes: int, stream=None):
     et = _etype(etype)
     c, M = _conn_arg(conn, et)
     lib = load()
-    al = _TorchAllocator(c.device)
+    al = _TorchAllocator(c.device, stream)
     out, err = _Csr(), _ErrDetail()
     with torch.cuda.device(c.device):
         rc = lib.mn_find_node_neighbors(et, c.data_ptr(), M, int(num_nodes), ctypes.byref(al.struct),
@@ -270,7 +278,7 @@ def find_node_neighbors_sortpairs(conn: torch.Tensor, etype, num_nodes: int, str
     et = _etype(etype)
     c, M = _conn_arg(conn, et)
     lib = load()
-    al = _TorchAllocator(c.device)
+    al = _TorchAllocator(c.device, stream)
     out, err = _Csr(), _ErrDetail()
     with torch.cuda.device(c.device):
         rc = lib.mn_find_node_neighbors_sortpairs(et, c.data_ptr(), M, int(num_nodes), ctypes.byref(al.struct),
@@ -284,7 +292,7 @@ def find_node_neighbors_shared(conn: torch.Tensor, etype, num_nodes: int, stream
     et = _etype(etype)
     c, M = _conn_arg(conn, et)
     lib = load()
-    al = _TorchAllocator(c.device)
+    al = _TorchAllocator(c.device, stream)
     out, err = _Csr(), _ErrDetail()
     with torch.cuda.device(c.device):
         rc = lib.mn_find_node_neighbors_shared(et, c.data_ptr(), M, int(num_nodes), ctypes.byref(al.struct),
@@ -298,7 +306,7 @@ def find_elem_neighbors(conn: torch.Tensor, etype, num_nodes: int, stream=None):
     et = _etype(etype)
     c, M = _conn_arg(conn, et)
     lib = load()
-    al = _TorchAllocator(c.device)
+    al = _TorchAllocator(c.device, stream)
     out, err = _Csr(), _ErrDetail()
     with torch.cuda.device(c.device):
         rc = lib.mn_find_elem_neighbors(et, c.data_ptr(), M, int(num_nodes), ctypes.byref(al.struct),
@@ -312,7 +320,7 @@ def find_neighbors(conn: torch.Tensor, etype, num_nodes: int, stream=None):
     et = _etype(etype)
     c, M = _conn_arg(conn, et)
     lib = load()
-    al = _TorchAllocator(c.device)
+    al = _TorchAllocator(c.device, stream)
     no, eo, err = _Csr(), _Csr(), _ErrDetail()
     with torch.cuda.device(c.device):
         rc = lib.mn_find_neighbors_both(et, c.data_ptr(), M, int(num_nodes), ctypes.byref(al.struct),
@@ -336,7 +344,7 @@ def find_poly_neighbors(off: torch.Tensor, idx: torch.Tensor, num_nodes: int, no
         raise ValueError("off needs num_elems + 1 entries")
     off, idx = off.contiguous(), idx.contiguous()
     lib = load()
-    al = _TorchAllocator(off.device)
+    al = _TorchAllocator(off.device, stream)
     outs = [_Csr() if w else None for w in (node, elem, shared)]
     err = _ErrDetail()
     ref = [ctypes.byref(o) if o is not None else None for o in outs]
@@ -349,7 +357,8 @@ def find_poly_neighbors(off: torch.Tensor, idx: torch.Tensor, num_nodes: int, no
 
 
 def _parse(fn, data):
-    if isinstance(data, (str, os.PathLike)):
+    # a path: os.PathLike, or a str holding no line break; any other str is the file's text
+    if isinstance(data, os.PathLike) or (isinstance(data, str) and "\n" not in data and "\r" not in data):
         with open(data, "rb") as f:
             data = f.read()
     if isinstance(data, str):
@@ -384,7 +393,7 @@ def find_neighbors_chunked(conn: torch.Tensor, etype, num_nodes: int, max_worksp
     et = _etype(etype)
     c, M = _conn_arg(conn, et)
     lib = load()
-    al = _TorchAllocator(c.device)
+    al = _TorchAllocator(c.device, stream)
     no, eo, err = _Csr(), _Csr(), _ErrDetail()
     k = ctypes.c_int64(0)
     with torch.cuda.device(c.device):
@@ -409,7 +418,7 @@ def find_neighbors_host(conn_host: torch.Tensor, etype, num_nodes: int, device=N
     M = c.numel() // ARITY[et]
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     lib = load()
-    dal, hal = _TorchAllocator(dev), _PinnedAllocator()
+    dal, hal = _TorchAllocator(dev, stream), _PinnedAllocator()
     no, eo, err = _Csr(), _Csr(), _ErrDetail()
     with torch.cuda.device(dev):
         rc = lib.mn_find_neighbors_both_host(et, c.data_ptr(), M, int(num_nodes), ctypes.byref(dal.struct),
@@ -471,7 +480,7 @@ def emit_elem_pairs(conn: torch.Tensor, etype, num_nodes: int, stream=None):
 def radix_sort_keys(keys: torch.Tensor, key_bits: int, stream=None) -> torch.Tensor:
     """Row a3: in-place ascending LSD sort of int64 (u64) or int32 (u32 bit pattern) keys."""
     kb = keys.element_size()
-    al = _TorchAllocator(keys.device)
+    al = _TorchAllocator(keys.device, stream)
     with torch.cuda.device(keys.device):
         rc = load().mn_radix_sort_keys(keys.data_ptr(), kb, keys.numel(), int(key_bits), ctypes.byref(al.struct),
                                        _stream_ptr(stream))
@@ -481,7 +490,7 @@ def radix_sort_keys(keys: torch.Tensor, key_bits: int, stream=None) -> torch.Ten
 
 def radix_sort_pairs_u32(keys: torch.Tensor, vals: torch.Tensor, key_bits: int, stream=None):
     """Row a3e: in-place stable LSD sort of uint32 (key, value) pairs."""
-    al = _TorchAllocator(keys.device)
+    al = _TorchAllocator(keys.device, stream)
     with torch.cuda.device(keys.device):
         rc = load().mn_radix_sort_pairs_u32(keys.data_ptr(), vals.data_ptr(), keys.numel(), int(key_bits),
                                             ctypes.byref(al.struct), _stream_ptr(stream))
@@ -495,7 +504,7 @@ def unique_node_csr(sorted_keys: torch.Tensor, num_nodes: int, stream=None):
     off = torch.empty(int(num_nodes) + 1, dtype=torch.int64, device=sorted_keys.device)
     idx = torch.empty(max(n, 1), dtype=torch.int32, device=sorted_keys.device)
     nnz = ctypes.c_int64(0)
-    al = _TorchAllocator(sorted_keys.device)
+    al = _TorchAllocator(sorted_keys.device, stream)
     with torch.cuda.device(sorted_keys.device):
         rc = load().mn_unique_node_csr(sorted_keys.data_ptr(), sorted_keys.element_size(), n, int(num_nodes),
                                        off.data_ptr(), idx.data_ptr(), ctypes.byref(nnz), ctypes.byref(al.struct),
@@ -517,7 +526,7 @@ def elem_offsets(sorted_keys: torch.Tensor, num_nodes: int, stream=None) -> torc
 def exclusive_scan(counts: torch.Tensor, stream=None) -> torch.Tensor:
     """Row a5: int32 counts -> int64 exclusive scan with the total appended (n+1 entries)."""
     out = torch.empty(counts.numel() + 1, dtype=torch.int64, device=counts.device)
-    al = _TorchAllocator(counts.device)
+    al = _TorchAllocator(counts.device, stream)
     with torch.cuda.device(counts.device):
         rc = load().mn_exclusive_scan_i32(counts.data_ptr(), counts.numel(), out.data_ptr(), ctypes.byref(al.struct),
                                           _stream_ptr(stream))
@@ -540,7 +549,7 @@ def dist_bucket(conn_shard: torch.Tensor, etype, global_elem_base: int, num_node
     hc = (ctypes.c_int64 * world)()
     hrc = (ctypes.c_int64 * world)()
     pe, pr = ctypes.c_void_p(), ctypes.c_void_p()
-    al = _TorchAllocator(c.device)
+    al = _TorchAllocator(c.device, stream)
     err = _ErrDetail()
     with torch.cuda.device(c.device):
         rc = load().mn_dist_bucket(et, c.data_ptr(), M, int(global_elem_base), int(num_nodes), int(world),
@@ -559,7 +568,7 @@ def dist_finish(etype, pairs: torch.Tensor, row_elems: torch.Tensor, rows: torch
     the received remote rows and the own shard."""
     et = _etype(etype)
     dev = pairs.device
-    al = _TorchAllocator(dev)
+    al = _TorchAllocator(dev, stream)
     ns, es = _Csr(), _Csr()
     rows = rows.contiguous()
     shard = conn_shard.contiguous()

@@ -19,7 +19,9 @@
 //     position in the line (0-based; -1 when not token-specific).
 //   * The result is validated like every input of the library (R18 order: arity >= 3, index range,
 //     repeated node), detail = (face index, position).
+#include <algorithm>
 #include <cerrno>
+#include <new>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -145,11 +147,7 @@ mn_status finish(std::vector<int64_t>& off, std::vector<int32_t>& idx, int64_t N
   return MN_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-mn_status mn_parse_off(const char* bytes, size_t len, mn_host_mesh* out, mn_error_detail* err) {
+mn_status parse_off(const char* bytes, size_t len, mn_host_mesh* out, mn_error_detail* err) {
   if (err) { err->elem = -1; err->pos = -1; }
   if (!out || (len && !bytes)) return MN_ERR_INVALID_ARG;
   std::memset(out, 0, sizeof(*out));
@@ -187,7 +185,8 @@ mn_status mn_parse_off(const char* bytes, size_t len, mn_host_mesh* out, mn_erro
   }
   std::vector<int64_t> off;
   std::vector<int32_t> idx;
-  off.reserve((size_t)F + 1);
+  // the face count is untrusted: every face line takes at least 2 bytes, so never reserve more
+  off.reserve((size_t)std::min<int64_t>(F, (int64_t)(c.end - c.p) / 2) + 1);
   off.push_back(0);
   for (int64_t f = 0; f < F; ++f) {
     if (!next_line(c, b, e)) return fail(err, MN_ERR_COUNT_MISMATCH, c.line, -1);
@@ -206,7 +205,7 @@ mn_status mn_parse_off(const char* bytes, size_t len, mn_host_mesh* out, mn_erro
   return finish(off, idx, V, out, err);
 }
 
-mn_status mn_parse_obj(const char* bytes, size_t len, mn_host_mesh* out, mn_error_detail* err) {
+mn_status parse_obj(const char* bytes, size_t len, mn_host_mesh* out, mn_error_detail* err) {
   if (err) { err->elem = -1; err->pos = -1; }
   if (!out || (len && !bytes)) return MN_ERR_INVALID_ARG;
   std::memset(out, 0, sizeof(*out));
@@ -240,6 +239,35 @@ mn_status mn_parse_obj(const char* bytes, size_t len, mn_host_mesh* out, mn_erro
     // every other record type (vt, vn, vp, o, g, s, usemtl, mtllib, l, p, ...) is ignored
   }
   return finish(off, idx, nv, out, err);
+}
+
+}  // namespace
+
+extern "C" {
+
+// No C++ exception crosses the C ABI: an allocation failure while parsing is MN_ERR_OOM.
+mn_status mn_parse_off(const char* bytes, size_t len, mn_host_mesh* out, mn_error_detail* err) {
+  try {
+    return parse_off(bytes, len, out, err);
+  } catch (const std::bad_alloc&) {
+    if (out) mn_host_mesh_free(out);
+    return MN_ERR_OOM;
+  } catch (...) {
+    if (out) mn_host_mesh_free(out);
+    return MN_ERR_INVALID_ARG;
+  }
+}
+
+mn_status mn_parse_obj(const char* bytes, size_t len, mn_host_mesh* out, mn_error_detail* err) {
+  try {
+    return parse_obj(bytes, len, out, err);
+  } catch (const std::bad_alloc&) {
+    if (out) mn_host_mesh_free(out);
+    return MN_ERR_OOM;
+  } catch (...) {
+    if (out) mn_host_mesh_free(out);
+    return MN_ERR_INVALID_ARG;
+  }
 }
 
 void mn_host_mesh_free(mn_host_mesh* m) {

@@ -58,6 +58,14 @@ static cudaError_t launch(const char* name, double alg_bytes, cudaStream_t s, F&
   return e;
 }
 
+// Adds bytes known only after the call's host sync (a list size) to the latest record of `name`.
+// (skip: how many later records of the same name to pass over)
+static void prof_add_bytes(const char* name, double bytes, int skip = 0) {
+  if (!g_prof) return;
+  for (auto it = g_recs.rbegin(); it != g_recs.rend(); ++it)
+    if (std::strcmp(it->name, name) == 0 && skip-- == 0) { it->bytes += bytes; return; }
+}
+
 // ================================================================================================
 // memory
 // ================================================================================================
@@ -101,6 +109,29 @@ static uint64_t* pinned_pair() {
   }
   return p;
 }
+
+// Per-device one-time setup (kernel attributes, occupancy-derived grids): one flag per (site,
+// device), so a process that drives several GPUs, or several threads racing their first call, set
+// every attribute on every device before its first launch there.
+static int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) { cudaGetLastError(); d = 0; }
+  return d;
+}
+constexpr int kMaxDevices = 64;
+struct PerDevice {
+  std::mutex mu;
+  bool done[kMaxDevices] = {};
+  int value[kMaxDevices] = {};
+  template <class F>
+  int once(F&& f) {   // runs f() (returning int) once per device; returns its value for this device
+    const int d = current_device();
+    std::lock_guard<std::mutex> g(mu);
+    if (d < 0 || d >= kMaxDevices) return f();
+    if (!done[d]) { value[d] = f(); done[d] = true; }
+    return value[d];
+  }
+};
 
 static mn_status decode_err(uint64_t w, mn_error_detail* err) {
   if (w == ERR_NONE) return MN_OK;
@@ -205,11 +236,11 @@ static cudaError_t run_pass(PassArgs pa, cudaStream_t s, const char* name, doubl
                       ((PAYLOAD || SRC == 2) ? (size_t)kTile * 4 : 0);
   auto kern = k_onesweep<KeyT, SRC, T, PAYLOAD, OWNER, BINS, kPassThreads, kPassItems, kPassWindow, kPassMinBlocks,
                          0, COUNTS>;
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  attr.once([&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+    return 0;
+  });
   return launch(name, bytes, s, [&] { kern<<<(unsigned)tiles, kPassThreads, smem, s>>>(pa); });
 }
 
@@ -600,11 +631,11 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
 
     const int scap = 48 * 1024;
-    static bool seg_attr = false;
-    if (!seg_attr) {
+    static PerDevice seg_attr;
+    seg_attr.once([&] {
       cudaFuncSetAttribute(k_segsort_giant, cudaFuncAttributeMaxDynamicSharedMemorySize, scap * 4);
-      seg_attr = true;
-    }
+      return 0;
+    });
     if (transpose) {
       // ---- a2 + a3e + a4 + a5 (elements): transpose bucketed by 128-node chunk ----
       // belem spans ekA + ekB (>= 2 Pe entries), bnode the bytes of epA + epB (>= 8 Pe)
@@ -618,14 +649,13 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       if (capl > (int64_t)INT32_MAX - 4096) capl = (int64_t)INT32_MAX - 4096;
       const int cap = (int)capl;
       // one resident wave (grid-stride): the occupancy of this instantiation x the SM count
-      static int fixed_wave = 0;
-      if (!fixed_wave) {
-        int occ = 0, dev = 0, sms = 148;
+      static PerDevice wave;
+      const int fixed_wave = wave.once([&] {
+        int occ = 0, sms = 148;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chunk_scatter_fixed<T, true>, 256, 0);
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        fixed_wave = (occ > 0 ? occ : 4) * sms;
-      }
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device());
+        return (occ > 0 ? occ : 4) * sms;
+      });
       const int fgrid = (int)std::min<int64_t>(fixed_wave, (P.M + 255) / 256 > 0 ? (P.M + 255) / 256 : 1);
       MN_CUDA(launch("elem_scatter", 4.0 * P.K * P.M + 5.0 * P.Pe, s, [&] {
         if (aligned)
@@ -702,11 +732,11 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       pa.err = errw;
       MN_CUDA((run_pass<uint32_t, 2, T, false, true, kMsdBins>(pa, s, "onesweep_elem_first", 12.0 * P.Pe)));
       const size_t rsm = (size_t)msd_R * 4;
-      static bool rattr = false;
-      if (!rattr) {
+      static PerDevice rattr;
+      rattr.once([&] {
         cudaFuncSetAttribute(k_range_transpose<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeMax * 4);
-        rattr = true;
-      }
+        return 0;
+      });
       // persistent grid of 96 CTAs (one per SM at most): their random-write windows (one bucket's
       // element ids, 1 MB each on config 4) stay in L2.  Config 4: 3.72 ms with 512 CTAs, 3.92 with
       // 148, 2.67 with 96, 3.00 with 64, 4.65 with 40.
@@ -788,7 +818,9 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     if (want_node) {
       // ---- a1 + a3n + a4 (nodes): expand the element CSR per node, sort + dedupe per node ----
       uint32_t* temp = ekA;   // CE * Pe entries: the dead element-sort buffers (ekA widened when CE > 4)
-      const double gb = 8.0 * (P.N + 1) + 4.0 * P.Pe + 4.0 * P.K * P.Pe;   // offsets, incidences, rows
+      // algorithmic bytes: element-CSR offsets + indices, every connectivity row once, counts and
+      // list offsets written; the written lists (4 B per distinct neighbour) are added after the sync
+      const double gb = 8.0 * (P.N + 1) + 4.0 * P.Pe + 4.0 * P.K * P.M + 8.0 * P.N;
       const unsigned ng = (unsigned)tiles_of(P.N, kNodeThreads);
       if (P.N > 0) {   // (M > 0 with N == 0 always fails validation: nothing to expand)
         MN_CUDA(launch("node_gather", gb, s, [&] {
@@ -808,14 +840,14 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
         }));
       }
       const int cap = 48 * 1024;   // uint32 entries sorted in shared memory by k_node_giant (192 KB)
-      static bool giant_attr = false;
-      if (!giant_attr) {
+      static PerDevice giant_attr;
+      giant_attr.once([&] {
         cudaFuncSetAttribute(k_node_giant<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
         cudaFuncSetAttribute(k_node_giant<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
         cudaFuncSetAttribute(k_node_giant<T, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
         cudaFuncSetAttribute(k_node_giant<T, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
-        giant_attr = true;
-      }
+        return 0;
+      });
       MN_CUDA(launch("node_giant", 0.0, s, [&] {
         const RowSrc rs{conn, 0, P.M, nullptr, nullptr, 0};
         if (shared && aligned)
@@ -842,6 +874,7 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     if (st != MN_OK) goto done;
     if (want_node) {
       U = (int64_t)host[1];
+      prof_add_bytes("node_gather", 4.0 * U);
       int32_t* out = U ? (int32_t*)mem.get((size_t)U * 4) : nullptr;
       if (U && !out) { st = MN_ERR_OOM; goto done; }
       if (U) {
@@ -987,7 +1020,8 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
         // (3) node slice: per-node expansion + dedupe, counts, offsets
         const RowSrc rs{conn, 0, P.M, nullptr, nullptr, 0};
         const unsigned ng = (unsigned)tiles_of(nloc, kNodeThreads);
-        MN_CUDA(launch("node_gather", 8.0 * (nloc + 1) + 4.0 * Ie + 4.0 * P.K * Ie, s, [&] {
+        // rows: at least Ie / K distinct elements touch the range (4 K B each); lists added after the sync
+        MN_CUDA(launch("node_gather", 8.0 * (nloc + 1) + 4.0 * Ie + 4.0 * Ie + 8.0 * nloc, s, [&] {
           if (aligned)
             k_node_gather_t<T, true><<<ng, kNodeThreads, 0, s>>>(eoff, eslice, rs, nloc, temp, cnt, lofs, giants,
                                                                  ngiant, errw, lo);
@@ -1020,6 +1054,7 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
       MN_CUDA(cudaMemcpyAsync(host + 1, noff + nloc, 8, cudaMemcpyDeviceToHost, s));
       MN_CUDA(cudaStreamSynchronize(s));
       const int64_t U = (int64_t)host[1];
+      prof_add_bytes("node_gather", 4.0 * U);
       if (U) {
         int32_t* part = (int32_t*)mem.get((size_t)U * 4);
         if (!part) { st = MN_ERR_OOM; goto done; }
@@ -1295,25 +1330,26 @@ static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, in
           segsort_fn<<<(unsigned)tiles_of(N, kSegThreads), kSegThreads, 0, s>>>(eoff, N, eidx, sgiants, nsgiant,
                                                                                    errw);
         }));
-      static bool seg_attr = false;
-      if (!seg_attr) {
+      static PerDevice seg_attr;
+      seg_attr.once([&] {
         cudaFuncSetAttribute(k_segsort_giant, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
-        seg_attr = true;
-      }
+        return 0;
+      });
       MN_CUDA(launch("segsort_giant", 0.0, s, [&] {
         k_segsort_giant<<<148, 1024, cap * 4, s>>>(eoff, eidx, sgiants, nsgiant, cap, errw);
       }));
     }
-    static bool poly_attr = false;
-    if (!poly_attr) {
+    static PerDevice poly_attr;
+    poly_attr.once([&] {
       cudaFuncSetAttribute(k_poly_giant<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
       cudaFuncSetAttribute(k_poly_giant<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
-      poly_attr = true;
-    }
+      return 0;
+    });
     if (wn) {   // ring-edge node adjacency: 2 raw candidates per incidence
       if (!tempR) tempR = L ? (uint32_t*)mem.get((size_t)2 * L * 4) : nullptr;
       if (L && !tempR) { st = MN_ERR_OOM; goto done; }
-      MN_CUDA(launch("poly_gather", 8.0 * (N + 1) + 4.0 * L + 24.0 * L, s, [&] {
+      // element CSR, every ring once (offsets + entries), counts + list offsets; lists added after the sync
+      MN_CUDA(launch("poly_gather", 8.0 * (N + 1) + 4.0 * L + 8.0 * (M + 1) + 4.0 * L + 8.0 * N, s, [&] {
         k_poly_gather<false><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, off, idx, N, nullptr, 2, tempR, cntR, lofsR,
                                                         giants, ngiant, errw);
       }));
@@ -1331,7 +1367,7 @@ static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, in
       tempS = rawtotal ? (uint32_t*)mem.get((size_t)rawtotal * 4) : nullptr;
       if (rawtotal && !tempS) { st = MN_ERR_OOM; goto done; }
       MN_CUDA(cudaMemsetAsync(ngiant, 0, 4, s));
-      MN_CUDA(launch("poly_gather", 16.0 * (N + 1) + 4.0 * L + 4.0 * rawtotal, s, [&] {
+      MN_CUDA(launch("poly_gather", 16.0 * (N + 1) + 4.0 * L + 8.0 * (M + 1) + 4.0 * L + 8.0 * N, s, [&] {
         k_poly_gather<true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, off, idx, N, rawoff, 0, tempS, cntS, lofsS,
                                                        giants, ngiant, errw);
       }));
@@ -1354,6 +1390,8 @@ static mn_status poly_find(const int64_t* off, const int32_t* idx, int64_t M, in
   MN_CUDA(cudaStreamSynchronize(s));
   Un = (wn && M > 0) ? (int64_t)host[2] : 0;
   Us = (wsh && M > 0) ? (int64_t)host[3] : 0;
+  if (wsh) prof_add_bytes("poly_gather", 4.0 * (double)Us);
+  if (wn) prof_add_bytes("poly_gather", 4.0 * (double)Un, wsh ? 1 : 0);
   if (Un) {
     nidx = (int32_t*)mem.get((size_t)Un * 4);
     if (!nidx) { st = MN_ERR_OOM; goto done; }
@@ -1773,12 +1811,12 @@ static mn_status dist_finish_impl(const uint64_t* pairs, int64_t n, const int32_
                                                                         giants, ngiant, errw, lo);
         }));
         const int cap = 48 * 1024;
-        static bool attr = false;
-        if (!attr) {
+        static PerDevice attr;
+        attr.once([&] {
           cudaFuncSetAttribute(k_node_giant<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
           cudaFuncSetAttribute(k_node_giant<T, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap * 4);
-          attr = true;
-        }
+          return 0;
+        });
         MN_CUDA(launch("node_giant", 0.0, s, [&] {
           if (aligned)
             k_node_giant<T, true, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant,
@@ -1924,8 +1962,13 @@ mn_status mn_find_neighbors_both_host(mn_elem_type t, const int32_t* h_conn, int
   if (st != MN_OK) return st;
   if (!host_alloc || !host_alloc->alloc || !no || !eo) return MN_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  static thread_local cudaStream_t side = nullptr;
-  static thread_local cudaEvent_t ev = nullptr;
+  // side stream + event of the element-CSR D2H: per calling thread and per device
+  static thread_local cudaStream_t sides[kMaxDevices] = {};
+  static thread_local cudaEvent_t evs[kMaxDevices] = {};
+  const int dev = current_device();
+  if (dev < 0 || dev >= kMaxDevices) return MN_ERR_INVALID_ARG;
+  cudaStream_t& side = sides[dev];
+  cudaEvent_t& ev = evs[dev];
   if (!side && cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) return MN_ERR_CUDA;
   if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return MN_ERR_CUDA;
   Mem mem(dev_alloc, s);

@@ -20,7 +20,7 @@ def test_reference_arm_line_config1():
     assert line["impl"] == "reference" and line["unit"] == "elements/s" and line["higher_is_better"] is True
     assert line["config"]["workload"].startswith("config 1: ")
     assert line["config"]["elements"] == 2048 and line["config"]["nodes"] == 1089
-    assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] == 1
+    assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["gpu_launches"] == 0
 
 

@@ -324,8 +324,32 @@ def test_deterministic_repeats(elem_path):
 
 
 # ------------------------------------------------------------------------------------------------
-# full-size configs 3-5: sampled vertices vs the oracle's one-vertex form + size-free properties
+# full-size configs 3-5: both CSRs compared in full (memcmp) with the T-thread node-range oracle
+# (SURVEY §8(c), T = host cores), plus sampled vertices vs the one-vertex form and size-free
+# properties (closed-form valences, handshake, symmetry)
 # ------------------------------------------------------------------------------------------------
+_FULL_ORACLE = {}
+
+
+def _full_oracle(cfg, et, conn_cpu, N):
+    """Both oracle CSRs of a full-size config, computed once per session (T = host cores)."""
+    if cfg not in _FULL_ORACLE:
+        T = oracle.host_threads()
+        no, ni, _ = oracle.csr_mt(oracle.NODE, et, conn_cpu, N, T)
+        eo, ei, _ = oracle.csr_mt(oracle.ELEM, et, conn_cpu, N, T)
+        _FULL_ORACLE[cfg] = ((no, ni), (eo, ei))
+    return _FULL_ORACLE[cfg]
+
+
+def _assert_full(got, exp, what):
+    go, gi = (_np(x) for x in got)
+    eo, ei = exp
+    assert go.shape == eo.shape and np.array_equal(go, eo), f"{what}: offsets differ"
+    assert gi.shape == ei.shape, f"{what}: nnz {gi.size} vs oracle {ei.size}"
+    if not np.array_equal(gi, ei):
+        bad = int(np.nonzero(gi != ei)[0][0])
+        v = int(np.searchsorted(eo, bad, side="right") - 1)
+        raise AssertionError(f"{what}: first differing index {bad} (vertex {v})")
 def _sampled_check(et, conn_cpu, N, got_node, got_elem, nsample=48, seed=0):
     rng = np.random.default_rng(seed)
     sample = np.unique(np.concatenate([rng.integers(0, N, nsample), [0, N - 1, N // 2]]))
@@ -389,7 +413,11 @@ def test_full_size_config(cfg, elem_path):
         cnt[pi] = val
         assert torch.equal(no[1:] - no[:-1], cnt)       # permutation equivariance of valences
     assert _symmetric(no, ni)
-    _sampled_check(et, conn.cpu(), N, (no, ni), (eo, ei))
+    conn_cpu = conn.cpu()
+    _sampled_check(et, conn_cpu, N, (no, ni), (eo, ei))
+    ref_node, ref_elem = _full_oracle(cfg, et, conn_cpu, N)
+    _assert_full((no, ni), ref_node, f"config {cfg} node CSR")
+    _assert_full((eo, ei), ref_elem, f"config {cfg} elem CSR")
 
 
 @pytest.mark.slow
@@ -402,7 +430,18 @@ def test_full_size_config5_single_gpu():
     val, ne = _kuhn_counts(n, "cuda")
     assert torch.equal(no[1:] - no[:-1], val) and torch.equal(eo[1:] - eo[:-1], ne)
     del val, ne
-    _sampled_check(et, conn.cpu(), N, (no, ni), (eo, ei), nsample=24)
+    conn_cpu = conn.cpu()
+    _sampled_check(et, conn_cpu, N, (no, ni), (eo, ei), nsample=24)
+    del conn
+    got_node = (no.cpu(), ni.cpu())
+    got_elem = (eo.cpu(), ei.cpu())
+    del no, ni, eo, ei
+    T = oracle.host_threads()
+    ro, ri, _ = oracle.csr_mt(oracle.NODE, et, conn_cpu, N, T)
+    _assert_full(got_node, (ro, ri), "config 5 node CSR")
+    del ro, ri, got_node
+    ro, ri, _ = oracle.csr_mt(oracle.ELEM, et, conn_cpu, N, T)
+    _assert_full(got_elem, (ro, ri), "config 5 elem CSR")
 
 
 # ------------------------------------------------------------------------------------------------

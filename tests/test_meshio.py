@@ -115,6 +115,21 @@ def test_path_argument(tmp_path):
     assert _rings(off, idx) == [[0, 1, 2]]
 
 
+def test_str_text_and_pathlike(tmp_path):
+    """A str holding the file's text is parsed as text; os.PathLike and line-free str are paths."""
+    off, idx, N, _ = mn.load_obj("v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 2 3\n")
+    assert _rings(off, idx) == [[0, 1, 2]] and N == 3
+    p = tmp_path / "m.off"
+    p.write_text("OFF\n3 1 0\n0 0 0\n1 0 0\n0 1 0\n3 0 1 2\n")
+    assert _rings(*mn.load_off(p)[:2]) == [[0, 1, 2]]
+
+
+def test_untrusted_face_count_is_not_reserved():
+    """A header claiming 2^31-1 faces in a 40-byte file is a count mismatch, not an allocation of
+    16 GB (no C++ exception escapes the C ABI)."""
+    assert _err(_off, "OFF\n3 2147483647 0\n0 0 0\n1 0 0\n0 1 0\n3 0 1 2\n")[0] == mn.MN_ERR_COUNT_MISMATCH
+
+
 def test_empty_obj_and_off():
     off, idx, N, k = _obj("")
     assert off.tolist() == [0] and idx.numel() == 0 and N == 0

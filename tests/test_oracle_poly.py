@@ -147,3 +147,16 @@ def test_sampled_form_matches_full(make):
         assert a.tolist() == i[o[v]:o[v + 1]].tolist()
         assert b.tolist() == ei[eo[v]:eo[v + 1]].tolist()
         assert c.tolist() == si[so[v]:so[v + 1]].tolist()
+
+
+@pytest.mark.parametrize("seed,M,N,kmin,kmax", [(1, 40, 30, 3, 7), (2, 200, 60, 3, 12), (4, 60, 12, 3, 12)])
+def test_range_mode_brute_force(seed, M, N, kmin, kmax):
+    """Node-range mode == brute-force rows lo..hi-1 for every mode, every range end."""
+    off, idx, N = meshgen.random_poly(M, N, kmin, kmax, seed)
+    exp = {oracle.NODE: _brute(off, idx, N, "node"), oracle.ELEM: _brute(off, idx, N, "elem"),
+           oracle.SHARED: _brute(off, idx, N, "shared")}
+    for lo in range(0, N + 1, 3):
+        for hi in (lo, min(N, lo + 1), min(N, lo + 7), N):
+            for mode, rows in exp.items():
+                o, i = oracle.poly_csr_range(mode, off, idx, N, lo, hi)
+                assert o[0] == 0 and _lists(o, i) == [list(r) for r in rows[lo:hi]], (mode, lo, hi)

@@ -1,4 +1,5 @@
-# scratch command for one gpurun call (edited per experiment); default: build, GPU parity, quick bench
+# scratch command for one gpurun call (edited per experiment)
+mkdir -p gpurun_out
+(nproc; free -g; lscpu | grep -E "Model name|^CPU\(s\)|Thread|Socket|NUMA node\(s\)"; nvidia-smi -L) > gpurun_out/host_info.txt 2>&1
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -1
-timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -1
-bash tools/_quick.sh 2>&1 | tail -4
+bash tools/_quick.sh 2>&1 | tail -6
