@@ -477,11 +477,19 @@ def run_ours(args):
         outs = {0: r[0], 1: r[1]}
     for m, c in outs.items():
         nnz[m] = int(c[1].numel())
-    if world > 1:   # slices: total nnz over ranks
-        tot = torch.tensor([nnz.get(0, 0), nnz.get(1, 0)], dtype=torch.int64,
-                           device=dev if dist.get_backend() == "nccl" else "cpu")
-        dist.all_reduce(tot)
-        nnz = {0: int(tot[0]), 1: int(tot[1])}
+    exchange = None
+    if world > 1:   # slices: total nnz over ranks; exchange volume (SURVEY §8(d) multi-GPU model)
+        nnz = {0: r.node_nnz_total, 1: r.elem_nnz_total}
+        x = torch.tensor([r.sent_bytes, r.recv_bytes, r.own_incidences], dtype=torch.int64,
+                         device=dev if dist.get_backend() == "nccl" else "cpu")
+        xs = [torch.empty_like(x) for _ in range(world)]
+        dist.all_gather(xs, x)
+        xs = torch.stack(xs).cpu().tolist()
+        exchange = {"payload": "remote (node, element) incidences 8 B + remote element id and row 4(k+1) B; "
+                               "own incidences stay in place",
+                    "sent_bytes_per_rank": [v[0] for v in xs], "recv_bytes_per_rank": [v[1] for v in xs],
+                    "own_incidence_fraction": sum(v[2] for v in xs) / max(1, nnz[1]),
+                    "backend": dist.get_backend()}
     if not args.no_parity and rank == 0:
         if world > 1:   # rank 0 checks its own slice against the whole mesh (built on the host)
             import meshgen
@@ -579,7 +587,12 @@ def run_ours(args):
             def estep():
                 c = host_conn.to(dev, non_blocking=True)
                 res = find_neighbors_dist(c, et, base, N)
-                outs = [x.to("cpu") for x in (*res.node, *res.elem)]
+                outs = []
+                for x in (*res.node, *res.elem):   # pinned, async D2H, one sync
+                    h = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+                    h.copy_(x, non_blocking=True)
+                    outs.append(h)
+                torch.cuda.current_stream().synchronize()
                 return outs
         else:
             def estep():
@@ -638,6 +651,7 @@ def run_ours(args):
                           if args.max_workspace_gb and not poly and world == 1 else {})},
             "roofline": roofline, "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "parity": parity,
+            **({"exchange": exchange} if exchange else {}),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

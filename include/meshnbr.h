@@ -71,7 +71,9 @@ typedef enum {
                                     detail = (e, -1) (SPEC ArityMismatch, R18)         */
   MN_ERR_SYNTAX = 8,             /* OFF/OBJ: malformed line; detail = (line, token position)    */
   MN_ERR_COUNT_MISMATCH = 9,     /* OFF: fewer / more vertex or face lines than the counts line  */
-  MN_ERR_ZERO_INDEX = 10         /* OBJ: face index 0; detail = (line, token position)           */
+  MN_ERR_ZERO_INDEX = 10,        /* OBJ: face index 0; detail = (line, token position)           */
+  MN_ERR_COMM = 11               /* multi-GPU: an exchange operation (NCCL or the caller's mn_comm)
+                                    failed, or NCCL could not be loaded                          */
 } mn_status;
 
 typedef void* mn_stream; /* cudaStream_t */
@@ -248,8 +250,8 @@ mn_status mn_exclusive_scan_i32(const int32_t* d_counts, int64_t n, int64_t* d_o
  * [r*ceil(N/G), (r+1)*ceil(N/G)); each rank holds an element shard with a global element base.
  * Only incidences travel: the owner of node a receives every (a, e) pair together with e's row,
  * which is all it needs for both CSR slices (the node pairs of a are the expansion of a's element
- * list).  The exchange between the two calls is done by the caller
- * (torch.distributed all_to_all over NCCL / NVLink); see paper_1604_04689_b200/dist.py.
+ * list).  mn_find_neighbors_dist (below) runs both with the exchange in between;
+ * these stage entry points serve tests that emulate several ranks on one device.
  * ------------------------------------------------------------------------------------------- */
 
 /* Validate the shard (error element ids are global) and bucket its incidences by owner rank,
@@ -276,6 +278,115 @@ mn_status mn_dist_finish(mn_elem_type type, const uint64_t* d_pairs, int64_t n, 
                          int64_t shard_elems, int64_t global_elem_base, int64_t num_nodes, int64_t lo,
                          int64_t hi, const mn_allocator* alloc, mn_stream stream, mn_csr* node_slice,
                          mn_csr* elem_slice);
+
+/* ---------------------------------------------------------------------------------------------
+ * Multi-GPU whole path (the paper's stated limit is one device's memory,
+ * PAPER.md §3.2.2).  One process (or thread) per GPU; rank r holds the element shard
+ * [global_elem_base, global_elem_base + shard_elems) of a mesh of num_nodes nodes (shards
+ * contiguous, ascending with the rank) and receives the CSR slices of the nodes it owns,
+ * [lo, hi) = [r * ceil(N/G), (r+1) * ceil(N/G)) clipped to N.  Inside one call, on `stream`:
+ *   1. validate the shard and bucket its (node, element) incidences stably by owner (one onesweep
+ *      pass, pairs created from conn), with one element row per (remote owner, element);
+ *   2. count exchange: one all-gather of every rank's [error word, status, incidence counts,
+ *      row counts]; the lowest error over all ranks is returned by EVERY rank (so no rank is left
+ *      waiting in a collective), before any payload moves;
+ *   3. payload exchange: one grouped all-to-all(v) of the remote incidences, the remote element
+ *      ids and their rows; an owner's own incidences never travel (read in place from step 1);
+ *   4. local finish: element CSR slice by a stable sort on the local node id (transpose or LSD, as
+ *      the 1-GPU path), node CSR slice by per-node expansion + dedupe (rows from the own shard or
+ *      the received table);
+ *   5. one all-gather of the slice nnz values: the global offset bases of the slices.
+ * Concatenating the slices of all ranks in rank order (offsets shifted by the bases) is
+ * bit-identical to the single-GPU CSRs.  Blocks the calling thread four times (steps 1, 2, 4, 5).
+ * All collectives are called in the same order on every rank.
+ * ------------------------------------------------------------------------------------------- */
+
+/* One all-to-all(v) exchange of a group: rank r sends send_counts[g] elements of elem_bytes bytes,
+ * starting at element send_displs[g] of `send`, to rank g, and receives recv_counts[g] elements
+ * from rank g at element recv_displs[g] of `recv`.  Device buffers; host count/displacement
+ * arrays of `world` entries.  A zero count means no message. */
+typedef struct {
+  const void* send;
+  const int64_t* send_counts;
+  const int64_t* send_displs;
+  void* recv;
+  const int64_t* recv_counts;
+  const int64_t* recv_displs;
+  size_t elem_bytes;
+} mn_a2a_op;
+
+/* The exchange operations the multi-GPU path needs.  mn_comm_from_nccl fills one over NCCL
+ * (NVLink / NVSwitch); a caller may supply its own (tests drive the path over gloo with host
+ * staging this way).  Both callbacks return 0 on success, and must be stream-ordered on `stream`
+ * or complete before returning. */
+typedef struct {
+  int rank;
+  int world;
+  void* ctx;
+  /* every rank contributes `bytes` bytes at d_send; d_recv gets world * bytes in rank order */
+  int (*allgather)(void* ctx, const void* d_send, void* d_recv, size_t bytes, mn_stream stream);
+  /* the n_ops exchanges as one group (NCCL: one ncclGroupStart / ncclGroupEnd) */
+  int (*alltoallv)(void* ctx, const mn_a2a_op* ops, int n_ops, mn_stream stream);
+} mn_comm;
+
+typedef struct {
+  int64_t lo, hi;              /* owned node range                                          */
+  int64_t node_base, elem_base;/* global offsets of this rank's slices in the 1-GPU CSRs       */
+  int64_t node_nnz_total;      /* node CSR nnz over all ranks                                 */
+  int64_t elem_nnz_total;      /* element CSR nnz over all ranks (= arity * total elements)  */
+  int64_t sent_bytes;          /* payload bytes this rank sent to other ranks (step 3)        */
+  int64_t recv_bytes;          /* payload bytes it received                                   */
+  int64_t own_incidences;      /* incidences it kept (read in place, not exchanged)           */
+} mn_dist_info;
+
+/* Both CSR slices (node_slice, elem_slice: local offsets, slice offsets[0] = 0, hi - lo + 1
+ * entries; global node / element ids as indices).  Validation errors are global: every rank
+ * returns the lowest offending (global element id, position) of all shards.  A comm failure gives
+ * MN_ERR_COMM; a local failure (OOM, CUDA) on any rank gives that status on every rank if it
+ * happens before step 2, else on that rank only.  info may be NULL. */
+mn_status mn_find_neighbors_dist(mn_elem_type type, const int32_t* d_conn_shard, int64_t shard_elems,
+                                 int64_t global_elem_base, int64_t num_nodes, const mn_comm* comm,
+                                 const mn_allocator* alloc, mn_stream stream, mn_csr* node_slice,
+                                 mn_csr* elem_slice, mn_dist_info* info, mn_error_detail* err);
+
+/* SURVEY.md §8(b)'s single-output forms over an NCCL communicator (an ncclComm_t passed as void*,
+ * e.g. from mn_nccl_comm_init): the node (elem) slice of nodes [*lo, *hi) and its global offset
+ * *global_nnz_base. */
+mn_status mn_find_node_neighbors_dist(mn_elem_type type, const int32_t* d_conn_shard, int64_t shard_elems,
+                                      int64_t global_elem_base, int64_t num_nodes, void* nccl_comm,
+                                      const mn_allocator* alloc, mn_stream stream, mn_csr* slice, int64_t* lo,
+                                      int64_t* hi, int64_t* global_nnz_base, mn_error_detail* err);
+mn_status mn_find_elem_neighbors_dist(mn_elem_type type, const int32_t* d_conn_shard, int64_t shard_elems,
+                                      int64_t global_elem_base, int64_t num_nodes, void* nccl_comm,
+                                      const mn_allocator* alloc, mn_stream stream, mn_csr* slice, int64_t* lo,
+                                      int64_t* hi, int64_t* global_nnz_base, mn_error_detail* err);
+
+/* NCCL plumbing.  libnccl.so.2 is loaded on first use (dlopen; in a process that already loaded
+ * PyTorch's NCCL that same library is used); MN_ERR_COMM if it cannot be.  Bootstrap: rank 0 calls
+ * mn_nccl_get_unique_id, the caller broadcasts the 128 bytes (e.g. over a torch process group),
+ * every rank calls mn_nccl_comm_init on its own (current) device. */
+int mn_nccl_available(void);
+mn_status mn_nccl_get_unique_id(void* id128);
+mn_status mn_nccl_comm_init(const void* id128, int world, int rank, void** nccl_comm);
+mn_status mn_nccl_comm_destroy(void* nccl_comm);
+/* Fills *out with NCCL-backed exchange operations on nccl_comm (rank, world from the communicator). */
+mn_status mn_comm_from_nccl(void* nccl_comm, mn_comm* out);
+
+/* Host-only exchange plan of step 2 (used by mn_find_neighbors_dist; exported so the protocol can
+ * be checked without a GPU).  gathered: world rows of (2 + 2 * world) int64 each, row g =
+ * [error word of rank g, status of rank g, counts_g[0..world), row_counts_g[0..world)]
+ * where counts_g[h] / row_counts_g[h] are the incidences / rows rank g sends to rank h.  Writes
+ * recv_counts[g] = counts_g[rank] and recv_row_counts[g] = row_counts_g[rank] and returns the
+ * global outcome: the first nonzero status in rank order, else the error of the lowest error word
+ * (detail decoded into err), else MN_OK.  Error word: (global element << 5) | (repeated node << 4)
+ * | position, all ones when the shard is valid — so the lowest word is the lowest element, and
+ * within it a range error before a repeated node (reading R8). */
+mn_status mn_dist_plan(int world, int rank, const int64_t* gathered, int64_t* recv_counts,
+                       int64_t* recv_row_counts, mn_error_detail* err);
+
+/* Stream-ordered copy between any two buffers (cudaMemcpyDefault), then a sync of `stream`
+ * (host-staged exchange callbacks use it). */
+mn_status mn_memcpy_sync(void* dst, const void* src, size_t bytes, mn_stream stream);
 
 /* ---------------------------------------------------------------------------------------------
  * Algorithm selection for the element CSR (process-wide; results are identical either way).

@@ -23,7 +23,7 @@ __all__ = [
     "workspace_bytes", "node_key_bits", "node_key_bytes", "find_neighbors_chunked", "chunk_workspace_bytes",
     "emit_node_pairs", "emit_elem_pairs", "radix_sort_keys", "radix_sort_pairs_u32",
     "unique_node_csr", "elem_offsets", "exclusive_scan",
-    "dist_bucket", "dist_finish",
+    "dist_bucket", "dist_finish", "find_neighbors_dist_comm", "find_neighbors_dist_nccl", "dist_plan",
     "launch_count", "profile_enable", "profile_reset", "profile_collect", "set_elem_path", "get_elem_path", "set_chunk_cap",
 ]
 
@@ -34,7 +34,7 @@ _NAMES = {"tri3": TRI3, "tri": TRI3, "quad4": QUAD4, "quad": QUAD4, "tet4": TET4
 
 MN_OK, MN_ERR_INVALID_ARG, MN_ERR_INDEX_OUT_OF_RANGE, MN_ERR_DEGENERATE = 0, 1, 2, 3
 MN_ERR_CAPACITY, MN_ERR_OOM, MN_ERR_CUDA, MN_ERR_ARITY = 4, 5, 6, 7
-MN_ERR_SYNTAX, MN_ERR_COUNT_MISMATCH, MN_ERR_ZERO_INDEX = 8, 9, 10
+MN_ERR_SYNTAX, MN_ERR_COUNT_MISMATCH, MN_ERR_ZERO_INDEX, MN_ERR_COMM = 8, 9, 10, 11
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 
@@ -77,9 +77,32 @@ class _ErrDetail(ctypes.Structure):
     _fields_ = [("elem", ctypes.c_int64), ("pos", ctypes.c_int32)]
 
 
-_lib = None
 _VP, _I64, _I32, _INT = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
 _P = ctypes.POINTER
+
+
+class A2AOp(ctypes.Structure):
+    """mn_a2a_op: one all-to-all(v) of a group (element counts / displacements per rank)."""
+    _fields_ = [("send", _VP), ("send_counts", _P(_I64)), ("send_displs", _P(_I64)), ("recv", _VP),
+                ("recv_counts", _P(_I64)), ("recv_displs", _P(_I64)), ("elem_bytes", ctypes.c_size_t)]
+
+
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, _VP, _VP, _VP, ctypes.c_size_t, _VP)
+ALLTOALLV_FN = ctypes.CFUNCTYPE(ctypes.c_int, _VP, _P(A2AOp), ctypes.c_int, _VP)
+
+
+class Comm(ctypes.Structure):
+    """mn_comm: the exchange operations of the multi-GPU path (include/meshnbr.h)."""
+    _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int), ("ctx", _VP), ("allgather", ALLGATHER_FN),
+                ("alltoallv", ALLTOALLV_FN)]
+
+
+class DistInfo(ctypes.Structure):
+    _fields_ = [("lo", _I64), ("hi", _I64), ("node_base", _I64), ("elem_base", _I64), ("node_nnz_total", _I64),
+                ("elem_nnz_total", _I64), ("sent_bytes", _I64), ("recv_bytes", _I64), ("own_incidences", _I64)]
+
+
+_lib = None
 
 
 def _declare(lib):
@@ -120,6 +143,19 @@ def _declare(lib):
                                _P(_I64), _P(_Allocator), _VP, _P(_ErrDetail)]),
         "mn_dist_finish": (S, [_INT, _VP, _I64, _VP, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _I64,
                                _P(_Allocator), _VP, _P(_Csr), _P(_Csr)]),
+        "mn_find_neighbors_dist": (S, [_INT, _VP, _I64, _I64, _I64, _P(Comm), _P(_Allocator), _VP, _P(_Csr),
+                                       _P(_Csr), _P(DistInfo), _P(_ErrDetail)]),
+        "mn_find_node_neighbors_dist": (S, [_INT, _VP, _I64, _I64, _I64, _VP, _P(_Allocator), _VP, _P(_Csr),
+                                            _P(_I64), _P(_I64), _P(_I64), _P(_ErrDetail)]),
+        "mn_find_elem_neighbors_dist": (S, [_INT, _VP, _I64, _I64, _I64, _VP, _P(_Allocator), _VP, _P(_Csr),
+                                            _P(_I64), _P(_I64), _P(_I64), _P(_ErrDetail)]),
+        "mn_nccl_available": (_INT, []),
+        "mn_nccl_get_unique_id": (S, [_VP]),
+        "mn_nccl_comm_init": (S, [_VP, _INT, _INT, _P(_VP)]),
+        "mn_nccl_comm_destroy": (S, [_VP]),
+        "mn_comm_from_nccl": (S, [_VP, _P(Comm)]),
+        "mn_dist_plan": (S, [_INT, _INT, _P(_I64), _P(_I64), _P(_I64), _P(_ErrDetail)]),
+        "mn_memcpy_sync": (S, [_VP, _VP, ctypes.c_size_t, _VP]),
         "mn_launch_count": (_I64, []),
         "mn_set_elem_path": (S, [_INT]),
         "mn_get_elem_path": (_INT, []),
@@ -580,6 +616,58 @@ def dist_finish(etype, pairs: torch.Tensor, row_elems: torch.Tensor, rows: torch
                                    ctypes.byref(ns), ctypes.byref(es))
     _check(rc)
     return _take(al, ns), _take(al, es)
+
+
+def find_neighbors_dist_comm(conn_shard: torch.Tensor, etype, global_elem_base: int, num_nodes: int, comm: Comm,
+                             stream=None):
+    """mn_find_neighbors_dist: this rank's node and element CSR slices over the exchange `comm`
+    (an mn_comm; see paper_1604_04689_b200.dist for NCCL / gloo ones).  Returns
+    (node (offsets, indices), elem (offsets, indices), DistInfo)."""
+    et = _etype(etype)
+    c, M = _conn_arg(conn_shard, et)
+    al = _TorchAllocator(c.device, stream)
+    ns, es, info, err = _Csr(), _Csr(), DistInfo(), _ErrDetail()
+    with torch.cuda.device(c.device):
+        rc = load().mn_find_neighbors_dist(et, c.data_ptr() if M else None, M, int(global_elem_base), int(num_nodes),
+                                           ctypes.byref(comm), ctypes.byref(al.struct), _stream_ptr(stream),
+                                           ctypes.byref(ns), ctypes.byref(es), ctypes.byref(info), ctypes.byref(err))
+    _check(rc, err)
+    return _take(al, ns), _take(al, es), info
+
+
+def find_neighbors_dist_nccl(conn_shard: torch.Tensor, etype, global_elem_base: int, num_nodes: int, nccl_comm,
+                             which: str = "node", stream=None):
+    """SURVEY §8(b)'s single-output forms (mn_find_node_neighbors_dist / mn_find_elem_neighbors_dist)
+    over a raw ncclComm_t handle.  Returns ((offsets, indices), lo, hi, global_nnz_base)."""
+    et = _etype(etype)
+    c, M = _conn_arg(conn_shard, et)
+    al = _TorchAllocator(c.device, stream)
+    out, err = _Csr(), _ErrDetail()
+    lo, hi, gb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    fn = load().mn_find_node_neighbors_dist if which == "node" else load().mn_find_elem_neighbors_dist
+    with torch.cuda.device(c.device):
+        rc = fn(et, c.data_ptr() if M else None, M, int(global_elem_base), int(num_nodes), nccl_comm,
+                ctypes.byref(al.struct), _stream_ptr(stream), ctypes.byref(out), ctypes.byref(lo), ctypes.byref(hi),
+                ctypes.byref(gb), ctypes.byref(err))
+    _check(rc, err)
+    return _take(al, out), int(lo.value), int(hi.value), int(gb.value)
+
+
+def dist_plan(world: int, rank: int, gathered):
+    """mn_dist_plan (host only): (status, recv_counts, recv_row_counts, err elem, err pos) from the
+    all-gathered int64 rows [error word, status, counts[world], row_counts[world]] of every rank."""
+    g = np.ascontiguousarray(np.asarray(gathered, dtype=np.int64).reshape(world, 2 + 2 * world))
+    rc = (ctypes.c_int64 * world)()
+    rr = (ctypes.c_int64 * world)()
+    err = _ErrDetail()
+    st = load().mn_dist_plan(int(world), int(rank), g.ctypes.data_as(_P(_I64)), rc, rr, ctypes.byref(err))
+    return int(st), list(rc), list(rr), int(err.elem), int(err.pos)
+
+
+def memcpy_sync(dst: int, src: int, nbytes: int, stream_ptr=None):
+    """Copy between raw device / host pointers (cudaMemcpyDefault) on the raw cudaStream_t
+    `stream_ptr`, then sync it (used by host-staged exchange callbacks)."""
+    _check(load().mn_memcpy_sync(ctypes.c_void_p(dst), ctypes.c_void_p(src), int(nbytes), ctypes.c_void_p(stream_ptr)))
 
 
 # ------------------------------------------------------------------------------------------------

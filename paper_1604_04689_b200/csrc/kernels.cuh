@@ -1837,17 +1837,31 @@ k_shift_offsets(const int64_t* __restrict__ in, int64_t n, int64_t base, int64_t
     out[i] = in[i] + base;
 }
 
+// The incidences an owner finishes, in source-rank order, as up to three pieces: those received
+// from lower ranks, its own bucket read in place from the bucketing output (never copied through
+// the exchange), those received from higher ranks.  Piece q covers positions [end[q-1], end[q]).
+struct PairSrc {
+  const uint64_t* p[3];
+  int64_t end[3];
+  __device__ __forceinline__ uint64_t at(int64_t j) const {
+    if (j < end[0]) return p[0][j];
+    if (j < end[1]) return p[1][j - end[0]];
+    return p[2][j - end[1]];
+  }
+};
+inline PairSrc pair_src(const uint64_t* pairs, int64_t n) { return PairSrc{{pairs, pairs, pairs}, {n, n, n}}; }
+
 // Multi-GPU finish, transpose form (received pairs are element-major, i.e. as coherent as conn):
 // distinct nodes per window of 32 consecutive pairs (locality sample), per-node counts, and the
 // warp-aggregated scatter of element ids (sorted per node afterwards by k_elem_segsort).
 __global__ void __launch_bounds__(256)
-k_pairs_locality(const uint64_t* __restrict__ pairs, int64_t n, unsigned long long* __restrict__ out) {
+k_pairs_locality(PairSrc pairs, int64_t n, unsigned long long* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t j = (int64_t)((double)n * (double)gw / (double)nw) + lane;
   const bool in = j < n;
-  const int64_t x = in ? (int64_t)(pairs[j] >> 32) : -1;   // one shared sentinel: match cost grows with distinct values
+  const int64_t x = in ? (int64_t)(pairs.at(j) >> 32) : -1;   // one shared sentinel: match cost grows with distinct values
   const unsigned peers = __match_any_sync(FULL, (unsigned long long)x);
   const unsigned g = __reduce_add_sync(FULL, (in && lane == __ffs(peers) - 1) ? 1u : 0u);
   const unsigned act = __popc(__ballot_sync(FULL, in));
@@ -1865,7 +1879,7 @@ k_pairs_locality(const uint64_t* __restrict__ pairs, int64_t n, unsigned long lo
 // by *ovf) counted buckets at cbase[x] with cursors `cur`.
 template <bool FIXED>
 __global__ void __launch_bounds__(256)
-k_pairs_chunk_scatter(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, int cap,
+k_pairs_chunk_scatter(PairSrc pairs, int64_t n, int64_t lo, int cap,
                       const int64_t* __restrict__ cbase, int32_t* __restrict__ cur, int32_t* __restrict__ belem,
                       uint8_t* __restrict__ bnode, unsigned int* __restrict__ ovf) {
   if (!FIXED && *ovf == 0u) return;
@@ -1874,7 +1888,7 @@ k_pairs_chunk_scatter(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo,
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
     const int64_t j = base + lane;
     const bool in = j < n;
-    const uint64_t p = in ? pairs[j] : 0;
+    const uint64_t p = in ? pairs.at(j) : 0;
     const int a = in ? (int)((int64_t)(p >> 32) - lo) : 0;
     const int x = in ? (a >> kChunkShift) : -1;   // one shared sentinel: match cost grows with distinct values
     const unsigned peers = __match_any_sync(FULL, x);
@@ -1895,7 +1909,7 @@ k_pairs_chunk_scatter(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo,
 
 // Fallback chunk counts of received pairs (guarded by *ovf).
 __global__ void __launch_bounds__(256)
-k_pairs_chunk_count(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, int32_t* __restrict__ ccnt,
+k_pairs_chunk_count(PairSrc pairs, int64_t n, int64_t lo, int32_t* __restrict__ ccnt,
                     const unsigned int* __restrict__ ovf) {
   if (*ovf == 0u) return;
   const int lane = threadIdx.x & 31;
@@ -1903,7 +1917,7 @@ k_pairs_chunk_count(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, i
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
     const int64_t j = base + lane;
     const bool in = j < n;
-    const int x = in ? (int)(((int64_t)(pairs[j] >> 32) - lo) >> kChunkShift) : -1;
+    const int x = in ? (int)(((int64_t)(pairs.at(j) >> 32) - lo) >> kChunkShift) : -1;
     const unsigned peers = __match_any_sync(FULL, x);
     if (in && lane == __ffs(peers) - 1) atomicAdd(ccnt + x, (int)__popc(peers));
   }
@@ -1911,10 +1925,10 @@ k_pairs_chunk_count(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, i
 
 // Multi-GPU finish: local node key and element-id payload of every received pair.
 __global__ void __launch_bounds__(256)
-k_local_keys(const uint64_t* __restrict__ pairs, int64_t n, int64_t lo, uint32_t* __restrict__ keys,
+k_local_keys(PairSrc pairs, int64_t n, int64_t lo, uint32_t* __restrict__ keys,
              uint32_t* __restrict__ elems) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t p = pairs[i];
+    const uint64_t p = pairs.at(i);
     keys[i] = (uint32_t)((int64_t)(p >> 32) - lo);
     elems[i] = (uint32_t)(p & 0xffffffffull);
   }

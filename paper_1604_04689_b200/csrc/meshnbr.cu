@@ -1590,7 +1590,10 @@ done:
 template <int T, int BINS>
 static mn_status dist_bucket_impl(const int32_t* conn, int64_t M, int64_t base, int64_t N, int world, int self,
                                   uint64_t* pairs, int64_t* hc, int32_t** relems_out, int32_t** rrows_out,
-                                  int64_t* hrc, Mem& mem, mn_error_detail* err) {
+                                  int64_t* hrc, Mem& mem, mn_error_detail* err, uint64_t* defer = nullptr) {
+  // defer != nullptr (mn_find_neighbors_dist): a validation failure is not returned but stored in
+  // *defer (the raw error word, ERR_NONE if none) with all counts 0, so this rank still joins the
+  // count exchange, where the lowest word over all ranks decides (every rank returns it)
   cudaStream_t s = mem.s;
   mn_status st = MN_OK;
   uint64_t* host = pinned_pair();
@@ -1652,6 +1655,14 @@ static mn_status dist_bucket_impl(const int32_t* conn, int64_t M, int64_t base, 
     MN_CUDA(cudaMemcpyAsync(hr.data(), rcnt, BINS * 8, cudaMemcpyDeviceToHost, s));
     MN_CUDA(cudaMemcpyAsync(host, errw, 8, cudaMemcpyDeviceToHost, s));
     MN_CUDA(cudaStreamSynchronize(s));
+    if (defer) {
+      *defer = host[0];
+      if (host[0] != ERR_NONE) {
+        for (int g = 0; g < world; ++g) hc[g] = hrc[g] = 0;
+        *relems_out = *rrows_out = nullptr;
+        goto done;
+      }
+    }
     st = decode_err(host[0], err);
     if (st != MN_OK) goto done;
     R = M > 0 ? (int64_t)host[1] : 0;
@@ -1684,7 +1695,7 @@ done:
 // become the indices in place), node CSR slice by the same per-node expansion + dedupe as the
 // single-GPU path, rows read from the own shard or, for remote elements, the received row table.
 template <int T>
-static mn_status dist_finish_impl(const uint64_t* pairs, int64_t n, const int32_t* relems, const int32_t* rrows,
+static mn_status dist_finish_impl(const PairSrc& pairs, int64_t n, const int32_t* relems, const int32_t* rrows,
                                   int64_t nr, const int32_t* shard, int64_t shard_base, int64_t shard_m, int64_t N,
                                   int64_t lo, int64_t hi, Mem& mem, mn_csr* node_slice, mn_csr* elem_slice) {
   cudaStream_t s = mem.s;
@@ -1869,6 +1880,8 @@ done:
   return st;
 }
 
+#include "dist.cuh"
+
 }  // namespace mn
 
 // ==================================================================================================
@@ -1893,6 +1906,7 @@ const char* mn_status_string(mn_status s) {
     case MN_ERR_SYNTAX: return "mesh file syntax error";
     case MN_ERR_COUNT_MISMATCH: return "mesh file count mismatch";
     case MN_ERR_ZERO_INDEX: return "OBJ face index 0";
+    case MN_ERR_COMM: return "multi-GPU exchange failed (NCCL / mn_comm)";
   }
   return "unknown status";
 }
@@ -2213,7 +2227,7 @@ mn_status mn_dist_finish(mn_elem_type t, const uint64_t* d_pairs, int64_t n, con
     return MN_ERR_INVALID_ARG;
   Mem mem(a, (cudaStream_t)stream);
 #define MN_DF(TT)                                                                                          \
-  return dist_finish_impl<TT>(d_pairs, n, d_row_elems, d_rows, n_rows, d_conn_shard, global_elem_base,   \
+  return dist_finish_impl<TT>(pair_src(d_pairs, n), n, d_row_elems, d_rows, n_rows, d_conn_shard, global_elem_base,   \
                               shard_elems, N, lo, hi, mem, node_slice, elem_slice)
   switch (t) {
     case MN_TRI3: MN_DF(MN_TRI3);
@@ -2222,6 +2236,117 @@ mn_status mn_dist_finish(mn_elem_type t, const uint64_t* d_pairs, int64_t n, con
     default: MN_DF(MN_HEX8);
   }
 #undef MN_DF
+}
+
+mn_status mn_find_neighbors_dist(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t base, int64_t N,
+                                 const mn_comm* comm, const mn_allocator* a, mn_stream stream, mn_csr* node_slice,
+                                 mn_csr* elem_slice, mn_dist_info* info, mn_error_detail* err) {
+  if (err) { err->elem = -1; err->pos = -1; }
+  if (t < 0 || t > 3 || M < 0 || N < 0 || N > INT32_MAX || base < 0 || !comm || !comm->allgather ||
+      !comm->alltoallv || comm->world < 1 || comm->world > 512 || comm->rank < 0 || comm->rank >= comm->world ||
+      !node_slice || !elem_slice || (M > 0 && !d_conn))
+    return MN_ERR_INVALID_ARG;
+  if (base + M > INT32_MAX) return MN_ERR_CAPACITY;
+  if (info) std::memset(info, 0, sizeof(*info));
+  Mem mem(a, (cudaStream_t)stream);
+  return dist_dispatch(t, d_conn, M, base, N, comm, mem, node_slice, elem_slice, info, err);
+}
+
+static mn_status dist_one(bool node, mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t base, int64_t N,
+                          void* nccl_comm, const mn_allocator* a, mn_stream stream, mn_csr* slice, int64_t* lo,
+                          int64_t* hi, int64_t* gbase, mn_error_detail* err) {
+  if (!slice) return MN_ERR_INVALID_ARG;
+  mn_comm c{};
+  mn_status st = mn_comm_from_nccl(nccl_comm, &c);
+  if (st != MN_OK) return st;
+  mn_csr ns{}, es{};
+  mn_dist_info info{};
+  st = mn_find_neighbors_dist(t, d_conn, M, base, N, &c, a, stream, &ns, &es, &info, err);
+  if (st != MN_OK) return st;
+  if (node) { *slice = ns; mn_csr_release(&es, stream); } else { *slice = es; mn_csr_release(&ns, stream); }
+  if (lo) *lo = info.lo;
+  if (hi) *hi = info.hi;
+  if (gbase) *gbase = node ? info.node_base : info.elem_base;
+  return MN_OK;
+}
+
+mn_status mn_find_node_neighbors_dist(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t base, int64_t N,
+                                      void* nccl_comm, const mn_allocator* a, mn_stream stream, mn_csr* slice,
+                                      int64_t* lo, int64_t* hi, int64_t* gbase, mn_error_detail* err) {
+  return dist_one(true, t, d_conn, M, base, N, nccl_comm, a, stream, slice, lo, hi, gbase, err);
+}
+
+mn_status mn_find_elem_neighbors_dist(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t base, int64_t N,
+                                      void* nccl_comm, const mn_allocator* a, mn_stream stream, mn_csr* slice,
+                                      int64_t* lo, int64_t* hi, int64_t* gbase, mn_error_detail* err) {
+  return dist_one(false, t, d_conn, M, base, N, nccl_comm, a, stream, slice, lo, hi, gbase, err);
+}
+
+int mn_nccl_available(void) { return nccl().ok ? 1 : 0; }
+
+mn_status mn_nccl_get_unique_id(void* id128) {
+  if (!id128) return MN_ERR_INVALID_ARG;
+  const NcclApi& n = nccl();
+  if (!n.ok) return MN_ERR_COMM;
+  ncclUniqueId id;
+  if (n.get_unique_id(&id) != ncclSuccess) return MN_ERR_COMM;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id128, &id, sizeof(id));
+  return MN_OK;
+}
+
+mn_status mn_nccl_comm_init(const void* id128, int world, int rank, void** nccl_comm) {
+  if (!id128 || !nccl_comm || world < 1 || rank < 0 || rank >= world) return MN_ERR_INVALID_ARG;
+  const NcclApi& n = nccl();
+  if (!n.ok) return MN_ERR_COMM;
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  ncclComm_t c = nullptr;
+  if (n.comm_init_rank(&c, world, id, rank) != ncclSuccess) return MN_ERR_COMM;
+  *nccl_comm = c;
+  return MN_OK;
+}
+
+mn_status mn_nccl_comm_destroy(void* nccl_comm) {
+  if (!nccl_comm) return MN_ERR_INVALID_ARG;
+  const NcclApi& n = nccl();
+  if (!n.ok) return MN_ERR_COMM;
+  return n.comm_destroy((ncclComm_t)nccl_comm) == ncclSuccess ? MN_OK : MN_ERR_COMM;
+}
+
+mn_status mn_comm_from_nccl(void* nccl_comm, mn_comm* out) {
+  if (!nccl_comm || !out) return MN_ERR_INVALID_ARG;
+  const NcclApi& n = nccl();
+  if (!n.ok) return MN_ERR_COMM;
+  int world = 0, rank = 0;
+  if (n.comm_count((ncclComm_t)nccl_comm, &world) != ncclSuccess ||
+      n.comm_user_rank((ncclComm_t)nccl_comm, &rank) != ncclSuccess)
+    return MN_ERR_COMM;
+  out->rank = rank;
+  out->world = world;
+  out->ctx = nccl_comm;
+  out->allgather = nccl_allgather_cb;
+  out->alltoallv = nccl_alltoallv_cb;
+  return MN_OK;
+}
+
+mn_status mn_dist_plan(int world, int rank, const int64_t* gathered, int64_t* recv_counts, int64_t* recv_row_counts,
+                       mn_error_detail* err) {
+  if (err) { err->elem = -1; err->pos = -1; }
+  if (world < 1 || rank < 0 || rank >= world || !gathered || !recv_counts || !recv_row_counts)
+    return MN_ERR_INVALID_ARG;
+  return dist_plan(world, rank, gathered, recv_counts, recv_row_counts, err);
+}
+
+mn_status mn_memcpy_sync(void* dst, const void* src, size_t bytes, mn_stream stream) {
+  if (bytes == 0) return MN_OK;
+  if (!dst || !src) return MN_ERR_INVALID_ARG;
+  if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream) != cudaSuccess ||
+      cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) {
+    cudaGetLastError();
+    return MN_ERR_CUDA;
+  }
+  return MN_OK;
 }
 
 int64_t mn_launch_count(void) { return g_launches.load(); }

@@ -1,34 +1,30 @@
 """Multi-GPU one-ring neighbours: one process per GPU, elements sharded.
 
-Each rank holds a contiguous element shard (global element base given).  Nodes are owned in
-contiguous ranges [r*ceil(N/G), (r+1)*ceil(N/G)).  Per call:
+The whole path runs inside the library call ``mn_find_neighbors_dist`` (include/meshnbr.h):
+validate + bucket the shard's incidences by owner rank, one all-gather of the counts (and of the
+validation words, so every rank returns the globally lowest error), one grouped all-to-all(v) of
+the remote incidences, remote element ids and their rows, the local finish (element CSR slice by a
+stable sort, node CSR slice by per-node expansion + dedupe), one all-gather of the slice nnz.
 
-  1. mn_dist_bucket   (CUDA)  validate the shard, create its (node, element) incidences and
-                              stably bucket them by owner rank (one onesweep pass, pairs created
-                              from conn); one row per (remote destination, element) goes along;
-  2. count exchange           all_to_all of the G (incidence, row) counts (NCCL over NVLink);
-  3. payload exchange         all_to_all(v) of the pairs, the remote element ids and their rows,
-                              received in source-rank order, so element ids stay ascending;
-  4. mn_dist_finish   (CUDA)  element CSR slice by a stable sort on the local node id; node CSR
-                              slice by the same per-node expansion + dedupe as the 1-GPU path, rows
-                              read from the own shard (local elements) or the received table.
-
-Only incidences travel (8 bytes each, plus 4(k+1) bytes per remote element row), never the 2E node
-pairs per element; with a spatially coherent numbering almost everything stays on its rank.
-The result on rank r is the CSR of nodes [lo_r, hi_r) with local offsets; concatenating the slices
-in rank order (offsets shifted by the preceding ranks' nnz, returned as ``*_base``) is
+Nodes are owned in contiguous ranges [r*ceil(N/G), (r+1)*ceil(N/G)); an owner's own incidences are
+read in place and never exchanged.  The result on rank r is the CSR of nodes [lo_r, hi_r) with
+local offsets; concatenating the slices in rank order (offsets shifted by ``*_base``) is
 bit-identical to the single-GPU CSR.
 
-``ops`` is the per-rank compute: the CUDA library by default.  The exchange logic is independent
-of it, which is what lets tests/test_dist_gloo.py drive this exact orchestration over the gloo
-backend on CPU with a test-side stand-in for the two CUDA calls.
+This module only supplies the library's exchange operations (an ``mn_comm``) for a torch process
+group: over NCCL (the product path: the library drives its own NCCL communicator, bootstrapped by
+broadcasting an ncclUniqueId over the group), or host-staged over gloo (several ranks sharing one
+GPU in tests, where NCCL cannot run).
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist
+
+from . import ALLGATHER_FN, ALLTOALLV_FN, Comm, _check, find_neighbors_dist_comm, load, memcpy_sync
 
 
 @dataclass
@@ -39,7 +35,11 @@ class DistResult:
     elem: tuple
     node_base: int       # global offset of this slice in the single-GPU node CSR
     elem_base: int
-    sent_pairs: int      # incidences this rank sent to other ranks (exchange volume)
+    sent_bytes: int      # payload bytes this rank sent to other ranks
+    recv_bytes: int      # payload bytes it received
+    own_incidences: int  # incidences it kept in place (not exchanged)
+    node_nnz_total: int
+    elem_nnz_total: int
 
 
 def owner_range(num_nodes: int, world: int, rank: int):
@@ -49,29 +49,112 @@ def owner_range(num_nodes: int, world: int, rank: int):
     return lo, hi
 
 
-class CudaOps:
-    """The product compute: libmeshnbr's two dist entry points."""
+class NcclComm:
+    """The library's own NCCL communicator for a torch process group (NVLink / NVSwitch)."""
 
-    @staticmethod
-    def bucket(conn_shard, etype, elem_base, num_nodes, world, rank):
-        from . import dist_bucket
-        return dist_bucket(conn_shard, etype, elem_base, num_nodes, world, rank)
+    def __init__(self, group=None):
+        lib = load()
+        if not lib.mn_nccl_available():
+            raise RuntimeError("libnccl.so.2 could not be loaded by libmeshnbr")
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        idt = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            _check(lib.mn_nccl_get_unique_id(ctypes.c_void_p(idt.data_ptr())))
+        dev = torch.device("cuda", torch.cuda.current_device())
+        buf = idt.to(dev) if dist.get_backend(group) == "nccl" else idt
+        dist.broadcast(buf, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        idt = buf.cpu()
+        self.handle = ctypes.c_void_p()
+        _check(lib.mn_nccl_comm_init(ctypes.c_void_p(idt.data_ptr()), world, rank, ctypes.byref(self.handle)))
+        self.struct = Comm()
+        _check(lib.mn_comm_from_nccl(self.handle, ctypes.byref(self.struct)))
 
-    @staticmethod
-    def finish(etype, pairs, row_elems, rows, conn_shard, elem_base, num_nodes, lo, hi):
-        from . import dist_finish
-        return dist_finish(etype, pairs, row_elems, rows, conn_shard, elem_base, num_nodes, lo, hi)
+    def close(self):
+        if self.handle:
+            load().mn_nccl_comm_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
 
 
-def _a2a(out, inp, out_splits, in_splits, group):
-    """all_to_all_single; with a gloo group and CUDA tensors the exchange is staged through host
-    memory (gloo has no CUDA all-to-all) — used to exercise the multi-rank path on one GPU."""
-    if inp.is_cuda and dist.get_backend(group) == "gloo":
-        host_out = torch.empty(out.shape, dtype=out.dtype)
-        dist.all_to_all_single(host_out, inp.cpu(), out_splits, in_splits, group=group)
-        out.copy_(host_out)
-    else:
-        dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+class HostComm:
+    """Host-staged exchange over a gloo group: the callbacks copy the library's device buffers to
+    host memory, run the gloo collective, and copy back (tests: several ranks sharing one GPU)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.struct = Comm()
+        self.struct.rank = dist.get_rank(group)
+        self.struct.world = dist.get_world_size(group)
+        self._ag = ALLGATHER_FN(self._allgather)
+        self._a2a = ALLTOALLV_FN(self._alltoallv)
+        self.struct.allgather = self._ag
+        self.struct.alltoallv = self._a2a
+
+    def _allgather(self, ctx, d_send, d_recv, nbytes, stream):
+        try:
+            world = self.struct.world
+            h = torch.empty(nbytes, dtype=torch.uint8)
+            memcpy_sync(h.data_ptr(), d_send, nbytes, stream)
+            outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(outs, h, group=self.group)
+            cat = torch.cat(outs)
+            memcpy_sync(d_recv, cat.data_ptr(), nbytes * world, stream)
+            return 0
+        except Exception:  # noqa: BLE001  (a failed exchange is MN_ERR_COMM in the library)
+            return 1
+
+    def _alltoallv(self, ctx, ops, n_ops, stream):
+        try:
+            world = self.struct.world
+            for o in range(n_ops):
+                op = ops[o]
+                eb = int(op.elem_bytes)
+                sc = [int(op.send_counts[g]) * eb for g in range(world)]
+                rc = [int(op.recv_counts[g]) * eb for g in range(world)]
+                send = torch.empty(sum(sc), dtype=torch.uint8)
+                pos = 0
+                for g in range(world):
+                    if sc[g]:
+                        memcpy_sync(send.data_ptr() + pos, op.send + int(op.send_displs[g]) * eb, sc[g], stream)
+                    pos += sc[g]
+                recv = torch.empty(sum(rc), dtype=torch.uint8)
+                dist.all_to_all_single(recv, send, rc, sc, group=self.group)
+                pos = 0
+                for g in range(world):
+                    if rc[g]:
+                        memcpy_sync(op.recv + int(op.recv_displs[g]) * eb, recv.data_ptr() + pos, rc[g], stream)
+                    pos += rc[g]
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+
+_COMMS = {}
+
+
+def comm_for(group=None):
+    """The cached mn_comm provider of a process group: NCCL for an NCCL group, host-staged for gloo."""
+    key = id(group) if group is not None else None
+    if key not in _COMMS:
+        _COMMS[key] = NcclComm(group) if dist.get_backend(group) == "nccl" else HostComm(group)
+    return _COMMS[key]
+
+
+def release_comms():
+    for c in _COMMS.values():
+        if isinstance(c, NcclComm):
+            c.close()
+    _COMMS.clear()
+
+
+def find_neighbors_dist(conn_shard: torch.Tensor, etype, global_elem_base: int, num_nodes: int,
+                        group=None, stream=None) -> DistResult:
+    """This rank's CSR slices through the C ABI (mn_find_neighbors_dist)."""
+    comm = comm_for(group)
+    node, elem, info = find_neighbors_dist_comm(conn_shard, etype, int(global_elem_base), int(num_nodes),
+                                                comm.struct, stream)
+    return DistResult(int(info.lo), int(info.hi), node, elem, int(info.node_base), int(info.elem_base),
+                      int(info.sent_bytes), int(info.recv_bytes), int(info.own_incidences),
+                      int(info.node_nnz_total), int(info.elem_nnz_total))
 
 
 def _all_gather(outs, inp, group):
@@ -82,43 +165,6 @@ def _all_gather(outs, inp, group):
             o.copy_(h)
     else:
         dist.all_gather(outs, inp, group=group)
-
-
-def find_neighbors_dist(conn_shard: torch.Tensor, etype, global_elem_base: int, num_nodes: int,
-                        group=None, ops=None) -> DistResult:
-    ops = ops or CudaOps
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    dev = conn_shard.device
-    pairs, count, relems, rows, rcount = ops.bucket(conn_shard, etype, int(global_elem_base), int(num_nodes),
-                                                   world, rank)
-    k = rows.shape[1] if rows.dim() == 2 else 1
-    # ---- count exchange: row g of `send` goes to rank g ----
-    send = torch.tensor([[count[g], rcount[g]] for g in range(world)], dtype=torch.int64, device=dev)
-    recv = torch.empty_like(send)
-    _a2a(recv.view(-1), send.reshape(-1), None, None, group)
-    recv = recv.reshape(world, 2).cpu()
-    rc, rr = recv[:, 0].tolist(), recv[:, 1].tolist()
-    # ---- payload exchange, received in source-rank order ----
-    pairs_in = torch.empty(sum(rc), dtype=torch.int64, device=dev)
-    relems_in = torch.empty(sum(rr), dtype=torch.int32, device=dev)
-    rows_in = torch.empty((sum(rr), k), dtype=torch.int32, device=dev)
-    _a2a(pairs_in, pairs, rc, list(count), group)
-    _a2a(relems_in, relems, rr, list(rcount), group)
-    _a2a(rows_in, rows, rr, list(rcount), group)
-    del pairs, relems, rows
-    lo, hi = owner_range(num_nodes, world, rank)
-    node, elem = ops.finish(etype, pairs_in, relems_in, rows_in, conn_shard, int(global_elem_base),
-                            num_nodes, lo, hi)
-    # ---- global bases of the slices (exclusive scan of the per-rank nnz) ----
-    mine = torch.tensor([node[1].numel(), elem[1].numel()], dtype=torch.int64, device=dev)
-    allv = [torch.empty_like(mine) for _ in range(world)]
-    _all_gather(allv, mine, group)
-    allv = torch.stack(allv).cpu()
-    node_base = int(allv[:rank, 0].sum())
-    elem_base = int(allv[:rank, 1].sum())
-    sent = sum(int(count[g]) for g in range(world) if g != rank)   # remote incidences
-    return DistResult(lo, hi, node, elem, node_base, elem_base, sent)
 
 
 def gather_global(res: DistResult, num_nodes: int, group=None):
@@ -147,3 +193,7 @@ def gather_global(res: DistResult, num_nodes: int, group=None):
         full_off = torch.cat(offs + [torch.tensor([total], dtype=torch.int64, device=off.device)])
         out.append((full_off, torch.cat(idxs)))
     return out[0], out[1]
+
+
+__all__ = ["DistResult", "owner_range", "NcclComm", "HostComm", "comm_for", "release_comms",
+           "find_neighbors_dist", "gather_global"]

@@ -113,6 +113,20 @@ def test_virtual_ranks_config5_shape_small(elem_path):
         assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
 
 
+@pytest.mark.slow
+def test_virtual_ranks_full_config5():
+    """Full config 5 (Kuhn 320^3, 196.6 M tets) as 8 virtual ranks on one GPU, through the stage
+    entry points: the concatenated slices equal the 1-GPU CSRs bit for bit."""
+    import paper_1604_04689_b200 as mn
+    et, conn, N = meshgen.make_config(5, device="cuda")
+    ref = mn.find_neighbors(conn, et, N)
+    ref = [(a.cpu(), b.cpu()) for a, b in ref]
+    torch.cuda.empty_cache()
+    got = _virtual_ranks(conn, et, N, 8)
+    for a, b in zip(ref, got):
+        assert torch.equal(a[0], b[0].cpu()) and torch.equal(a[1], b[1].cpu())
+
+
 def test_bucket_reports_invalid_with_global_ids():
     import paper_1604_04689_b200 as mn
     conn = torch.tensor([[0, 1, 2], [1, 2, 9]], dtype=torch.int32).cuda()
@@ -134,11 +148,27 @@ def test_nccl_world_size_one():
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
     try:
         conn, N = meshgen.kuhn_tets(12, device="cuda")
+        from paper_1604_04689_b200.dist import comm_for, release_comms
         res = find_neighbors_dist(conn, "tet4", 0, N)
         ref = mn.find_neighbors(conn, "tet4", N)
         assert (res.lo, res.hi) == (0, N)
         assert torch.equal(res.node[0], ref[0][0]) and torch.equal(res.node[1], ref[0][1])
         assert torch.equal(res.elem[0], ref[1][0]) and torch.equal(res.elem[1], ref[1][1])
+        assert res.sent_bytes == 0 and res.own_incidences == 4 * conn.shape[0]
+        assert (res.node_nnz_total, res.elem_nnz_total) == (ref[0][1].numel(), ref[1][1].numel())
+        # SURVEY §8(b)'s single-output forms over the raw ncclComm_t
+        h = comm_for().handle
+        (o, i), lo, hi, gb = mn.find_neighbors_dist_nccl(conn, "tet4", 0, N, h, "node")
+        assert (lo, hi, gb) == (0, N, 0) and torch.equal(o, ref[0][0]) and torch.equal(i, ref[0][1])
+        (o, i), lo, hi, gb = mn.find_neighbors_dist_nccl(conn, "tet4", 0, N, h, "elem")
+        assert (lo, hi, gb) == (0, N, 0) and torch.equal(o, ref[1][0]) and torch.equal(i, ref[1][1])
+        # a validation error comes back through the exchange's error reduction
+        bad = conn.clone()
+        bad[77, 2] = N + 3
+        with pytest.raises(mn.MeshError) as ei:
+            find_neighbors_dist(bad, "tet4", 0, N)
+        assert (ei.value.code, ei.value.elem, ei.value.pos) == (mn.MN_ERR_INDEX_OUT_OF_RANGE, 77, 2)
+        release_comms()
     finally:
         dist.destroy_process_group()
 
@@ -152,16 +182,33 @@ def _spawn_worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
-        conn, N = meshgen.relabel(*meshgen.hex_grid(14), 21, 22), 15 ** 3
+        ok = True
+        for et, (conn, N) in ((meshgen.HEX8, (meshgen.relabel(*meshgen.hex_grid(14), 21, 22), 15 ** 3)),
+                              (meshgen.TET4, meshgen.kuhn_tets(11))):
+            M = conn.shape[0]
+            s0, s1 = rank * M // world, (rank + 1) * M // world
+            res = find_neighbors_dist(conn[s0:s1].contiguous().cuda(), et, s0, N)
+            (no, ni), (eo, ei) = gather_global(res, N)
+            ro, ri = oracle.node_csr(et, conn, N)
+            so, si = oracle.elem_csr(et, conn, N)
+            ok &= (np.array_equal(no.cpu().numpy(), ro) and np.array_equal(ni.cpu().numpy(), ri)
+                   and np.array_equal(eo.cpu().numpy(), so) and np.array_equal(ei.cpu().numpy(), si))
+            ok &= res.node_nnz_total == len(ri) and res.elem_nnz_total == len(si)
+        # an invalid element in the last shard: every rank raises the same (global) error
+        conn, N = meshgen.kuhn_tets(6)
         M = conn.shape[0]
+        bad = conn.clone()
+        bad[M - 5, 1] = bad[M - 5, 0]
+        if world == 3:                 # a lower error in the middle shard
+            bad[M // 2, 3] = -4
         s0, s1 = rank * M // world, (rank + 1) * M // world
-        res = find_neighbors_dist(conn[s0:s1].contiguous().cuda(), "hex8", s0, N)
-        (no, ni), (eo, ei) = gather_global(res, N)
-        ro, ri = oracle.node_csr(meshgen.HEX8, conn, N)
-        so, si = oracle.elem_csr(meshgen.HEX8, conn, N)
-        ok = (np.array_equal(no.cpu().numpy(), ro) and np.array_equal(ni.cpu().numpy(), ri)
-              and np.array_equal(eo.cpu().numpy(), so) and np.array_equal(ei.cpu().numpy(), si))
-        q.put((rank, bool(ok), res.sent_pairs))
+        try:
+            find_neighbors_dist(bad[s0:s1].contiguous().cuda(), "tet4", s0, N)
+            ok = False
+        except mn.MeshError as e:
+            exp = (mn.MN_ERR_INDEX_OUT_OF_RANGE, M // 2, 3) if world == 3 else (mn.MN_ERR_DEGENERATE, M - 5, 1)
+            ok &= (e.code, e.elem, e.pos) == exp
+        q.put((rank, bool(ok), res.sent_bytes))
     except Exception as e:  # noqa: BLE001
         q.put((rank, False, repr(e)))
     finally:
@@ -170,8 +217,9 @@ def _spawn_worker(rank, world, port, q):
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_real_kernels_multi_rank_one_gpu(world):
-    """The product dist path (CUDA bucket/finish kernels) with `world` ranks sharing cuda:0; the
-    exchange goes through gloo (host-staged) since NCCL needs one GPU per rank."""
+    """The product dist path (mn_find_neighbors_dist through the C ABI) with `world` ranks sharing
+    cuda:0; the exchange callbacks are host-staged over gloo (NCCL needs one GPU per rank); the
+    globally lowest validation error is raised on every rank."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
