@@ -460,6 +460,19 @@ def run_ours(args):
         del r
     torch.cuda.synchronize()
 
+    mem_bound = None
+    if args.max_workspace_gb and not poly and world == 1:   # measured peak of the bounded mode
+        torch.cuda.synchronize()
+        mn.alloc_trace(True)
+        rr = step()
+        torch.cuda.synchronize()
+        peak, peak_ws, outb = mn.trace_peaks(mn.alloc_trace_take())
+        del rr
+        mem_bound = {"max_workspace_bytes": int(args.max_workspace_gb * 2**30), "peak_workspace_bytes": peak_ws,
+                     "peak_with_node_slices_bytes": peak, "output_bytes": outb,
+                     "node_ranges": chunks_used[-1],
+                     "source": "library allocation log (paper_1604_04689_b200.alloc_trace)"}
+
     # ---- parity gate: one more call, its outputs compared with the oracle's
     # node-range mode before anything is timed; also gives the output sizes for B_min ----
     r = step()
@@ -652,6 +665,7 @@ def run_ours(args):
             "roofline": roofline, "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "parity": parity,
             **({"exchange": exchange} if exchange else {}),
+            **({"memory_bound": mem_bound} if mem_bound else {}),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

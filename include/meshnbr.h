@@ -159,11 +159,16 @@ mn_status mn_find_neighbors_both(mn_elem_type type, const int32_t* d_conn, int64
                                  mn_csr* node_out, mn_csr* elem_out, mn_error_detail* err);
 
 /* Memory-bounded form of mn_find_neighbors_both (the device-memory cost the
- * paper names as its shortcoming, §3.2.2): the nodes are processed in K
- * contiguous ranges, K the smallest power of two whose per-range workspace estimate fits in
- * max_workspace_bytes (outputs not included), each range by the counting-sort transpose +
- * per-node expansion restricted to its nodes.  Same outputs as mn_find_neighbors_both; blocks
- * twice per range.  *chunks_used (nullable) receives K. */
+ * paper names as its shortcoming, §3.2.2): the nodes are processed in contiguous
+ * ranges, first K of them (K the smallest power of two whose per-range estimate,
+ * mn_chunk_workspace_bytes, fits), each by the counting-sort transpose + per-node expansion
+ * restricted to its nodes.  A range whose actual workspace (known after its count pass) exceeds
+ * max_workspace_bytes is halved until it fits, so the workspace never exceeds the budget except
+ * for a single node whose own incidences do (processed alone).  Not counted in the budget: the
+ * outputs, and the node-index slices of the finished ranges (node nnz in total), which are
+ * concatenated into the output at the end (2 x node nnz at that moment).  Same outputs as
+ * mn_find_neighbors_both; blocks twice per range.  *chunks_used (nullable) receives the number of
+ * ranges processed. */
 mn_status mn_find_neighbors_both_chunked(mn_elem_type type, const int32_t* d_conn, int64_t num_elems,
                                          int64_t num_nodes, size_t max_workspace_bytes,
                                          const mn_allocator* alloc, mn_stream stream, mn_csr* node_out,

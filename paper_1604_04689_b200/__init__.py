@@ -24,6 +24,7 @@ __all__ = [
     "emit_node_pairs", "emit_elem_pairs", "radix_sort_keys", "radix_sort_pairs_u32",
     "unique_node_csr", "elem_offsets", "exclusive_scan",
     "dist_bucket", "dist_finish", "find_neighbors_dist_comm", "find_neighbors_dist_nccl", "dist_plan",
+    "alloc_trace", "alloc_trace_take", "trace_peaks",
     "launch_count", "profile_enable", "profile_reset", "profile_collect", "set_elem_path", "get_elem_path", "set_chunk_cap",
 ]
 
@@ -190,6 +191,50 @@ def load():
 # ------------------------------------------------------------------------------------------------
 # torch caching allocator -> mn_allocator
 # ------------------------------------------------------------------------------------------------
+_TRACE = None   # allocation log of the library's device allocations (alloc_trace)
+
+
+def alloc_trace(enable: bool = True):
+    """Start (or stop) logging every device allocation / release the library makes through the
+    torch allocator: [("a", ptr, bytes) | ("r", ptr)] in call order (memory-bound checks)."""
+    global _TRACE
+    _TRACE = [] if enable else None
+
+
+def alloc_trace_take():
+    """The log since alloc_trace(True), and logging stopped."""
+    global _TRACE
+    t, _TRACE = _TRACE or [], None
+    return t
+
+
+def trace_peaks(trace):
+    """From an allocation log: (peak workspace bytes = the most bytes simultaneously live among
+    allocations released before the end, peak of the same excluding the allocations still live
+    when the last surviving allocation (the last output) was made, output bytes)."""
+    size, born, died = {}, {}, {}
+    for i, ev in enumerate(trace):
+        if ev[0] == "a":
+            size[(ev[1], i)] = ev[2]
+            born[ev[1]] = (ev[1], i)
+        else:
+            k = born.pop(ev[1], None)
+            if k is not None:
+                died[k] = i
+    outputs = [k for k in size if k not in died]
+    last_out = max((k[1] for k in outputs), default=-1)
+    late = {k for k in size if k in died and k[1] < last_out < died[k]}   # e.g. node-index slices
+    live = peak = live2 = peak2 = 0
+    order = sorted([(k[1], +1, k) for k in size if k in died] + [(died[k], -1, k) for k in died])
+    for _, sign, k in order:
+        live += sign * size[k]
+        peak = max(peak, live)
+        if k not in late:
+            live2 += sign * size[k]
+            peak2 = max(peak2, live2)
+    return peak, peak2, sum(size[k] for k in outputs)
+
+
 class _TorchAllocator:
     """Hands out torch uint8 CUDA tensors; keeps them alive until released or adopted."""
 
@@ -215,11 +260,15 @@ class _TorchAllocator:
             return None
         p = t.data_ptr()
         self.live[p] = t
+        if _TRACE is not None:
+            _TRACE.append(("a", p, int(nbytes)))
         return p
 
     def _release(self, ctx, ptr, stream):
         if ptr:
             self.live.pop(int(ptr), None)
+            if _TRACE is not None:
+                _TRACE.append(("r", int(ptr)))
 
     def adopt(self, ptr, count, dtype):
         """Take ownership of a library output as a typed tensor view."""

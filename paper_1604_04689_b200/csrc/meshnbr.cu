@@ -935,6 +935,12 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
   int64_t K = 1;
   while (K < P.N && chunk_workspace(P, K) > max_ws) K *= 2;
   if (chunks) *chunks = K;
+  // the K ranges, processed in ascending order from the back of `todo`; a range whose actual
+  // workspace (known after its count pass) exceeds max_ws is split in two, so the bound holds for
+  // every range except a single node whose own incidences exceed it (processed alone)
+  std::vector<std::pair<int64_t, int64_t>> todo;
+  for (int64_t k = K - 1; k >= 0; --k) todo.push_back({P.N * k / K, P.N * (k + 1) / K});
+  int64_t ranges = 0;
   int64_t* node_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
   int64_t* elem_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
   int32_t* elem_idx = P.Pe ? (int32_t*)mem.get((size_t)P.Pe * 4 + 16) : nullptr;
@@ -946,8 +952,9 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
   if (!node_off || !elem_off || (P.Pe && !elem_idx)) { st = MN_ERR_OOM; goto done; }
   MN_CUDA(cudaMemsetAsync(node_off, 0, (size_t)(P.N + 1) * 8, s));
   MN_CUDA(cudaMemsetAsync(elem_off, 0, (size_t)(P.N + 1) * 8, s));
-  for (int64_t k = 0; k < K && P.M > 0; ++k) {
-    const int64_t lo = P.N * k / K, hi = P.N * (k + 1) / K, nloc = hi - lo;
+  while (!todo.empty() && P.M > 0) {
+    const int64_t lo = todo.back().first, hi = todo.back().second, nloc = hi - lo;
+    todo.pop_back();
     if (nloc == 0) continue;
     Arena ar;
     unsigned long long* errw = ar.take<unsigned long long>(2);
@@ -992,6 +999,15 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
       st = decode_err(host[0], err);
       if (st != MN_OK) goto done;
       const int64_t Ie = (int64_t)host[1];
+      if (ar.off + (size_t)C * (size_t)Ie * 4 > max_ws && nloc > 1) {   // over budget: split the range
+        mem.put(ws);
+        ws = nullptr;
+        const int64_t mid = lo + nloc / 2;
+        todo.push_back({mid, hi});
+        todo.push_back({lo, mid});
+        continue;
+      }
+      ++ranges;
       int32_t* eslice = elem_idx + ebase;
       // (2) element slice: scatter + per-node sort, straight into the output
       temp = Ie ? (uint32_t*)mem.get((size_t)C * Ie * 4) : nullptr;
@@ -1088,6 +1104,7 @@ static mn_status chunked_both(const Plan& P, const int32_t* conn, Mem& mem, size
   for (auto& pr : parts) mem.put(pr.first);
   parts.clear();
   MN_CUDA(cudaStreamSynchronize(s));
+  if (chunks) *chunks = std::max<int64_t>(ranges, 1);
   node_out->num_nodes = P.N; node_out->nnz = nbase; node_out->offsets = node_off; node_out->indices = node_idx;
   node_out->owner = mem.a;
   elem_out->num_nodes = P.N; elem_out->nnz = P.Pe; elem_out->offsets = elem_off; elem_out->indices = elem_idx;

@@ -467,6 +467,65 @@ def test_chunked_full_size_config3_bit_equal():
         assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
 
 
+def _traced(fn):
+    m = mn()
+    torch.cuda.synchronize()
+    m.alloc_trace(True)
+    try:
+        out = fn()
+        torch.cuda.synchronize()
+    finally:
+        trace = m.alloc_trace_take()
+    return out, m.trace_peaks(trace)
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_workspace_estimate_fidelity(cfg):
+    """mn_workspace_bytes (the peak workspace the header promises) within +-10% of the peak the
+    library's allocation log shows for mn_find_neighbors_both (SPEC S:L468 estimate_memory)."""
+    et, conn, N = meshgen.make_config(cfg, device="cuda")
+    (res, (peak, _, outb)) = _traced(lambda: mn().find_neighbors(conn, et, N))
+    est = mn().workspace_bytes(et, conn.shape[0], N, 3)
+    assert 0.9 * peak <= est <= 1.1 * peak, (est, peak)
+    nnz = res[0][1].numel()
+    assert outb >= 4 * (nnz + 4 * conn.shape[0]) + 16 * N
+
+
+@pytest.mark.parametrize("cfg,budgets", [(3, [1 << 26, 1 << 28]), (5, [1 << 30, 3 << 30])])
+def test_chunked_respects_budget(cfg, budgets):
+    """The memory-bounded mode: the workspace the allocation log
+    shows never exceeds max_workspace_bytes (outputs and the finished ranges' node-index slices
+    excluded, as the header states), and the CSRs equal the unbounded call's."""
+    et, conn, N = meshgen.make_config(cfg, device="cuda")
+    ref = mn().find_neighbors(conn, et, N)
+    (free_peak, _, _) = _traced(lambda: mn().find_neighbors(conn, et, N))[1]
+    for budget in budgets:
+        (got, (peak, peak_ws, _)) = _traced(lambda: mn().find_neighbors_chunked(conn, et, N, budget))
+        assert peak_ws <= budget, (budget, peak_ws)
+        assert peak_ws < free_peak
+        assert peak - peak_ws <= 4 * ref[0][1].numel() + (1 << 20)   # only the node slices on top
+        for a, b in zip(ref, got[:2]):
+            assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+        del got
+    del ref
+
+
+def test_chunked_splits_uneven_ranges():
+    """A mesh whose incidences crowd into a few nodes (a 60,000-triangle fan plus a grid): ranges
+    over budget are halved, the bound holds, the result equals the oracle."""
+    fan, nf = meshgen.nonmanifold_fan(3000)
+    grid, ng = meshgen.tri_grid(60, 60)
+    conn = torch.cat([fan, grid + nf]).contiguous()
+    N = nf + ng
+    budget = 1 << 17
+    ((no, ni), (eo, ei), K), (peak, peak_ws, _) = _traced(
+        lambda: mn().find_neighbors_chunked(conn.cuda(), 0, N, budget))
+    assert K >= 2
+    assert peak_ws <= max(budget, 2 * 3000 * 4 + (1 << 16))   # single-node range: its own incidences
+    _assert_csr((no, ni), oracle.node_csr(0, conn, N), "uneven chunked node")
+    _assert_csr((eo, ei), oracle.elem_csr(0, conn, N), "uneven chunked elem")
+
+
 @pytest.mark.parametrize("ntri", [200, 60000])
 def test_chunked_fans_and_errors(ntri):
     conn, N = meshgen.nonmanifold_fan(ntri)
