@@ -417,6 +417,10 @@ int mn_get_elem_path(void);
  * depend on it; tests use a small cap to force that fallback.  MN_ERR_INVALID_ARG if cap < 0. */
 mn_status mn_set_chunk_cap(int cap);
 
+/* Development knob (process-wide): which variant of the node-gather kernel the fixed-type path
+ * launches (0 = default); variants give identical results and exist for A/B measurements. */
+mn_status mn_set_gather_variant(int variant);
+
 /* ---------------------------------------------------------------------------------------------
  * Instrumentation (bench only; not thread-safe)
  * ------------------------------------------------------------------------------------------- */

@@ -161,6 +161,7 @@ def _declare(lib):
         "mn_set_elem_path": (S, [_INT]),
         "mn_get_elem_path": (_INT, []),
         "mn_set_chunk_cap": (S, [_INT]),
+        "mn_set_gather_variant": (S, [_INT]),
         "mn_profile_enable": (None, [_INT]),
         "mn_profile_reset": (None, []),
         "mn_profile_collect": (_INT, []),
@@ -733,6 +734,11 @@ def set_elem_path(mode="auto"):
 def set_chunk_cap(cap: int = 0):
     """Test knob: cap the fixed chunk-bucket capacity of the transpose path (0 = auto; include/meshnbr.h)."""
     _check(load().mn_set_chunk_cap(int(cap)))
+
+
+def set_gather_variant(v: int = 0):
+    """Development knob: node-gather kernel variant for A/B measurements (include/meshnbr.h)."""
+    _check(load().mn_set_gather_variant(int(v)))
 
 
 def get_elem_path() -> str:

@@ -766,8 +766,13 @@ __device__ __forceinline__ void sort_small(uint32_t (*tab)[kNodeThreads], int t,
 // SM vs 4.19 on config 5 -- not kept)
 // >= 10 CTAs per SM (<= 48 registers) for arity <= 4: 4.48 vs 4.75 ms on config 5; hex keeps its
 // registers for the 8-int rows (48 registers: 3.25 vs 2.63 ms on config 4).  profiles/round1/sweep_gather_minb.txt
+// BATCHP: every candidate of a batch of B incidences looks up its home slot before any of them is
+// inserted (B * C independent shared loads in flight instead of a chain of dependent ones); the
+// candidates are then resolved in order against those values, re-reading a home slot only when an
+// earlier candidate of the same batch wrote it (tracked in a register mask), and probing on only
+// when the home slot holds another value.
 template <int T, bool ALIGNED, bool DIST = false, bool SHARED = false,
-          int MINB = (Elem<T>::K <= 4) ? 10 : 1>
+          int MINB = (Elem<T>::K <= 4) ? 10 : 1, bool BATCHP = false>
 __global__ void __launch_bounds__(kNodeThreads, MINB)
 k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, RowSrc rs,
                 int64_t N, uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, int32_t* __restrict__ lofs,
@@ -822,6 +827,56 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
 #pragma unroll
       for (int q = 0; q < B; ++q)
         if (e[q] >= 0) fetch_row<T, ALIGNED, DIST>(rs, e[q], row[q]);
+      if constexpr (BATCHP && !WIDE) {
+        constexpr bool simplex = (C == K - 1);
+        const int A = (int)(a + a_base);
+        // candidate c of incidence q (simplex: the row values != a, in order)
+        auto cand = [&](int q, int c) -> uint32_t {
+          if (simplex) {
+            bool passed = false;
+            uint32_t v = 0;
+#pragma unroll
+            for (int j = 0; j <= c; ++j) {
+              passed = passed || row[q][j] == A;
+              v = (uint32_t)(passed ? row[q][j + 1] : row[q][j]);
+            }
+            return v;
+          }
+          return pick<T>(row[q], nbr_local<T>(local_of<T>(row[q], A), c));
+        };
+        uint32_t cx[B][C];
+#pragma unroll
+        for (int q = 0; q < B; ++q)
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const uint32_t v = cand(q, c);
+            cx[q][c] = e[q] >= 0 ? tab[(v * 0x9E3779B1u) >> (32 - HB)][t] : v;
+          }
+        Mask wr = 0;   // slots written by this batch
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+          if (e[q] < 0) continue;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const uint32_t v = cand(q, c);
+            uint32_t h = (v * 0x9E3779B1u) >> (32 - HB);
+            uint32_t x = ((wr >> h) & 1) ? tab[h][t] : cx[q][c];
+            if (x != v && L <= MU) {   // at most MU + 1 entries: the set never fills
+              while (x != v && x != EMPTY) {
+                h = (h + 1) & (HS - 1);
+                x = tab[h][t];
+              }
+              if (x == EMPTY) {
+                tab[h][t] = v;
+                used |= Mask(1) << h;
+                wr |= Mask(1) << h;
+                ++L;
+              }
+            }
+          }
+        }
+        continue;
+      }
 #pragma unroll
       for (int q = 0; q < B; ++q) {
         if (e[q] < 0) continue;
