@@ -544,6 +544,23 @@ def run_ours(args):
     mn.profile_reset()
     value = M_total / (ms / 1e3)
 
+    # ---- latency of one call (small configs are launch/latency-bound: report microseconds) ----
+    latency = None
+    if world == 1 and not poly and args.outputs == "both" and not args.max_workspace_gb and M_total <= 20_000_000:
+        reps = 300 if M_total <= 100_000 else 50
+        c_med, c_min = mn.time_both(conn, et, N, reps=reps)
+        walls = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            r = mn.find_neighbors(conn, et, N)
+            torch.cuda.current_stream().synchronize()
+            walls.append((time.perf_counter() - t0) * 1e6)
+            del r
+        walls.sort()
+        latency = {"c_abi_median_us": c_med, "c_abi_min_us": c_min, "python_median_us": walls[len(walls) // 2],
+                   "reps": reps, "what": "host wall time per call, entry to return with both CSRs complete "
+                                         "(C ABI: mn_time_both, default allocator; python: find_neighbors + sync)"}
+
     # ---- roofline of the dominant kernel (live CUDA events on the launching stream) ----
     peak, peak_src = peaks()
     prof = sorted(prof, key=lambda e: -e["ms"])
@@ -666,6 +683,7 @@ def run_ours(args):
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "parity": parity,
             **({"exchange": exchange} if exchange else {}),
             **({"memory_bound": mem_bound} if mem_bound else {}),
+            **({"latency": latency} if latency else {}),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

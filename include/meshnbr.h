@@ -417,6 +417,13 @@ int mn_get_elem_path(void);
  * depend on it; tests use a small cap to force that fallback.  MN_ERR_INVALID_ARG if cap < 0. */
 mn_status mn_set_chunk_cap(int cap);
 
+/* Small meshes (process-wide knob): with the automatic element path, fixed-type calls on meshes of
+ * at most `max_incidences` (<= 16384, default 16384) element-node incidences and <= 8192 nodes run
+ * in ONE CTA (validation, both transposes, the per-node sort + dedupe and both scans in shared
+ * memory), then one blocking read and one copy of the node lists (latency path, configs 1-like);
+ * identical results.  0 disables it.  Not used for _shared, _host or forced element paths. */
+mn_status mn_set_small_path(int64_t max_incidences);
+
 /* Development knob (process-wide): which variant of the node-gather kernel the fixed-type path
  * launches (0 = default); variants give identical results and exist for A/B measurements. */
 mn_status mn_set_gather_variant(int variant);
@@ -424,6 +431,14 @@ mn_status mn_set_gather_variant(int variant);
 /* ---------------------------------------------------------------------------------------------
  * Instrumentation (bench only; not thread-safe)
  * ------------------------------------------------------------------------------------------- */
+/* Latency of the C-ABI call: runs mn_find_neighbors_both `reps` times back to back (after 2
+ * warm-up calls) with the default allocator (cudaMallocAsync on `stream`; the current device's
+ * default pool is set to keep freed blocks) and reports the median (and minimum) host wall time
+ * per call in microseconds — from entry to return with both CSRs complete on `stream`, the one
+ * blocking read included.  Outputs are released after each call. */
+mn_status mn_time_both(mn_elem_type type, const int32_t* d_conn, int64_t num_elems, int64_t num_nodes, int reps,
+                       mn_stream stream, double* median_us, double* min_us);
+
 /* Count of kernels this library has launched since load. */
 int64_t mn_launch_count(void);
 /* When enabled, every kernel launch is bracketed by CUDA events on its stream. */

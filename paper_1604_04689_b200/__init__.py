@@ -162,6 +162,8 @@ def _declare(lib):
         "mn_get_elem_path": (_INT, []),
         "mn_set_chunk_cap": (S, [_INT]),
         "mn_set_gather_variant": (S, [_INT]),
+        "mn_set_small_path": (S, [_I64]),
+        "mn_time_both": (S, [_INT, _VP, _I64, _I64, _INT, _VP, _P(ctypes.c_double), _P(ctypes.c_double)]),
         "mn_profile_enable": (None, [_INT]),
         "mn_profile_reset": (None, []),
         "mn_profile_collect": (_INT, []),
@@ -734,6 +736,22 @@ def set_elem_path(mode="auto"):
 def set_chunk_cap(cap: int = 0):
     """Test knob: cap the fixed chunk-bucket capacity of the transpose path (0 = auto; include/meshnbr.h)."""
     _check(load().mn_set_chunk_cap(int(cap)))
+
+
+def time_both(conn: torch.Tensor, etype, num_nodes: int, reps: int = 200, stream=None):
+    """mn_time_both: (median, min) host wall microseconds per C-ABI mn_find_neighbors_both call."""
+    et = _etype(etype)
+    c, M = _conn_arg(conn, et)
+    med, mn_ = ctypes.c_double(), ctypes.c_double()
+    with torch.cuda.device(c.device):
+        _check(load().mn_time_both(et, c.data_ptr(), M, int(num_nodes), int(reps), _stream_ptr(stream),
+                                   ctypes.byref(med), ctypes.byref(mn_)))
+    return med.value, mn_.value
+
+
+def set_small_path(max_incidences: int = 16384):
+    """One-CTA latency path for small meshes (0 disables; include/meshnbr.h mn_set_small_path)."""
+    _check(load().mn_set_small_path(int(max_incidences)))
 
 
 def set_gather_variant(v: int = 0):

@@ -766,13 +766,13 @@ __device__ __forceinline__ void sort_small(uint32_t (*tab)[kNodeThreads], int t,
 // SM vs 4.19 on config 5 -- not kept)
 // >= 10 CTAs per SM (<= 48 registers) for arity <= 4: 4.48 vs 4.75 ms on config 5; hex keeps its
 // registers for the 8-int rows (48 registers: 3.25 vs 2.63 ms on config 4).  profiles/round1/sweep_gather_minb.txt
-// BATCHP: every candidate of a batch of B incidences looks up its home slot before any of them is
+// VAR 1: every candidate of a batch of B incidences looks up its home slot before any of them is
 // inserted (B * C independent shared loads in flight instead of a chain of dependent ones); the
 // candidates are then resolved in order against those values, re-reading a home slot only when an
 // earlier candidate of the same batch wrote it (tracked in a register mask), and probing on only
 // when the home slot holds another value.
 template <int T, bool ALIGNED, bool DIST = false, bool SHARED = false,
-          int MINB = (Elem<T>::K <= 4) ? 10 : 1, bool BATCHP = false>
+          int MINB = (Elem<T>::K <= 4) ? 10 : 1, int VAR = 0>
 __global__ void __launch_bounds__(kNodeThreads, MINB)
 k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, RowSrc rs,
                 int64_t N, uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, int32_t* __restrict__ lofs,
@@ -809,7 +809,11 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
       // the B incidences from one or two aligned 16-byte loads (half the L1 lookups of B scalar
       // loads; the element CSR allocations carry 16 bytes of padding for the window)
       int e[B];
-      {
+      if constexpr (VAR == 2) {   // B scalar loads (L1 hits mostly) instead of the aligned-window selects
+        const int n = d - i0 < B ? (int)(d - i0) : B;
+#pragma unroll
+        for (int q = 0; q < B; ++q) e[q] = q < n ? __ldg(inc + i0 + q) : -1;
+      } else {
         const int n = d - i0 < B ? (int)(d - i0) : B;
         const uintptr_t ad = reinterpret_cast<uintptr_t>(inc + i0);
         const int r = (int)((ad >> 2) & 3);
@@ -827,7 +831,7 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
 #pragma unroll
       for (int q = 0; q < B; ++q)
         if (e[q] >= 0) fetch_row<T, ALIGNED, DIST>(rs, e[q], row[q]);
-      if constexpr (BATCHP && !WIDE) {
+      if constexpr (VAR == 1 && !WIDE) {
         constexpr bool simplex = (C == K - 1);
         const int A = (int)(a + a_base);
         // candidate c of incidence q (simplex: the row values != a, in order)
@@ -877,6 +881,7 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
         }
         continue;
       }
+      const bool roomy = L + B * C <= HS - 2;   // (VAR >= 2) even B * C new values leave a free slot
 #pragma unroll
       for (int q = 0; q < B; ++q) {
         if (e[q] < 0) continue;
@@ -908,6 +913,19 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
                   h = (h + 1) & (HS - 1);
                   x = tab[h][t];
                 } while (x != v && x != EMPTY);
+              }
+              if (x == EMPTY) {
+                tab[h][t] = v;
+                used |= Mask(1) << h;
+                ++L;
+              }
+            }
+          } else if (VAR >= 2 && roomy) {   // this batch cannot fill the set: no per-candidate bound check
+            uint32_t x = tab[h][t];
+            if (x != v) {
+              while (x != EMPTY && x != v) {
+                h = (h + 1) & (HS - 1);
+                x = tab[h][t];
               }
               if (x == EMPTY) {
                 tab[h][t] = v;

@@ -12,6 +12,7 @@
 //   exact-size node indices + D2D copy         a6
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -20,6 +21,7 @@
 
 #include "kernels.cuh"
 #include "poly.cuh"
+#include "small.cuh"
 
 namespace mn {
 
@@ -31,6 +33,7 @@ static std::atomic<int64_t> g_launches{0};
 static std::atomic<int> g_elem_path{0};
 static std::atomic<int> g_chunk_cap{0};   // test knob: cap on the fixed chunk-bucket capacity (0 = auto)
 static std::atomic<int> g_gather_variant{0};   // dev knob: node-gather kernel variant (A/B measurements)
+static std::atomic<int64_t> g_small_max{kSmallMaxPe};   // incidences up to which the one-CTA path runs
 constexpr int64_t kTransposeMinElems = 1 << 20;
 constexpr int kMsdBins = 512;   // node ranges of the MSD element path
 constexpr double kTransposeMaxGroupRatio = 0.5;
@@ -833,10 +836,13 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
             k_node_gather_t<T, false, false, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs,
                                                                                giants, ngiant, errw);
           else if (aligned && g_gather_variant.load() == 1)
-            k_node_gather_t<T, true, false, false, (Elem<T>::K <= 4) ? 10 : 1, true><<<ng, kNodeThreads, 0, s>>>(
+            k_node_gather_t<T, true, false, false, (Elem<T>::K <= 4) ? 10 : 1, 1><<<ng, kNodeThreads, 0, s>>>(
                 eoff, eidx, rs, P.N, temp, cnt, lofs, giants, ngiant, errw);
           else if (aligned && g_gather_variant.load() == 2)
-            k_node_gather_t<T, true, false, false, 8, true><<<ng, kNodeThreads, 0, s>>>(
+            k_node_gather_t<T, true, false, false, (Elem<T>::K <= 4) ? 10 : 1, 2><<<ng, kNodeThreads, 0, s>>>(
+                eoff, eidx, rs, P.N, temp, cnt, lofs, giants, ngiant, errw);
+          else if (aligned && g_gather_variant.load() == 3)
+            k_node_gather_t<T, true, false, false, (Elem<T>::K <= 4) ? 10 : 1, 3><<<ng, kNodeThreads, 0, s>>>(
                 eoff, eidx, rs, P.N, temp, cnt, lofs, giants, ngiant, errw);
           else if (aligned)
             k_node_gather_t<T, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs, giants,
@@ -1146,9 +1152,87 @@ static mn_status check_args(int t, const void* conn, int64_t M, int64_t N) {
   return MN_OK;
 }
 
+// The one-CTA path (small.cuh).  *fallback = true (and nothing returned) when a node's lists are
+// too long for it; the caller then runs the staged path.
+template <int T>
+static mn_status small_path(const Plan& P, const int32_t* conn, Mem& mem, bool wn, bool we, mn_csr* no,
+                            mn_csr* eo, mn_error_detail* err, bool* fallback) {
+  cudaStream_t s = mem.s;
+  mn_status st = MN_OK;
+  *fallback = false;
+  uint64_t* host = pinned_pair();
+  if (!host) return MN_ERR_CUDA;
+  const bool aligned = ((uintptr_t)conn & 15) == 0;
+  const size_t smem = small_smem_bytes(P.N, P.Pe);
+  static PerDevice attr;
+  attr.once([&] {
+    cudaFuncSetAttribute(k_small_both<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)small_smem_bytes(kSmallMaxN, kSmallMaxPe));
+    cudaFuncSetAttribute(k_small_both<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)small_smem_bytes(kSmallMaxN, kSmallMaxPe));
+    return 0;
+  });
+  int64_t *node_off = nullptr, *elem_off = nullptr;
+  int32_t *elem_idx = nullptr, *node_idx = nullptr;
+  // workspace: ctrl words, candidate segments (C * Pe), packed node lists (C * Pe)
+  const size_t rawn = (size_t)P.C * (size_t)P.Pe;
+  char* ws = (char*)mem.get(64 + 8 * rawn);
+  unsigned long long* ctrl = (unsigned long long*)ws;
+  uint32_t* raw = (uint32_t*)(ws + 64);
+  uint32_t* fin = raw + rawn;
+  if (!ws) return MN_ERR_OOM;
+  if (wn) node_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
+  if (we) {
+    elem_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
+    elem_idx = (int32_t*)mem.get((size_t)P.Pe * 4 + 16);
+  }
+  if ((wn && !node_off) || (we && (!elem_off || !elem_idx))) { st = MN_ERR_OOM; goto done; }
+  MN_CUDA(launch("small_both", 4.0 * P.K * P.M + 8.0 * (P.N + 1) * ((wn ? 1 : 0) + (we ? 1 : 0)) +
+                                   (we ? 4.0 * P.Pe : 0.0), s, [&] {
+    if (aligned)
+      k_small_both<T, true><<<1, kSmallThreads, smem, s>>>(conn, (int)P.M, (int)P.N, elem_off, elem_idx, node_off,
+                                                            raw, fin, ctrl);
+    else
+      k_small_both<T, false><<<1, kSmallThreads, smem, s>>>(conn, (int)P.M, (int)P.N, elem_off, elem_idx, node_off,
+                                                             raw, fin, ctrl);
+  }));
+  MN_CUDA(cudaMemcpyAsync(host, ctrl, 24, cudaMemcpyDeviceToHost, s));
+  MN_CUDA(cudaStreamSynchronize(s));
+  st = decode_err(host[0], err);
+  if (st != MN_OK) goto done;
+  if (host[2]) { *fallback = true; goto done; }
+  if (wn) {
+    const int64_t U = (int64_t)host[1];
+    prof_add_bytes("small_both", 4.0 * U);
+    if (U) {
+      node_idx = (int32_t*)mem.get((size_t)U * 4);
+      if (!node_idx) { st = MN_ERR_OOM; goto done; }
+      MN_CUDA(cudaMemcpyAsync(node_idx, fin, (size_t)U * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    no->num_nodes = P.N; no->nnz = U; no->offsets = node_off; no->indices = node_idx; no->owner = mem.a;
+  }
+  if (we) {
+    eo->num_nodes = P.N; eo->nnz = P.Pe; eo->offsets = elem_off; eo->indices = elem_idx; eo->owner = mem.a;
+  }
+  mem.put(ws);
+  return MN_OK;
+done:
+  cudaStreamSynchronize(s);
+  mem.put(ws);
+  mem.put(node_off); mem.put(elem_off); mem.put(elem_idx); mem.put(node_idx);
+  if (wn && no) std::memset(no, 0, sizeof(*no));
+  if (we && eo) std::memset(eo, 0, sizeof(*eo));
+  return st;
+}
+
 template <int T>
 static mn_status dispatch_inc(const Plan& P, const int32_t* conn, Mem& mem, bool wn, bool we, mn_csr* no,
                               mn_csr* eo, mn_error_detail* err, HostSink* sink, bool shared) {
+  if (!sink && !shared && g_elem_path.load() == 0 && P.M > 0 && P.Pe <= g_small_max.load() && P.N <= kSmallMaxN) {
+    bool fallback = false;
+    const mn_status st = small_path<T>(P, conn, mem, wn, we, no, eo, err, &fallback);
+    if (!fallback) return st;
+  }
   if (P.bins == 256) return pipeline_inc<T, 256>(P, conn, mem, wn, we, no, eo, err, sink, shared);
   return pipeline_inc<T, 512>(P, conn, mem, wn, we, no, eo, err, sink, shared);
 }
@@ -2382,6 +2466,38 @@ mn_status mn_set_elem_path(int mode) {
 }
 
 int mn_get_elem_path(void) { return g_elem_path.load(); }
+
+mn_status mn_time_both(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N, int reps, mn_stream stream,
+                       double* median_us, double* min_us) {
+  if (reps < 1 || !median_us) return MN_ERR_INVALID_ARG;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, current_device()) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;   // keep freed blocks in the pool between calls
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  std::vector<double> us;
+  for (int r = 0; r < reps + 2; ++r) {   // 2 warm-up calls
+    mn_csr no{}, eo{};
+    const auto t0 = std::chrono::steady_clock::now();
+    const mn_status st = mn_find_neighbors_both(t, d_conn, M, N, nullptr, stream, &no, &eo, nullptr);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (st != MN_OK) return st;
+    mn_csr_release(&no, stream);
+    mn_csr_release(&eo, stream);
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return MN_ERR_CUDA;
+    if (r >= 2) us.push_back(std::chrono::duration<double, std::micro>(t1 - t0).count());
+  }
+  std::sort(us.begin(), us.end());
+  *median_us = us[us.size() / 2];
+  if (min_us) *min_us = us.front();
+  return MN_OK;
+}
+
+mn_status mn_set_small_path(int64_t max_incidences) {
+  if (max_incidences < 0) return MN_ERR_INVALID_ARG;
+  g_small_max.store(std::min<int64_t>(max_incidences, kSmallMaxPe));
+  return MN_OK;
+}
 
 mn_status mn_set_gather_variant(int v) {
   if (v < 0 || v > 7) return MN_ERR_INVALID_ARG;

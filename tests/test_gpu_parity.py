@@ -184,8 +184,9 @@ def test_row_a5_exclusive_scan(n):
 # ------------------------------------------------------------------------------------------------
 # whole path vs the std::set oracle
 # ------------------------------------------------------------------------------------------------
-@pytest.fixture(params=["radix", "transpose", "msd"])
+@pytest.fixture(params=["radix", "transpose", "msd", "auto"])
 def elem_path(request):
+    """Forced element paths use the staged pipeline; "auto" takes the one-CTA path on small meshes."""
     mn().set_elem_path(request.param)
     yield request.param
     mn().set_elem_path("auto")
@@ -576,3 +577,57 @@ def test_shared_equals_edges_for_simplices_full_size():
     a = mn().find_node_neighbors_shared(conn, et, N)
     b = mn().find_node_neighbors(conn, et, N)
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+# ------------------------------------------------------------------------------------------------
+# one-CTA latency path for small meshes (csrc/small.cuh)
+# ------------------------------------------------------------------------------------------------
+SMALL_PATH = [
+    ("tri_grid_32", meshgen.TRI3, lambda: meshgen.tri_grid(32, 32)),            # config 1
+    ("quad_grid_20x30", meshgen.QUAD4, lambda: meshgen.quad_grid(20, 30)),
+    ("kuhn_8", meshgen.TET4, lambda: meshgen.kuhn_tets(8)),
+    ("hex_10_perm", meshgen.HEX8, lambda: _perm_hex(10, 3, 5)),
+    ("rand_tri_dense", meshgen.TRI3, lambda: meshgen.random_mesh(meshgen.TRI3, 4000, 300, seed=21)),
+    ("rand_tet_isolated", meshgen.TET4, lambda: meshgen.random_mesh(meshgen.TET4, 500, 8000, seed=22)),
+    ("fan_70", meshgen.TRI3, lambda: meshgen.nonmanifold_fan(70)),
+    ("fan_500_fallback", meshgen.TRI3, lambda: meshgen.nonmanifold_fan(500)),   # hub degree > 160
+    ("single_tri", meshgen.TRI3, lambda: (torch.tensor([[2, 0, 1]], dtype=torch.int32), 5)),
+]
+
+
+@pytest.mark.parametrize("name,et,make", SMALL_PATH)
+def test_small_path_matches_oracle_and_staged(name, et, make):
+    conn, N = make()
+    m = mn()
+    m.set_elem_path("auto")
+    c = conn.cuda()
+    m.set_small_path(16384)
+    before = m.launch_count()
+    got = m.find_neighbors(c, et, N)
+    launched = m.launch_count() - before
+    m.set_small_path(0)
+    staged = m.find_neighbors(c, et, N)
+    m.set_small_path(16384)
+    _assert_csr(got[0], oracle.node_csr(et, conn, N), f"{name} small node")
+    _assert_csr(got[1], oracle.elem_csr(et, conn, N), f"{name} small elem")
+    for a, b in zip(got, staged):
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    if "fallback" not in name:
+        assert launched == 1, launched          # one kernel for both outputs
+    single = m.find_node_neighbors(c, et, N), m.find_elem_neighbors(c, et, N)
+    for a, b in zip(got, single):
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_small_path_validation():
+    """Errors on the one-CTA path: lowest element, range before repeated node (R8)."""
+    m = mn()
+    conn, N = meshgen.kuhn_tets(5)
+    bad = conn.clone()
+    bad[300, 2] = bad[300, 0]
+    bad[120, 3] = N
+    bad[120, 1] = bad[120, 0]
+    with pytest.raises(m.MeshError) as ei:
+        m.find_neighbors(bad.cuda(), "tet4", N)
+    assert (ei.value.code, ei.value.elem, ei.value.pos) == (m.MN_ERR_INDEX_OUT_OF_RANGE, 120, 3)
+    assert oracle.validate(meshgen.TET4, bad, N) == (oracle.ERR_RANGE, 120, 3)
