@@ -418,9 +418,10 @@ int mn_get_elem_path(void);
 mn_status mn_set_chunk_cap(int cap);
 
 /* Small meshes (process-wide knob): with the automatic element path, fixed-type calls on meshes of
- * at most `max_incidences` (<= 16384, default 16384) element-node incidences and <= 8192 nodes run
+ * at most `max_incidences` (<= 8192, default 8192) element-node incidences and <= 4096 nodes run
  * in ONE CTA (validation, both transposes, the per-node sort + dedupe and both scans in shared
- * memory), then one blocking read and one copy of the node lists (latency path, configs 1-like);
+ * memory; the node lists are written straight into the output, whose allocation then has capacity
+ * C * incidences >= nnz, at most 96 KB), then one blocking read (latency path, configs 1-like);
  * identical results.  0 disables it.  Not used for _shared, _host or forced element paths. */
 mn_status mn_set_small_path(int64_t max_incidences);
 

@@ -749,7 +749,7 @@ def time_both(conn: torch.Tensor, etype, num_nodes: int, reps: int = 200, stream
     return med.value, mn_.value
 
 
-def set_small_path(max_incidences: int = 16384):
+def set_small_path(max_incidences: int = 8192):
     """One-CTA latency path for small meshes (0 disables; include/meshnbr.h mn_set_small_path)."""
     _check(load().mn_set_small_path(int(max_incidences)))
 

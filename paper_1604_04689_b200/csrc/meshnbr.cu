@@ -1160,43 +1160,38 @@ static mn_status small_path(const Plan& P, const int32_t* conn, Mem& mem, bool w
   cudaStream_t s = mem.s;
   mn_status st = MN_OK;
   *fallback = false;
-  uint64_t* host = pinned_pair();
+  uint64_t* host = pinned_pair();   // the kernel writes (error, nnz, fallback) here directly
   if (!host) return MN_ERR_CUDA;
   const bool aligned = ((uintptr_t)conn & 15) == 0;
-  const size_t smem = small_smem_bytes(P.N, P.Pe);
+  const size_t smem = small_smem_bytes(P.N, P.Pe, P.C);
   static PerDevice attr;
   attr.once([&] {
-    cudaFuncSetAttribute(k_small_both<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)small_smem_bytes(kSmallMaxN, kSmallMaxPe));
-    cudaFuncSetAttribute(k_small_both<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)small_smem_bytes(kSmallMaxN, kSmallMaxPe));
+    const int mx = (int)small_smem_bytes(kSmallMaxN, kSmallMaxPe, 3);
+    cudaFuncSetAttribute(k_small_both<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_small_both<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     return 0;
   });
   int64_t *node_off = nullptr, *elem_off = nullptr;
   int32_t *elem_idx = nullptr, *node_idx = nullptr;
-  // workspace: ctrl words, candidate segments (C * Pe), packed node lists (C * Pe)
-  const size_t rawn = (size_t)P.C * (size_t)P.Pe;
-  char* ws = (char*)mem.get(64 + 8 * rawn);
-  unsigned long long* ctrl = (unsigned long long*)ws;
-  uint32_t* raw = (uint32_t*)(ws + 64);
-  uint32_t* fin = raw + rawn;
-  if (!ws) return MN_ERR_OOM;
-  if (wn) node_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
+  // node indices: one allocation of capacity C * Pe (<= 96 KB), filled in node order, nnz <= capacity
+  if (wn) {
+    node_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
+    node_idx = (int32_t*)mem.get((size_t)P.C * P.Pe * 4);
+  }
   if (we) {
     elem_off = (int64_t*)mem.get((size_t)(P.N + 1) * 8);
     elem_idx = (int32_t*)mem.get((size_t)P.Pe * 4 + 16);
   }
-  if ((wn && !node_off) || (we && (!elem_off || !elem_idx))) { st = MN_ERR_OOM; goto done; }
+  if ((wn && (!node_off || !node_idx)) || (we && (!elem_off || !elem_idx))) { st = MN_ERR_OOM; goto done; }
   MN_CUDA(launch("small_both", 4.0 * P.K * P.M + 8.0 * (P.N + 1) * ((wn ? 1 : 0) + (we ? 1 : 0)) +
                                    (we ? 4.0 * P.Pe : 0.0), s, [&] {
     if (aligned)
       k_small_both<T, true><<<1, kSmallThreads, smem, s>>>(conn, (int)P.M, (int)P.N, elem_off, elem_idx, node_off,
-                                                            raw, fin, ctrl);
+                                                            (uint32_t*)node_idx, (volatile unsigned long long*)host);
     else
       k_small_both<T, false><<<1, kSmallThreads, smem, s>>>(conn, (int)P.M, (int)P.N, elem_off, elem_idx, node_off,
-                                                             raw, fin, ctrl);
+                                                             (uint32_t*)node_idx, (volatile unsigned long long*)host);
   }));
-  MN_CUDA(cudaMemcpyAsync(host, ctrl, 24, cudaMemcpyDeviceToHost, s));
   MN_CUDA(cudaStreamSynchronize(s));
   st = decode_err(host[0], err);
   if (st != MN_OK) goto done;
@@ -1204,21 +1199,14 @@ static mn_status small_path(const Plan& P, const int32_t* conn, Mem& mem, bool w
   if (wn) {
     const int64_t U = (int64_t)host[1];
     prof_add_bytes("small_both", 4.0 * U);
-    if (U) {
-      node_idx = (int32_t*)mem.get((size_t)U * 4);
-      if (!node_idx) { st = MN_ERR_OOM; goto done; }
-      MN_CUDA(cudaMemcpyAsync(node_idx, fin, (size_t)U * 4, cudaMemcpyDeviceToDevice, s));
-    }
     no->num_nodes = P.N; no->nnz = U; no->offsets = node_off; no->indices = node_idx; no->owner = mem.a;
   }
   if (we) {
     eo->num_nodes = P.N; eo->nnz = P.Pe; eo->offsets = elem_off; eo->indices = elem_idx; eo->owner = mem.a;
   }
-  mem.put(ws);
   return MN_OK;
 done:
   cudaStreamSynchronize(s);
-  mem.put(ws);
   mem.put(node_off); mem.put(elem_off); mem.put(elem_idx); mem.put(node_idx);
   if (wn && no) std::memset(no, 0, sizeof(*no));
   if (we && eo) std::memset(eo, 0, sizeof(*eo));

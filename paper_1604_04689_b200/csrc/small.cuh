@@ -8,20 +8,22 @@
 //   a3n/a4 per node: its C * deg candidate neighbours (the rows of its elements), sorted and
 //         deduplicated in place (the paper's sort + adjacent difference, per segment)
 //   a5    exclusive scan of the distinct counts -> node-CSR offsets, lists packed
-// Then the one host read (error word, node nnz, fallback flag) and a copy of the packed node lists
-// into the exact-size output.  A node with more than kSmallMaxCand candidates (or an element list
+// The node lists are packed straight into the node-index output (capacity C * Pe) and the kernel
+// writes (error word, node nnz, fallback flag) into pinned host memory: one launch, one sync.  A node with more than kSmallMaxCand candidates (or an element list
 // longer than kSmallMaxDeg) sets the fallback flag and the call reruns on the staged path.
 #pragma once
 
 namespace mn {
 
 constexpr int kSmallThreads = 1024;
-constexpr int64_t kSmallMaxN = 8192;          // nodes (3 int arrays of N in shared memory)
-constexpr int64_t kSmallMaxPe = 16384;        // incidences (element lists in shared memory)
+constexpr int64_t kSmallMaxN = 4096;          // nodes (3 int arrays of N + 1 in shared memory)
+constexpr int64_t kSmallMaxPe = 8192;         // incidences (element lists + C * Pe candidates in smem)
 constexpr int kSmallMaxCand = 160;            // per-node candidates sorted by one thread
 constexpr int kSmallMaxDeg = 160;             // per-node element-list length sorted by one thread
 
-inline size_t small_smem_bytes(int64_t N, int64_t Pe) { return (size_t)(3 * (N + 1) + Pe + 64) * 4; }
+inline size_t small_smem_bytes(int64_t N, int64_t Pe, int C) {
+  return (size_t)(3 * (N + 1) + Pe + (int64_t)C * Pe + 64) * 4;
+}
 
 // In-place exclusive scan of a[0, n) (n <= 8 * blockDim), total to a[n]; all threads call it.
 __device__ __forceinline__ void small_block_scan(int* a, int n, int* wsum) {
@@ -73,25 +75,25 @@ __device__ __forceinline__ void small_isort(V* v, int n) {
   }
 }
 
-// ctrl[0] = error word (ERR_NONE if valid), ctrl[1] = node nnz, ctrl[2] = fallback flag.
-// raw: C * Pe entries (per-node candidate segments at C * eoff[v]); fin: the packed node lists.
+// ctrl (pinned host memory, written directly): [0] error word (ERR_NONE if valid), [1] node nnz,
+// [2] fallback flag.  fin: the node CSR indices (capacity C * Pe, packed in node order).
 template <int T, bool ALIGNED>
 __global__ void __launch_bounds__(kSmallThreads, 1)
 k_small_both(const int32_t* __restrict__ conn, int M, int N, int64_t* __restrict__ elem_off,
-             int32_t* __restrict__ elem_idx, int64_t* __restrict__ node_off, uint32_t* __restrict__ raw,
-             uint32_t* __restrict__ fin, unsigned long long* __restrict__ ctrl) {
+             int32_t* __restrict__ elem_idx, int64_t* __restrict__ node_off, uint32_t* __restrict__ fin,
+             volatile unsigned long long* __restrict__ ctrl) {
   constexpr int K = Elem<T>::K, C = Elem<T>::C;
   constexpr bool simplex = (C == K - 1);
   extern __shared__ int sm[];
   int* s_off = sm;                 // N + 1: counts -> element-CSR offsets
-  int* s_cur = s_off + N + 1;      // N + 1: scatter cursors, then node distinct counts -> offsets
-  int* s_ncnt = s_cur + N + 1;     // N + 1
+  int* s_cur = s_off + N + 1;      // N + 1: scatter cursors
+  int* s_ncnt = s_cur + N + 1;     // N + 1: node distinct counts -> node-CSR offsets
   int* s_el = s_ncnt + N + 1;      // Pe: element ids by node
+  uint32_t* raw = reinterpret_cast<uint32_t*>(s_el + M * K);   // C * Pe: candidate segments at C * eoff[v]
   __shared__ int s_ws[33];
   __shared__ unsigned long long s_err;
   __shared__ int s_big;
   const int t = threadIdx.x;
-  const int Pe = M * K;
   for (int v = t; v <= N; v += blockDim.x) s_off[v] = 0;
   if (t == 0) { s_err = ERR_NONE; s_big = 0; }
   __syncthreads();
@@ -121,7 +123,7 @@ k_small_both(const int32_t* __restrict__ conn, int M, int N, int64_t* __restrict
   }
   __syncthreads();
   if (s_err != ERR_NONE) {
-    if (t == 0) ctrl[0] = s_err;
+    if (t == 0) { ctrl[1] = 0; ctrl[2] = 0; __threadfence_system(); ctrl[0] = s_err; }
     return;
   }
   // ---- a5 (elements): offsets ----
@@ -189,9 +191,10 @@ k_small_both(const int32_t* __restrict__ conn, int M, int N, int64_t* __restrict
   }
   __syncthreads();
   if (t == 0) {
-    ctrl[0] = ERR_NONE;
     ctrl[1] = (node_off && !s_big) ? (unsigned long long)s_ncnt[N] : 0ull;
     ctrl[2] = s_big ? 1ull : 0ull;
+    __threadfence_system();
+    ctrl[0] = ERR_NONE;
   }
 }
 

@@ -585,10 +585,10 @@ def test_shared_equals_edges_for_simplices_full_size():
 SMALL_PATH = [
     ("tri_grid_32", meshgen.TRI3, lambda: meshgen.tri_grid(32, 32)),            # config 1
     ("quad_grid_20x30", meshgen.QUAD4, lambda: meshgen.quad_grid(20, 30)),
-    ("kuhn_8", meshgen.TET4, lambda: meshgen.kuhn_tets(8)),
+    ("kuhn_6", meshgen.TET4, lambda: meshgen.kuhn_tets(6)),
     ("hex_10_perm", meshgen.HEX8, lambda: _perm_hex(10, 3, 5)),
-    ("rand_tri_dense", meshgen.TRI3, lambda: meshgen.random_mesh(meshgen.TRI3, 4000, 300, seed=21)),
-    ("rand_tet_isolated", meshgen.TET4, lambda: meshgen.random_mesh(meshgen.TET4, 500, 8000, seed=22)),
+    ("rand_tri_dense", meshgen.TRI3, lambda: meshgen.random_mesh(meshgen.TRI3, 2500, 300, seed=21)),
+    ("rand_tet_isolated", meshgen.TET4, lambda: meshgen.random_mesh(meshgen.TET4, 500, 4000, seed=22)),
     ("fan_70", meshgen.TRI3, lambda: meshgen.nonmanifold_fan(70)),
     ("fan_500_fallback", meshgen.TRI3, lambda: meshgen.nonmanifold_fan(500)),   # hub degree > 160
     ("single_tri", meshgen.TRI3, lambda: (torch.tensor([[2, 0, 1]], dtype=torch.int32), 5)),
@@ -601,13 +601,13 @@ def test_small_path_matches_oracle_and_staged(name, et, make):
     m = mn()
     m.set_elem_path("auto")
     c = conn.cuda()
-    m.set_small_path(16384)
+    m.set_small_path(8192)
     before = m.launch_count()
     got = m.find_neighbors(c, et, N)
     launched = m.launch_count() - before
     m.set_small_path(0)
     staged = m.find_neighbors(c, et, N)
-    m.set_small_path(16384)
+    m.set_small_path(8192)
     _assert_csr(got[0], oracle.node_csr(et, conn, N), f"{name} small node")
     _assert_csr(got[1], oracle.elem_csr(et, conn, N), f"{name} small elem")
     for a, b in zip(got, staged):
