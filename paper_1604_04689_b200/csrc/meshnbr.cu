@@ -1216,7 +1216,8 @@ done:
 template <int T>
 static mn_status dispatch_inc(const Plan& P, const int32_t* conn, Mem& mem, bool wn, bool we, mn_csr* no,
                               mn_csr* eo, mn_error_detail* err, HostSink* sink, bool shared) {
-  if (!sink && !shared && g_elem_path.load() == 0 && P.M > 0 && P.Pe <= g_small_max.load() && P.N <= kSmallMaxN) {
+  if (!sink && !shared && g_elem_path.load() == 0 && P.M > 0 && P.Pe <= g_small_max.load() && P.N <= kSmallMaxN &&
+      small_smem_bytes(P.N, P.Pe, P.C) <= small_smem_bytes(kSmallMaxN, kSmallMaxPe, 3)) {
     bool fallback = false;
     const mn_status st = small_path<T>(P, conn, mem, wn, we, no, eo, err, &fallback);
     if (!fallback) return st;

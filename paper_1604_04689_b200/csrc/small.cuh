@@ -22,7 +22,7 @@ constexpr int kSmallMaxCand = 160;            // per-node candidates sorted by o
 constexpr int kSmallMaxDeg = 160;             // per-node element-list length sorted by one thread
 
 inline size_t small_smem_bytes(int64_t N, int64_t Pe, int C) {
-  return (size_t)(3 * (N + 1) + Pe + (int64_t)C * Pe + 64) * 4;
+  return (size_t)(3 * (N + 1) + 2 * Pe + (int64_t)C * Pe + 64) * 4;
 }
 
 // In-place exclusive scan of a[0, n) (n <= 8 * blockDim), total to a[n]; all threads call it.
@@ -89,7 +89,8 @@ k_small_both(const int32_t* __restrict__ conn, int M, int N, int64_t* __restrict
   int* s_cur = s_off + N + 1;      // N + 1: scatter cursors
   int* s_ncnt = s_cur + N + 1;     // N + 1: node distinct counts -> node-CSR offsets
   int* s_el = s_ncnt + N + 1;      // Pe: element ids by node
-  uint32_t* raw = reinterpret_cast<uint32_t*>(s_el + M * K);   // C * Pe: candidate segments at C * eoff[v]
+  int* s_conn = s_el + M * K;      // Pe: the connectivity, read from global memory once
+  uint32_t* raw = reinterpret_cast<uint32_t*>(s_conn + M * K);   // C * Pe: candidate segments at C * eoff[v]
   __shared__ int s_ws[33];
   __shared__ unsigned long long s_err;
   __shared__ int s_big;
@@ -101,6 +102,8 @@ k_small_both(const int32_t* __restrict__ conn, int M, int N, int64_t* __restrict
   for (int e = t; e < M; e += blockDim.x) {
     int row[K];
     load_row<T, ALIGNED>(conn, e, row);
+#pragma unroll
+    for (int p = 0; p < K; ++p) s_conn[e * K + p] = row[p];
     int bad = -1, kind = 0;
 #pragma unroll
     for (int p = K - 1; p >= 0; --p)
@@ -134,21 +137,16 @@ k_small_both(const int32_t* __restrict__ conn, int M, int N, int64_t* __restrict
   }
   __syncthreads();
   // ---- a3e: element ids into their node segments, each segment sorted ----
-  for (int e = t; e < M; e += blockDim.x) {
-    int row[K];
-    load_row<T, ALIGNED>(conn, e, row);
-#pragma unroll
-    for (int p = 0; p < K; ++p) s_el[atomicAdd(&s_cur[row[p]], 1)] = e;
-  }
+  for (int i = t; i < M * K; i += blockDim.x) s_el[atomicAdd(&s_cur[s_conn[i]], 1)] = i / K;
   __syncthreads();
   for (int v = t; v < N; v += blockDim.x) {
     const int b = s_off[v], d = s_off[v + 1] - b;
     if (d > kSmallMaxDeg) { s_big = 1; continue; }
     small_isort(s_el + b, d);
-    if (elem_idx)
-      for (int i = 0; i < d; ++i) elem_idx[b + i] = s_el[b + i];
   }
   __syncthreads();
+  if (elem_idx)   // s_el is the element CSR's index array: one coalesced copy
+    for (int i = t; i < M * K; i += blockDim.x) elem_idx[i] = s_el[i];
   // ---- a3n + a4: per-node candidates, sorted, adjacent-difference dedupe ----
   if (node_off && !s_big) {
     for (int v = t; v < N; v += blockDim.x) {
@@ -157,7 +155,9 @@ k_small_both(const int32_t* __restrict__ conn, int M, int N, int64_t* __restrict
       int m = 0;
       for (int i = 0; i < d; ++i) {
         int row[K];
-        load_row<T, ALIGNED>(conn, s_el[b + i], row);
+        const int* r = s_conn + s_el[b + i] * K;
+#pragma unroll
+        for (int q = 0; q < K; ++q) row[q] = r[q];
         if (simplex) {
 #pragma unroll
           for (int q = 0; q < K; ++q)
