@@ -75,6 +75,21 @@ __device__ __forceinline__ void small_isort(V* v, int n) {
   }
 }
 
+// Sort + adjacent-difference dedupe of seg[0, m) (m <= NET) in registers; distinct values back to
+// seg[0, L).  Returns L.
+template <int NET>
+__device__ __forceinline__ int small_sort_unique(uint32_t* seg, int m) {
+  int32_t v[NET];
+#pragma unroll
+  for (int i = 0; i < NET; ++i) v[i] = i < m ? (int32_t)seg[i] : INT32_MAX;
+  oddeven_sort<NET>(v);
+  int L = 0;
+#pragma unroll
+  for (int i = 0; i < NET; ++i)
+    if (i < m && (i == 0 || v[i] != v[i - 1])) seg[L++] = (uint32_t)v[i];
+  return L;
+}
+
 // ctrl (pinned host memory, written directly): [0] error word (ERR_NONE if valid), [1] node nnz,
 // [2] fallback flag.  fin: the node CSR indices (capacity C * Pe, packed in node order).
 template <int T, bool ALIGNED>
@@ -142,7 +157,10 @@ k_small_both(const int32_t* __restrict__ conn, int M, int N, int64_t* __restrict
   for (int v = t; v < N; v += blockDim.x) {
     const int b = s_off[v], d = s_off[v + 1] - b;
     if (d > kSmallMaxDeg) { s_big = 1; continue; }
-    small_isort(s_el + b, d);
+    if (d <= 8) sort_segment<8>(s_el + b, d);
+    else if (d <= 16) sort_segment<16>(s_el + b, d);
+    else if (d <= 32) sort_segment<32>(s_el + b, d);
+    else small_isort(s_el + b, d);
   }
   __syncthreads();
   if (elem_idx)   // s_el is the element CSR's index array: one coalesced copy
@@ -171,6 +189,10 @@ k_small_both(const int32_t* __restrict__ conn, int M, int N, int64_t* __restrict
       int L = 0;
       if (m > kSmallMaxCand) {
         s_big = 1;
+      } else if (m <= 16) {
+        L = small_sort_unique<16>(seg, m);
+      } else if (m <= 32) {
+        L = small_sort_unique<32>(seg, m);
       } else {
         small_isort(seg, m);
         for (int i = 0; i < m; ++i)
