@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "kernels.cuh"
 #include "poly.cuh"
 #include "small.cuh"
@@ -51,10 +53,18 @@ static cudaEvent_t ev_get() {
   return e;
 }
 
+// NVTX ranges (nvtx3, header-only: a no-op unless a tool such as ncu / nsys is attached): one per
+// kernel launch (named as in the profiler table) and one per C-ABI entry point (NvtxScope).
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+
 template <class F>
 static cudaError_t launch(const char* name, double alg_bytes, cudaStream_t s, F&& f) {
   cudaEvent_t a = nullptr, b = nullptr;
   if (g_prof) { a = ev_get(); b = ev_get(); cudaEventRecord(a, s); }
+  const NvtxScope range(name);
   f();
   cudaError_t e = cudaGetLastError();
   if (g_prof) { cudaEventRecord(b, s); g_recs.push_back({name, a, b, alg_bytes}); }
@@ -1231,6 +1241,9 @@ static mn_status dispatch_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
 static mn_status find(int t, const int32_t* conn, int64_t M, int64_t N, const mn_allocator* a,
                       mn_stream stream, bool wn, bool we, mn_csr* no, mn_csr* eo, mn_error_detail* err,
                       bool sortpairs = false, HostSink* sink = nullptr, bool shared = false) {
+  const NvtxScope range(sortpairs ? "mn_find_node_neighbors_sortpairs" : shared ? "mn_find_node_neighbors_shared"
+                        : (wn && we) ? "mn_find_neighbors_both" : wn ? "mn_find_node_neighbors"
+                        : "mn_find_elem_neighbors");
   if (err) { err->elem = -1; err->pos = -1; }
   mn_status st = check_args(t, conn, M, N);
   if (st != MN_OK) return st;
@@ -2029,6 +2042,7 @@ mn_status mn_find_node_neighbors_shared(mn_elem_type t, const int32_t* d_conn, i
 mn_status mn_find_poly_neighbors(const int64_t* d_off, const int32_t* d_idx, int64_t num_elems, int64_t conn_len,
                                  int64_t num_nodes, const mn_allocator* a, mn_stream s, mn_csr* node_out,
                                  mn_csr* elem_out, mn_csr* shared_out, mn_error_detail* err) {
+  const NvtxScope range("mn_find_poly_neighbors");
   if (err) { err->elem = -1; err->pos = -1; }
   if (num_elems < 0 || conn_len < 0 || num_nodes < 0 || num_nodes > INT32_MAX) return MN_ERR_INVALID_ARG;
   if (num_elems > INT32_MAX || conn_len > INT32_MAX) return MN_ERR_CAPACITY;
@@ -2052,6 +2066,7 @@ mn_status mn_find_neighbors_both(mn_elem_type t, const int32_t* d_conn, int64_t 
 mn_status mn_find_neighbors_both_chunked(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N,
                                          size_t max_workspace_bytes, const mn_allocator* a, mn_stream stream,
                                          mn_csr* no, mn_csr* eo, int64_t* chunks_used, mn_error_detail* err) {
+  const NvtxScope range("mn_find_neighbors_both_chunked");
   if (err) { err->elem = -1; err->pos = -1; }
   mn_status st = check_args(t, d_conn, M, N);
   if (st != MN_OK) return st;
@@ -2069,6 +2084,7 @@ mn_status mn_find_neighbors_both_chunked(mn_elem_type t, const int32_t* d_conn, 
 mn_status mn_find_neighbors_both_host(mn_elem_type t, const int32_t* h_conn, int64_t M, int64_t N,
                                       const mn_allocator* dev_alloc, const mn_allocator* host_alloc,
                                       mn_stream stream, mn_csr* no, mn_csr* eo, mn_error_detail* err) {
+  const NvtxScope range("mn_find_neighbors_both_host");
   mn_status st = check_args(t, h_conn, M, N);
   if (st != MN_OK) return st;
   if (!host_alloc || !host_alloc->alloc || !no || !eo) return MN_ERR_INVALID_ARG;
@@ -2338,6 +2354,7 @@ mn_status mn_dist_finish(mn_elem_type t, const uint64_t* d_pairs, int64_t n, con
 mn_status mn_find_neighbors_dist(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t base, int64_t N,
                                  const mn_comm* comm, const mn_allocator* a, mn_stream stream, mn_csr* node_slice,
                                  mn_csr* elem_slice, mn_dist_info* info, mn_error_detail* err) {
+  const NvtxScope range("mn_find_neighbors_dist");
   if (err) { err->elem = -1; err->pos = -1; }
   if (t < 0 || t > 3 || M < 0 || N < 0 || N > INT32_MAX || base < 0 || !comm || !comm->allgather ||
       !comm->alltoallv || comm->world < 1 || comm->world > 512 || comm->rank < 0 || comm->rank >= comm->world ||
@@ -2458,6 +2475,7 @@ int mn_get_elem_path(void) { return g_elem_path.load(); }
 
 mn_status mn_time_both(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t N, int reps, mn_stream stream,
                        double* median_us, double* min_us) {
+  const NvtxScope range("mn_time_both");
   if (reps < 1 || !median_us) return MN_ERR_INVALID_ARG;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, current_device()) == cudaSuccess) {
