@@ -445,6 +445,28 @@ def test_full_size_config5_single_gpu():
     _assert_full(got_elem, (ro, ri), "config 5 elem CSR")
 
 
+@pytest.mark.slow
+def test_full_size_config5_lsd_paths():
+    """The paper-literal node pipeline (all 2.36e9 node pairs > 2^31 as u64 keys, 7 onesweep passes
+    with 54-bit look-back values and digit buckets > 2^30, then the look-back unique/compaction) and
+    the LSD element path at config-5 size, bit-equal to the default path (itself memcmp-checked
+    against the oracle in test_full_size_config5_single_gpu)."""
+    et, conn, N = meshgen.make_config(5, device="cuda")
+    ref_node, ref_elem = mn().find_neighbors(conn, et, N)
+    P = 12 * conn.shape[0]
+    assert P > 2 ** 31
+    off, idx = mn().find_node_neighbors_sortpairs(conn, et, N)
+    assert torch.equal(off, ref_node[0]) and torch.equal(idx, ref_node[1])
+    del off, idx
+    torch.cuda.empty_cache()
+    mn().set_elem_path("radix")
+    try:
+        eo, ei = mn().find_elem_neighbors(conn, et, N)
+    finally:
+        mn().set_elem_path("auto")
+    assert torch.equal(eo, ref_elem[0]) and torch.equal(ei, ref_elem[1])
+
+
 # ------------------------------------------------------------------------------------------------
 # memory-bounded (chunked) mode, SURVEY §8(f) row 4
 # ------------------------------------------------------------------------------------------------
