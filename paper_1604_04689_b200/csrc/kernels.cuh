@@ -350,6 +350,7 @@ k_onesweep(PassArgs pa) {
       }
       old = __shfl_sync(FULL, old, leader);
       dr[i] = d | ((old + __popc(pm[i] & lanemask_lt())) << 16);
+      __syncwarp();   // orders this leader's histogram write before the next item's read by another lane
     }
   } else {
 #pragma unroll
@@ -365,6 +366,7 @@ k_onesweep(PassArgs pa) {
       }
       old = __shfl_sync(FULL, old, leader);
       dr[i] = d | ((old + __popc(peers & lanemask_lt())) << 16);
+      __syncwarp();   // (as above)
     }
   }
   __syncthreads();
