@@ -366,6 +366,28 @@ mn_status mn_find_elem_neighbors_dist(mn_elem_type type, const int32_t* d_conn_s
                                       const mn_allocator* alloc, mn_stream stream, mn_csr* slice, int64_t* lo,
                                       int64_t* hi, int64_t* global_nnz_base, mn_error_detail* err);
 
+/* Fused bucket-and-send over peer memory (the dispatch all-to-all done inside the bucketing kernel):
+ * the same result as mn_find_neighbors_dist, but step 3's all-to-all disappears — after the count
+ * exchange, the owner-digit onesweep pass stores each incidence (and, for remote owners, the element
+ * row) directly into its owner's receive region of a symmetric heap that every rank maps from every
+ * other rank with CUDA IPC (NVLink / NVSwitch peer memory on one node; processes sharing a device in
+ * tests).  Then one all-gather as a barrier, the local finish reading the heap in place, and the nnz
+ * all-gather.  The heap grows collectively when a call needs more (all ranks decide the same size
+ * from the all-gathered counts).  Single node only (CUDA IPC). */
+typedef struct mn_symm mn_symm;
+/* Collective over comm (only its allgather is used): every rank allocates `initial_bytes` (0 =
+ * on first use) with cudaMalloc and maps the others'.  comm is copied (its ctx must stay valid). */
+mn_status mn_symm_create(const mn_comm* comm, size_t initial_bytes, mn_symm** out);
+/* Teardown: mn_symm_unmap on every rank (closes the mappings of the other ranks' heaps), then a
+ * barrier of the caller's, then mn_symm_destroy (frees the own heap; unmaps first if needed). */
+mn_status mn_symm_unmap(mn_symm* symm);
+mn_status mn_symm_destroy(mn_symm* symm);
+size_t mn_symm_capacity(const mn_symm* symm);
+mn_status mn_find_neighbors_dist_p2p(mn_elem_type type, const int32_t* d_conn_shard, int64_t shard_elems,
+                                     int64_t global_elem_base, int64_t num_nodes, mn_symm* symm,
+                                     const mn_allocator* alloc, mn_stream stream, mn_csr* node_slice,
+                                     mn_csr* elem_slice, mn_dist_info* info, mn_error_detail* err);
+
 /* NCCL plumbing.  libnccl.so.2 is loaded on first use (dlopen; in a process that already loaded
  * PyTorch's NCCL that same library is used); MN_ERR_COMM if it cannot be.  Bootstrap: rank 0 calls
  * mn_nccl_get_unique_id, the caller broadcasts the 128 bytes (e.g. over a torch process group),

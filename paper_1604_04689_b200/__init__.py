@@ -23,7 +23,8 @@ __all__ = [
     "workspace_bytes", "node_key_bits", "node_key_bytes", "find_neighbors_chunked", "chunk_workspace_bytes",
     "emit_node_pairs", "emit_elem_pairs", "radix_sort_keys", "radix_sort_pairs_u32",
     "unique_node_csr", "elem_offsets", "exclusive_scan",
-    "dist_bucket", "dist_finish", "find_neighbors_dist_comm", "find_neighbors_dist_nccl", "dist_plan",
+    "dist_bucket", "dist_finish", "find_neighbors_dist_comm", "find_neighbors_dist_nccl", "find_neighbors_dist_p2p", "symm_create",
+    "symm_unmap", "symm_destroy", "dist_plan",
     "alloc_trace", "alloc_trace_take", "trace_peaks",
     "launch_count", "profile_enable", "profile_reset", "profile_collect", "set_elem_path", "get_elem_path", "set_chunk_cap",
 ]
@@ -150,6 +151,12 @@ def _declare(lib):
                                             _P(_I64), _P(_I64), _P(_I64), _P(_ErrDetail)]),
         "mn_find_elem_neighbors_dist": (S, [_INT, _VP, _I64, _I64, _I64, _VP, _P(_Allocator), _VP, _P(_Csr),
                                             _P(_I64), _P(_I64), _P(_I64), _P(_ErrDetail)]),
+        "mn_symm_create": (S, [_P(Comm), ctypes.c_size_t, _P(_VP)]),
+        "mn_symm_destroy": (S, [_VP]),
+        "mn_symm_unmap": (S, [_VP]),
+        "mn_symm_capacity": (ctypes.c_size_t, [_VP]),
+        "mn_find_neighbors_dist_p2p": (S, [_INT, _VP, _I64, _I64, _I64, _VP, _P(_Allocator), _VP, _P(_Csr),
+                                           _P(_Csr), _P(DistInfo), _P(_ErrDetail)]),
         "mn_nccl_available": (_INT, []),
         "mn_nccl_get_unique_id": (S, [_VP]),
         "mn_nccl_comm_init": (S, [_VP, _INT, _INT, _P(_VP)]),
@@ -683,6 +690,38 @@ def find_neighbors_dist_comm(conn_shard: torch.Tensor, etype, global_elem_base: 
         rc = load().mn_find_neighbors_dist(et, c.data_ptr() if M else None, M, int(global_elem_base), int(num_nodes),
                                            ctypes.byref(comm), ctypes.byref(al.struct), _stream_ptr(stream),
                                            ctypes.byref(ns), ctypes.byref(es), ctypes.byref(info), ctypes.byref(err))
+    _check(rc, err)
+    return _take(al, ns), _take(al, es), info
+
+
+def symm_create(comm: Comm, initial_bytes: int = 0):
+    """mn_symm_create (collective): the symmetric receive heap of the fused P2P path."""
+    h = ctypes.c_void_p()
+    _check(load().mn_symm_create(ctypes.byref(comm), int(initial_bytes), ctypes.byref(h)))
+    return h
+
+
+def symm_unmap(h):
+    _check(load().mn_symm_unmap(h))
+
+
+def symm_destroy(h):
+    _check(load().mn_symm_destroy(h))
+
+
+def find_neighbors_dist_p2p(conn_shard: torch.Tensor, etype, global_elem_base: int, num_nodes: int, symm,
+                            stream=None):
+    """mn_find_neighbors_dist_p2p: the fused bucket-and-send path over the symmetric heap `symm`.
+    Returns (node (offsets, indices), elem (offsets, indices), DistInfo)."""
+    et = _etype(etype)
+    c, M = _conn_arg(conn_shard, et)
+    al = _TorchAllocator(c.device, stream)
+    ns, es, info, err = _Csr(), _Csr(), DistInfo(), _ErrDetail()
+    with torch.cuda.device(c.device):
+        rc = load().mn_find_neighbors_dist_p2p(et, c.data_ptr() if M else None, M, int(global_elem_base),
+                                               int(num_nodes), symm, ctypes.byref(al.struct), _stream_ptr(stream),
+                                               ctypes.byref(ns), ctypes.byref(es), ctypes.byref(info),
+                                               ctypes.byref(err))
     _check(rc, err)
     return _take(al, ns), _take(al, es), info
 

@@ -207,6 +207,12 @@ struct PassArgs {
   uint32_t epoch;
   const unsigned long long* err;
   int32_t* counts;         // COUNTS mode: per-key run lengths (last element pass)
+  // P2P (fused multi-GPU bucketing, SRC 3): the items of owner digit d are stored at dst[d] + their
+  // rank in the bucket — a region of rank d's receive buffer, reached over NVLink peer memory — and
+  // for d != self the element's row goes to rowdst[d] + rank * K (rank d's row table)
+  uint64_t* const* dst;
+  int32_t* const* rowdst;
+  int self;
 };
 
 template <int THREADS, int ITEMS, int BINS>
@@ -248,7 +254,7 @@ __device__ __forceinline__ unsigned digit_peers(uint32_t d) {
 // the first look-back window requested before the (slower) stable ranking, so the look-back round
 // trip overlaps the ranking instead of following it (the "early counts" of onesweep).
 template <typename KeyT, int SRC, int T, bool PAYLOAD, bool OWNER, int BINS, int THREADS, int ITEMS,
-          int W = 4, int MINB = 3, int RANK = 0, bool COUNTS = false, bool EARLY = false>
+          int W = 4, int MINB = 3, int RANK = 0, bool COUNTS = false, bool EARLY = false, bool P2P = false>
 __global__ void __launch_bounds__(THREADS, MINB)
 k_onesweep(PassArgs pa) {
   constexpr int WARPS = THREADS / 32;
@@ -462,7 +468,23 @@ k_onesweep(PassArgs pa) {
     const int li = j * THREADS + tid;
     if (li < nvalid) {
       const KeyT k = skeys[li];
-      const uint64_t g = sm.gofs[digit_of<KeyT, OWNER>(k, pa.pd, BINS - 1)] + li;
+      const uint32_t dg = digit_of<KeyT, OWNER>(k, pa.pd, BINS - 1);
+      const uint64_t g = sm.gofs[dg] + li;
+      if constexpr (P2P) {
+        static_assert(SRC == 3 && OWNER, "P2P is the fused dist bucketing pass");
+        constexpr int K = Elem<T>::K;
+        const uint64_t r = g - pa.bases[dg];   // rank inside the bucket of owner dg
+        pa.dst[dg][r] = (uint64_t)k;
+        if ((int)dg != pa.self) {
+          const int64_t e = (int64_t)((uint64_t)k & 0xffffffffull) - pa.elem_base;
+          int row[K];
+          load_row<T, false>(pa.conn, e, row);
+          int32_t* rd = pa.rowdst[dg] + r * K;
+#pragma unroll
+          for (int q = 0; q < K; ++q) rd[q] = row[q];
+        }
+        continue;
+      }
       if (!COUNTS) kout[g] = k;
       if (PAYLOAD || SRC == 2) pa.vals_out[g] = svals[li];
       if (COUNTS) {

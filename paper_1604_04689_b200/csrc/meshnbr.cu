@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <new>
 #include <string>
 #include <vector>
 
@@ -2364,6 +2365,54 @@ mn_status mn_find_neighbors_dist(mn_elem_type t, const int32_t* d_conn, int64_t 
   if (info) std::memset(info, 0, sizeof(*info));
   Mem mem(a, (cudaStream_t)stream);
   return dist_dispatch(t, d_conn, M, base, N, comm, mem, node_slice, elem_slice, info, err);
+}
+
+mn_status mn_symm_create(const mn_comm* comm, size_t initial_bytes, mn_symm** out) {
+  if (!comm || !out || !comm->allgather || comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world)
+    return MN_ERR_INVALID_ARG;
+  mn_symm* h = new (std::nothrow) mn_symm();
+  if (!h) return MN_ERR_OOM;
+  h->comm = *comm;
+  h->dev = current_device();
+  h->peer.assign(comm->world, nullptr);
+  const mn_status st = initial_bytes ? symm_reserve(h, initial_bytes, nullptr) : MN_OK;
+  if (st != MN_OK) { mn_symm_destroy(h); return st; }
+  *out = h;
+  return MN_OK;
+}
+
+mn_status mn_symm_unmap(mn_symm* h) {
+  if (!h) return MN_ERR_INVALID_ARG;
+  for (int g = 0; g < (int)h->peer.size(); ++g) {
+    if (g != h->comm.rank && h->peer[g]) cudaIpcCloseMemHandle(h->peer[g]);
+    if (g != h->comm.rank) h->peer[g] = nullptr;
+  }
+  h->cap = 0;   // a later call re-maps (collectively) before any use
+  return MN_OK;
+}
+
+mn_status mn_symm_destroy(mn_symm* h) {
+  if (!h) return MN_ERR_INVALID_ARG;
+  mn_symm_unmap(h);
+  if (h->local) cudaFree(h->local);
+  delete h;
+  return MN_OK;
+}
+
+size_t mn_symm_capacity(const mn_symm* h) { return h ? h->cap : 0; }
+
+mn_status mn_find_neighbors_dist_p2p(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t base, int64_t N,
+                                     mn_symm* symm, const mn_allocator* a, mn_stream stream, mn_csr* node_slice,
+                                     mn_csr* elem_slice, mn_dist_info* info, mn_error_detail* err) {
+  const NvtxScope range("mn_find_neighbors_dist_p2p");
+  if (err) { err->elem = -1; err->pos = -1; }
+  if (t < 0 || t > 3 || M < 0 || N < 0 || N > INT32_MAX || base < 0 || !symm || !node_slice || !elem_slice ||
+      (M > 0 && !d_conn) || symm->comm.world > 512)
+    return MN_ERR_INVALID_ARG;
+  if (base + M > INT32_MAX) return MN_ERR_CAPACITY;
+  if (info) std::memset(info, 0, sizeof(*info));
+  Mem mem(a, (cudaStream_t)stream);
+  return dist_p2p_dispatch(t, d_conn, M, base, N, symm, mem, node_slice, elem_slice, info, err);
 }
 
 static mn_status dist_one(bool node, mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t base, int64_t N,

@@ -24,7 +24,8 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as dist
 
-from . import ALLGATHER_FN, ALLTOALLV_FN, Comm, _check, find_neighbors_dist_comm, load, memcpy_sync
+from . import (ALLGATHER_FN, ALLTOALLV_FN, Comm, _check, find_neighbors_dist_comm, find_neighbors_dist_p2p, load,
+               memcpy_sync, symm_create, symm_destroy, symm_unmap)
 
 
 @dataclass
@@ -139,7 +140,27 @@ def comm_for(group=None):
     return _COMMS[key]
 
 
+_SYMMS = {}
+
+
+def symm_for(group=None):
+    """The cached symmetric receive heap of a process group (created collectively on first use)."""
+    key = id(group) if group is not None else None
+    if key not in _SYMMS:
+        _SYMMS[key] = symm_create(comm_for(group).struct)
+    return _SYMMS[key]
+
+
 def release_comms():
+    """Collective teardown: every rank unmaps the other heaps, a barrier, then frees its own."""
+    for key, h in _SYMMS.items():
+        symm_unmap(h)
+    if _SYMMS:
+        torch.cuda.synchronize()
+        dist.barrier()
+    for h in _SYMMS.values():
+        symm_destroy(h)
+    _SYMMS.clear()
     for c in _COMMS.values():
         if isinstance(c, NcclComm):
             c.close()
@@ -147,11 +168,17 @@ def release_comms():
 
 
 def find_neighbors_dist(conn_shard: torch.Tensor, etype, global_elem_base: int, num_nodes: int,
-                        group=None, stream=None) -> DistResult:
-    """This rank's CSR slices through the C ABI (mn_find_neighbors_dist)."""
+                        group=None, stream=None, p2p: bool = False) -> DistResult:
+    """This rank's CSR slices through the C ABI: mn_find_neighbors_dist (bucket, NCCL all-to-all,
+    finish), or with p2p=True mn_find_neighbors_dist_p2p (the bucketing kernel stores straight into
+    the owners' symmetric heaps over peer memory)."""
     comm = comm_for(group)
-    node, elem, info = find_neighbors_dist_comm(conn_shard, etype, int(global_elem_base), int(num_nodes),
-                                                comm.struct, stream)
+    if p2p:
+        node, elem, info = find_neighbors_dist_p2p(conn_shard, etype, int(global_elem_base), int(num_nodes),
+                                                   symm_for(group), stream)
+    else:
+        node, elem, info = find_neighbors_dist_comm(conn_shard, etype, int(global_elem_base), int(num_nodes),
+                                                    comm.struct, stream)
     return DistResult(int(info.lo), int(info.hi), node, elem, int(info.node_base), int(info.elem_base),
                       int(info.sent_bytes), int(info.recv_bytes), int(info.own_incidences),
                       int(info.node_nnz_total), int(info.elem_nnz_total))
@@ -195,5 +222,5 @@ def gather_global(res: DistResult, num_nodes: int, group=None):
     return out[0], out[1]
 
 
-__all__ = ["DistResult", "owner_range", "NcclComm", "HostComm", "comm_for", "release_comms",
+__all__ = ["DistResult", "owner_range", "NcclComm", "HostComm", "comm_for", "symm_for", "release_comms",
            "find_neighbors_dist", "gather_global"]

@@ -165,15 +165,21 @@ def test_nccl_world_size_one():
         # a validation error comes back through the exchange's error reduction
         bad = conn.clone()
         bad[77, 2] = N + 3
-        with pytest.raises(mn.MeshError) as ei:
-            find_neighbors_dist(bad, "tet4", 0, N)
-        assert (ei.value.code, ei.value.elem, ei.value.pos) == (mn.MN_ERR_INDEX_OUT_OF_RANGE, 77, 2)
+        for p2p in (False, True):
+            with pytest.raises(mn.MeshError) as ei:
+                find_neighbors_dist(bad, "tet4", 0, N, p2p=p2p)
+            assert (ei.value.code, ei.value.elem, ei.value.pos) == (mn.MN_ERR_INDEX_OUT_OF_RANGE, 77, 2)
+        # the fused bucket-and-send path over the symmetric heap (world 1: the own heap only)
+        for _ in range(2):
+            res = find_neighbors_dist(conn, "tet4", 0, N, p2p=True)
+            assert torch.equal(res.node[0], ref[0][0]) and torch.equal(res.node[1], ref[0][1])
+            assert torch.equal(res.elem[0], ref[1][0]) and torch.equal(res.elem[1], ref[1][1])
         release_comms()
     finally:
         dist.destroy_process_group()
 
 
-def _spawn_worker(rank, world, port, q):
+def _spawn_worker(rank, world, port, q, p2p=False):
     import torch.distributed as dist
 
     import paper_1604_04689_b200 as mn
@@ -187,7 +193,7 @@ def _spawn_worker(rank, world, port, q):
                               (meshgen.TET4, meshgen.kuhn_tets(11))):
             M = conn.shape[0]
             s0, s1 = rank * M // world, (rank + 1) * M // world
-            res = find_neighbors_dist(conn[s0:s1].contiguous().cuda(), et, s0, N)
+            res = find_neighbors_dist(conn[s0:s1].contiguous().cuda(), et, s0, N, p2p=p2p)
             (no, ni), (eo, ei) = gather_global(res, N)
             ro, ri = oracle.node_csr(et, conn, N)
             so, si = oracle.elem_csr(et, conn, N)
@@ -203,11 +209,13 @@ def _spawn_worker(rank, world, port, q):
             bad[M // 2, 3] = -4
         s0, s1 = rank * M // world, (rank + 1) * M // world
         try:
-            find_neighbors_dist(bad[s0:s1].contiguous().cuda(), "tet4", s0, N)
+            find_neighbors_dist(bad[s0:s1].contiguous().cuda(), "tet4", s0, N, p2p=p2p)
             ok = False
         except mn.MeshError as e:
             exp = (mn.MN_ERR_INDEX_OUT_OF_RANGE, M // 2, 3) if world == 3 else (mn.MN_ERR_DEGENERATE, M - 5, 1)
             ok &= (e.code, e.elem, e.pos) == exp
+        from paper_1604_04689_b200.dist import release_comms
+        release_comms()
         q.put((rank, bool(ok), res.sent_bytes))
     except Exception as e:  # noqa: BLE001
         q.put((rank, False, repr(e)))
@@ -215,8 +223,9 @@ def _spawn_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("p2p", [False, True])
 @pytest.mark.parametrize("world", [2, 3])
-def test_real_kernels_multi_rank_one_gpu(world):
+def test_real_kernels_multi_rank_one_gpu(world, p2p):
     """The product dist path (mn_find_neighbors_dist through the C ABI) with `world` ranks sharing
     cuda:0; the exchange callbacks are host-staged over gloo (NCCL needs one GPU per rank); the
     globally lowest validation error is raised on every rank."""
@@ -227,7 +236,7 @@ def test_real_kernels_multi_rank_one_gpu(world):
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    procs = [ctx.Process(target=_spawn_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_spawn_worker, args=(r, world, port, q, p2p)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=300) for _ in range(world)]
