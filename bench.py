@@ -43,6 +43,9 @@ def parse():
                     help="memory-bounded mode (SURVEY §8(f) row 4): node ranges whose workspace fits this budget")
     ap.add_argument("--elem-path", default="auto", choices=["auto", "radix", "transpose"],
                     help="element-CSR algorithm (auto = locality test; see DESIGN.md §3.5)")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "a2a"],
+                    help="N>1: p2p = fused bucket-and-send into the owners' symmetric heaps over peer memory "
+                         "(mn_find_neighbors_dist_p2p); a2a = bucket, NCCL all-to-all, finish (mn_find_neighbors_dist)")
     ap.add_argument("--cpu-seconds", type=float, default=16.0, help="target oracle sample time")
     ap.add_argument("--no-parity", action="store_true", help="skip the pre-timing parity gate (profiling only)")
     return ap.parse_args()
@@ -428,10 +431,17 @@ def run_ours(args):
         def step():
             return mn.find_node_neighbors_shared(conn, et, N)
     elif world > 1:
-        from paper_1604_04689_b200.dist import find_neighbors_dist
+        from paper_1604_04689_b200.dist import find_neighbors_dist, symm_for
+        use_p2p = args.exchange == "p2p"
+        if use_p2p:
+            try:
+                symm_for()          # collective: the symmetric heaps, mapped on every rank
+            except mn.MeshError as e:
+                print(f"p2p exchange unavailable ({e}); using the NCCL all-to-all", file=sys.stderr)
+                use_p2p = False
 
         def step():
-            return find_neighbors_dist(conn, et, base, N)
+            return find_neighbors_dist(conn, et, base, N, p2p=use_p2p)
     elif args.max_workspace_gb:
         budget = int(args.max_workspace_gb * 2**30)
         chunks_used = []
@@ -498,8 +508,11 @@ def run_ours(args):
         xs = [torch.empty_like(x) for _ in range(world)]
         dist.all_gather(xs, x)
         xs = torch.stack(xs).cpu().tolist()
-        exchange = {"payload": "remote (node, element) incidences 8 B + remote element id and row 4(k+1) B; "
-                               "own incidences stay in place",
+        exchange = {"mode": "p2p: bucketing kernel stores into the owners' symmetric heaps (NVLink peer memory)"
+                            if use_p2p else "a2a: bucket, one grouped NCCL all-to-all, finish",
+                    "payload": ("remote incidence 8 B + its element row 4k B" if use_p2p else
+                                "remote (node, element) incidence 8 B + remote element id and row 4(k+1) B")
+                               + "; own incidences stay in place",
                     "sent_bytes_per_rank": [v[0] for v in xs], "recv_bytes_per_rank": [v[1] for v in xs],
                     "own_incidence_fraction": sum(v[2] for v in xs) / max(1, nnz[1]),
                     "backend": dist.get_backend()}
@@ -616,7 +629,7 @@ def run_ours(args):
 
             def estep():
                 c = host_conn.to(dev, non_blocking=True)
-                res = find_neighbors_dist(c, et, base, N)
+                res = find_neighbors_dist(c, et, base, N, p2p=use_p2p)
                 outs = []
                 for x in (*res.node, *res.elem):   # pinned, async D2H, one sync
                     h = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
@@ -688,6 +701,8 @@ def run_ours(args):
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        from paper_1604_04689_b200.dist import release_comms
+        release_comms()
         dist.barrier()
         dist.destroy_process_group()
     return 0
