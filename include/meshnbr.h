@@ -447,9 +447,6 @@ mn_status mn_set_chunk_cap(int cap);
  * identical results.  0 disables it.  Not used for _shared, _host or forced element paths. */
 mn_status mn_set_small_path(int64_t max_incidences);
 
-/* Development knob (process-wide): which variant of the node-gather kernel the fixed-type path
- * launches (0 = default); variants give identical results and exist for A/B measurements. */
-mn_status mn_set_gather_variant(int variant);
 
 /* ---------------------------------------------------------------------------------------------
  * Instrumentation (bench only; not thread-safe)

@@ -168,7 +168,6 @@ def _declare(lib):
         "mn_set_elem_path": (S, [_INT]),
         "mn_get_elem_path": (_INT, []),
         "mn_set_chunk_cap": (S, [_INT]),
-        "mn_set_gather_variant": (S, [_INT]),
         "mn_set_small_path": (S, [_I64]),
         "mn_time_both": (S, [_INT, _VP, _I64, _I64, _INT, _VP, _P(ctypes.c_double), _P(ctypes.c_double)]),
         "mn_profile_enable": (None, [_INT]),
@@ -791,11 +790,6 @@ def time_both(conn: torch.Tensor, etype, num_nodes: int, reps: int = 200, stream
 def set_small_path(max_incidences: int = 8192):
     """One-CTA latency path for small meshes (0 disables; include/meshnbr.h mn_set_small_path)."""
     _check(load().mn_set_small_path(int(max_incidences)))
-
-
-def set_gather_variant(v: int = 0):
-    """Development knob: node-gather kernel variant for A/B measurements (include/meshnbr.h)."""
-    _check(load().mn_set_gather_variant(int(v)))
 
 
 def get_elem_path() -> str:

@@ -790,13 +790,12 @@ __device__ __forceinline__ void sort_small(uint32_t (*tab)[kNodeThreads], int t,
 // SM vs 4.19 on config 5 -- not kept)
 // >= 10 CTAs per SM (<= 48 registers) for arity <= 4: 4.48 vs 4.75 ms on config 5; hex keeps its
 // registers for the 8-int rows (48 registers: 3.25 vs 2.63 ms on config 4).  profiles/round1/sweep_gather_minb.txt
-// VAR 1: every candidate of a batch of B incidences looks up its home slot before any of them is
-// inserted (B * C independent shared loads in flight instead of a chain of dependent ones); the
-// candidates are then resolved in order against those values, re-reading a home slot only when an
-// earlier candidate of the same batch wrote it (tracked in a register mask), and probing on only
-// when the home slot holds another value.
+// (Round 2 measured two attempts at a shorter probe chain slower and removed them: every candidate
+// of a 4-incidence batch loading its home slot before any insert, 5.07 vs 4.13 ms on config 5; a
+// per-batch instead of per-candidate set-capacity check with scalar incidence loads, 4.33-4.44 ms.
+// DESIGN.md §5.)
 template <int T, bool ALIGNED, bool DIST = false, bool SHARED = false,
-          int MINB = (Elem<T>::K <= 4) ? 10 : 1, int VAR = 0>
+          int MINB = (Elem<T>::K <= 4) ? 10 : 1>
 __global__ void __launch_bounds__(kNodeThreads, MINB)
 k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, RowSrc rs,
                 int64_t N, uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, int32_t* __restrict__ lofs,
@@ -833,11 +832,7 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
       // the B incidences from one or two aligned 16-byte loads (half the L1 lookups of B scalar
       // loads; the element CSR allocations carry 16 bytes of padding for the window)
       int e[B];
-      if constexpr (VAR == 2) {   // B scalar loads (L1 hits mostly) instead of the aligned-window selects
-        const int n = d - i0 < B ? (int)(d - i0) : B;
-#pragma unroll
-        for (int q = 0; q < B; ++q) e[q] = q < n ? __ldg(inc + i0 + q) : -1;
-      } else {
+      {
         const int n = d - i0 < B ? (int)(d - i0) : B;
         const uintptr_t ad = reinterpret_cast<uintptr_t>(inc + i0);
         const int r = (int)((ad >> 2) & 3);
@@ -855,57 +850,6 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
 #pragma unroll
       for (int q = 0; q < B; ++q)
         if (e[q] >= 0) fetch_row<T, ALIGNED, DIST>(rs, e[q], row[q]);
-      if constexpr (VAR == 1 && !WIDE) {
-        constexpr bool simplex = (C == K - 1);
-        const int A = (int)(a + a_base);
-        // candidate c of incidence q (simplex: the row values != a, in order)
-        auto cand = [&](int q, int c) -> uint32_t {
-          if (simplex) {
-            bool passed = false;
-            uint32_t v = 0;
-#pragma unroll
-            for (int j = 0; j <= c; ++j) {
-              passed = passed || row[q][j] == A;
-              v = (uint32_t)(passed ? row[q][j + 1] : row[q][j]);
-            }
-            return v;
-          }
-          return pick<T>(row[q], nbr_local<T>(local_of<T>(row[q], A), c));
-        };
-        uint32_t cx[B][C];
-#pragma unroll
-        for (int q = 0; q < B; ++q)
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            const uint32_t v = cand(q, c);
-            cx[q][c] = e[q] >= 0 ? tab[(v * 0x9E3779B1u) >> (32 - HB)][t] : v;
-          }
-        Mask wr = 0;   // slots written by this batch
-#pragma unroll
-        for (int q = 0; q < B; ++q) {
-          if (e[q] < 0) continue;
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            const uint32_t v = cand(q, c);
-            uint32_t h = (v * 0x9E3779B1u) >> (32 - HB);
-            uint32_t x = ((wr >> h) & 1) ? tab[h][t] : cx[q][c];
-            if (x != v && L <= MU) {   // at most MU + 1 entries: the set never fills
-              while (x != v && x != EMPTY) {
-                h = (h + 1) & (HS - 1);
-                x = tab[h][t];
-              }
-              if (x == EMPTY) {
-                tab[h][t] = v;
-                used |= Mask(1) << h;
-                wr |= Mask(1) << h;
-                ++L;
-              }
-            }
-          }
-        }
-        continue;
-      }
-      const bool roomy = L + B * C <= HS - 2;   // (VAR >= 2) even B * C new values leave a free slot
 #pragma unroll
       for (int q = 0; q < B; ++q) {
         if (e[q] < 0) continue;
@@ -937,19 +881,6 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
                   h = (h + 1) & (HS - 1);
                   x = tab[h][t];
                 } while (x != v && x != EMPTY);
-              }
-              if (x == EMPTY) {
-                tab[h][t] = v;
-                used |= Mask(1) << h;
-                ++L;
-              }
-            }
-          } else if (VAR >= 2 && roomy) {   // this batch cannot fill the set: no per-candidate bound check
-            uint32_t x = tab[h][t];
-            if (x != v) {
-              while (x != EMPTY && x != v) {
-                h = (h + 1) & (HS - 1);
-                x = tab[h][t];
               }
               if (x == EMPTY) {
                 tab[h][t] = v;

@@ -35,7 +35,6 @@ static std::atomic<int64_t> g_launches{0};
 // element-CSR algorithm: 0 = auto (locality test), 1 = LSD radix sort, 2 = counting-sort transpose
 static std::atomic<int> g_elem_path{0};
 static std::atomic<int> g_chunk_cap{0};   // test knob: cap on the fixed chunk-bucket capacity (0 = auto)
-static std::atomic<int> g_gather_variant{0};   // dev knob: node-gather kernel variant (A/B measurements)
 static std::atomic<int64_t> g_small_max{kSmallMaxPe};   // incidences up to which the one-CTA path runs
 constexpr int64_t kTransposeMinElems = 1 << 20;
 constexpr int kMsdBins = 512;   // node ranges of the MSD element path
@@ -846,15 +845,6 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
           else if (shared)
             k_node_gather_t<T, false, false, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs,
                                                                                giants, ngiant, errw);
-          else if (aligned && g_gather_variant.load() == 1)
-            k_node_gather_t<T, true, false, false, (Elem<T>::K <= 4) ? 10 : 1, 1><<<ng, kNodeThreads, 0, s>>>(
-                eoff, eidx, rs, P.N, temp, cnt, lofs, giants, ngiant, errw);
-          else if (aligned && g_gather_variant.load() == 2)
-            k_node_gather_t<T, true, false, false, (Elem<T>::K <= 4) ? 10 : 1, 2><<<ng, kNodeThreads, 0, s>>>(
-                eoff, eidx, rs, P.N, temp, cnt, lofs, giants, ngiant, errw);
-          else if (aligned && g_gather_variant.load() == 3)
-            k_node_gather_t<T, true, false, false, (Elem<T>::K <= 4) ? 10 : 1, 3><<<ng, kNodeThreads, 0, s>>>(
-                eoff, eidx, rs, P.N, temp, cnt, lofs, giants, ngiant, errw);
           else if (aligned)
             k_node_gather_t<T, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs, giants,
                                                                  ngiant, errw);
@@ -2555,11 +2545,6 @@ mn_status mn_set_small_path(int64_t max_incidences) {
   return MN_OK;
 }
 
-mn_status mn_set_gather_variant(int v) {
-  if (v < 0 || v > 7) return MN_ERR_INVALID_ARG;
-  g_gather_variant.store(v);
-  return MN_OK;
-}
 
 mn_status mn_set_chunk_cap(int cap) {
   if (cap < 0) return MN_ERR_INVALID_ARG;
