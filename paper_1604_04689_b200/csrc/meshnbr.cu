@@ -1,15 +1,23 @@
 // meshnbr.cu — host orchestration + C ABI of libmeshnbr.so (declared in include/meshnbr.h).
 //
-// Pipeline of mn_find_neighbors_both (DESIGN.md §"Path"):
-//   memset(status, tickets, err)               once per call
-//   k_hist_validate                            a1/a2 validation + digit histograms (reads conn)
-//   k_bucket_bases                             bucket bases of every LSD pass
-//   k_onesweep x 2*nd (node, pass 0 from conn) a1 + a3n
-//   k_unique_node                              a4 + a5 (node)
-//   k_onesweep x nd   (elem, pass 0 from conn) a2 + a3e
-//   k_elem_offsets                             a4 + a5 (elem; indices are the sorted payloads)
-//   D2H(err, nnz) + one stream sync            a6
-//   exact-size node indices + D2D copy         a6
+// mn_find_neighbors_both, fixed element types:
+//   small meshes (<= 8192 incidences, <= 4096 nodes):   k_small_both, one CTA, one blocking read
+//   otherwise:
+//     k_locality_sample (+ 1 blocking read)   choose the element-CSR algorithm (meshes >= 2^20 elements)
+//     element CSR, locality (config 5):       k_chunk_scatter_fixed (a1/a2 validation + one read of conn
+//                                             into fixed 128-node chunk buckets), k_scan_i32 (chunk
+//                                             bases), guarded counted fallback, k_chunk_sort (a3e/a4/a5)
+//     element CSR, no locality (config 4):    k_hist_validate, k_bucket_bases, k_onesweep x nd (LSD,
+//                                             pass 0 creates the pairs from conn, last pass writes the
+//                                             payloads + run lengths), k_scan_i32 (a5)
+//     node CSR:                               k_node_gather_t (a1/a3n/a4: per-node expansion of the
+//                                             element CSR, hash-set dedupe, register sort), k_node_giant,
+//                                             k_scan_i32 (a5)
+//     D2H(err, nnz) + one stream sync          a6
+//     exact-size node indices, k_node_compact  a6
+// The paper-literal node pipeline (all node pairs, LSD over 2b key bits, k_unique_node) is
+// mn_find_node_neighbors_sortpairs.  Polygons: poly.cuh; small meshes: small.cuh; multi-GPU:
+// dist.cuh (bucket + NCCL all-to-all, or the fused bucket-and-send over peer memory).
 #include <algorithm>
 #include <atomic>
 #include <chrono>
