@@ -266,3 +266,61 @@ def test_bench_multi_rank_path_one_gpu():
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["gpu_launches"] > 0 and line["roofline"]["achieved"] > 0
+
+
+def _edge_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import paper_1604_04689_b200 as mn
+    from paper_1604_04689_b200.dist import find_neighbors_dist, gather_global, release_comms
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        ok = True
+        cases = [
+            ("two tets, empty shards", meshgen.TET4, (torch.tensor([[0, 1, 2, 3], [1, 2, 3, 4]], dtype=torch.int32), 5)),
+            ("N < world", meshgen.TRI3, (torch.tensor([[0, 1, 2]], dtype=torch.int32), 3)),
+            ("isolated tail nodes", meshgen.QUAD4, (meshgen.quad_grid(3, 4)[0], 40)),
+            ("empty mesh", meshgen.HEX8, (torch.zeros((0, 8), dtype=torch.int32), 11)),
+            ("fan hub owned by rank 0", meshgen.TRI3, meshgen.nonmanifold_fan(300)),
+        ]
+        for name, et, (conn, N) in cases:
+            M = conn.shape[0]
+            s0, s1 = rank * M // world, (rank + 1) * M // world
+            ro, ri = oracle.node_csr(et, conn, N)
+            so, si = oracle.elem_csr(et, conn, N)
+            for p2p in (False, True):
+                res = find_neighbors_dist(conn[s0:s1].contiguous().cuda(), et, s0, N, p2p=p2p)
+                (no, ni), (eo, ei) = gather_global(res, N)
+                good = (np.array_equal(no.cpu().numpy(), ro) and np.array_equal(ni.cpu().numpy(), ri)
+                        and np.array_equal(eo.cpu().numpy(), so) and np.array_equal(ei.cpu().numpy(), si))
+                if not good:
+                    q.put((rank, False, f"{name} p2p={p2p}"))
+                    ok = False
+        release_comms()
+        q.put((rank, bool(ok), "edge cases"))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dist_edge_cases_multi_rank_one_gpu():
+    """Both exchange modes through the C ABI with 3 ranks on one GPU: shards without elements,
+    fewer nodes than ranks, nodes used by no element, an empty mesh, a 300-valent hub."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = [ctx.Process(target=_edge_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(3)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, info in out:
+        assert ok, f"rank {rank}: {info}"
