@@ -16,7 +16,7 @@ NAMES = [("k_node_gather_t", "node_gather"), ("k_elem_scatter", "elem_scatter"),
          ("k_poly_count", "poly_count"), ("k_poly_scatter", "poly_scatter"), ("k_poly_gather", "poly_gather"),
          ("k_poly_giant", "poly_giant"), ("k_chunk_count", "count_fallback"), ("k_chunk_scatter<", "scatter_fallback"),
          ("k_chunk_scatter_fixed", "elem_scatter"),
-         ("k_chunk_sort", "elem_segsort")]
+         ("k_chunk_sort", "elem_segsort"), ("k_small_both", "small_both")]
 
 
 def main():
