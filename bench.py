@@ -79,11 +79,16 @@ class ClockSampler:
             return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
-            time.sleep(0.3)      # let the sampler start before the timed region
+            # nvidia-smi's start-up (NVML init) can stall CUDA calls for tens of ms: wait until it has
+            # produced samples before the timed region starts
+            t0 = time.time()
+            while len(self.lines) < 2 and time.time() - t0 < 10:
+                time.sleep(0.02)
+            time.sleep(0.1)
         except OSError:
             self.proc = None
         return self
@@ -467,11 +472,6 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for _ in range(args.warmup):
-        r = step()
-        del r
-    torch.cuda.synchronize()
-
     mem_bound = None
     if args.max_workspace_gb and not poly and world == 1:   # measured peak of the bounded mode
         torch.cuda.synchronize()
@@ -533,6 +533,13 @@ def run_ours(args):
     del r, outs
     torch.cuda.synchronize()
 
+    # warm-up after the parity gate / allocation-log calls, so the caching allocator is back in its
+    # steady state when the timed region starts (its first step must not pay a cudaMalloc)
+    for _ in range(args.warmup):
+        r = step()
+        del r
+    torch.cuda.synchronize()
+
     # ---- device-timed region ----
     s = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -543,13 +550,23 @@ def run_ours(args):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         t_host0 = time.time()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        mstat0 = torch.cuda.memory_stats(dev)
         ev0.record(s)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             r = step()
             del r
+            evs[i].record(s)
         ev1.record(s)
         torch.cuda.synchronize()
         clk.window = (t_host0, time.time())
+    step_seq = [ev0.elapsed_time(evs[0])] + [evs[i - 1].elapsed_time(evs[i]) for i in range(1, args.steps)]
+    step_ms = sorted(step_seq)
+    if os.environ.get("MN_BENCH_STEPS"):
+        ms_now = torch.cuda.memory_stats(dev)
+        print("steps", [round(x, 3) for x in step_seq],
+              {k: ms_now.get(k, 0) - mstat0.get(k, 0) for k in ("num_device_alloc", "num_device_free", "num_alloc_retries")},
+              file=sys.stderr)
     barrier()
     launches = mn.launch_count() - launches0
     mn.profile_enable(False)
@@ -595,7 +612,8 @@ def run_ours(args):
     kernels = [{"name": e["name"], "launches_per_step": e["launches"] / args.steps,
                 "ms_per_step": e["ms"] / args.steps, "share": e["ms"] / tot_ms if tot_ms else None,
                 "GBps": (e["alg_bytes"] / (e["ms"] / 1e3) / 1e9) if e["ms"] > 0 else None} for e in prof]
-    step_roof = {"alg_bytes_per_step": step_bytes, "achieved_GBps": step_bytes / (ms_local / 1e3) / 1e9,
+    step_roof = {"step_ms_min_median_max": [step_ms[0], step_ms[len(step_ms) // 2], step_ms[-1]],
+                 "alg_bytes_per_step": step_bytes, "achieved_GBps": step_bytes / (ms_local / 1e3) / 1e9,
                  "frac_of_peak": step_bytes / (ms_local / 1e3) / 1e9 / peak,
                  "kernel_ms_per_step": tot_ms / args.steps}
     # compulsory floor: connectivity read once, every output written once

@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-timeout 1200 python -m pytest tests/test_gpu_dist.py -q -x -k "edge or nccl or real_kernels" > gpurun_out/pytest_dist_edge.log 2>&1; tail -25 gpurun_out/pytest_dist_edge.log
+MN_BENCH_STEPS=1 python bench.py 2>&1 >/dev/null | grep steps
+MN_BENCH_STEPS=1 python bench.py --config 3 2>&1 >/dev/null | grep steps
+MN_BENCH_STEPS=1 python bench.py --config 1 2>&1 >/dev/null | grep steps
