@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-MN_BENCH_STEPS=1 python bench.py 2>&1 >/dev/null | grep steps
-MN_BENCH_STEPS=1 python bench.py --config 3 2>&1 >/dev/null | grep steps
-MN_BENCH_STEPS=1 python bench.py --config 1 2>&1 >/dev/null | grep steps
+python tools/ab_knobs.py gather_ws 0,1 5,3,4 2>&1 | tail -8
