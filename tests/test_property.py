@@ -20,13 +20,15 @@ TYPES = [meshgen.TRI3, meshgen.QUAD4, meshgen.TET4, meshgen.HEX8]
 
 @st.composite
 def meshes(draw, max_elems=40, max_nodes=30):
+    """Random element type, sizes and seed; the rows (k distinct nodes each, non-manifold edges and
+    isolated vertices included) come from meshgen.random_mesh with that seed."""
     et = draw(st.sampled_from(TYPES))
     k = meshgen.ARITY[et]
     N = draw(st.integers(min_value=k, max_value=max_nodes))
     M = draw(st.integers(min_value=0, max_value=max_elems))
-    rows = [draw(st.permutations(list(range(N))))[:k] for _ in range(M)]
-    conn = torch.tensor(rows, dtype=torch.int32).reshape(M, k)
-    return et, conn, N
+    seed = draw(st.integers(min_value=0, max_value=2 ** 31 - 1))
+    conn, _ = meshgen.random_mesh(et, M, N, seed=seed)
+    return et, conn.reshape(M, k).contiguous(), N
 
 
 @st.composite
