@@ -1718,6 +1718,10 @@ template <int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS)
 k_scan_i32(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out, uint64_t* status,
            uint32_t* ticket, uint32_t epoch, const unsigned int* __restrict__ guard = nullptr) {
+  // Each thread scans ITEMS consecutive counts sequentially (16-byte loads), the warps scan their
+  // threads' totals, the block its warps' totals, decoupled look-back across tiles; the exclusive
+  // prefixes leave as 16-byte stores (out[i] for i < n), the thread holding item n - 1 writes out[n].
+  static_assert(ITEMS % 4 == 0, "vector loads");
   constexpr int WARPS = THREADS / 32;
   if (guard && *guard == 0u) return;   // grid-uniform: a fallback scan that is not needed
   constexpr int TILE = THREADS * ITEMS;
@@ -1728,22 +1732,35 @@ k_scan_i32(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out,
   if (tid == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const int64_t chunk = (int64_t)tile * TILE + (int64_t)warp * 32 * ITEMS;
-  int64_t v[ITEMS];
-  uint64_t wtot = 0;
+  const int64_t base = (int64_t)tile * TILE + (int64_t)tid * ITEMS;
+  int64_t loc[ITEMS];   // inclusive prefix inside the thread
+  const bool full = base + ITEMS <= n && ((reinterpret_cast<uintptr_t>(in) & 15) == 0);
+  if (full) {
+    int64_t run = 0;
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int64_t idx = chunk + i * 32 + lane;
-    int64_t x = idx < n ? (int64_t)in[idx] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t y = __shfl_up_sync(FULL, x, o);
-      if (lane >= o) x += y;
+    for (int q = 0; q < ITEMS / 4; ++q) {
+      const int4 x = __ldg(reinterpret_cast<const int4*>(in + base) + q);
+      run += x.x; loc[4 * q] = run;
+      run += x.y; loc[4 * q + 1] = run;
+      run += x.z; loc[4 * q + 2] = run;
+      run += x.w; loc[4 * q + 3] = run;
     }
-    v[i] = x + (int64_t)wtot;               // inclusive within the warp chunk
-    wtot += (uint64_t)__shfl_sync(FULL, x, 31);
+  } else {
+    int64_t run = 0;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+      run += base + k < n ? (int64_t)in[base + k] : 0;
+      loc[k] = run;
+    }
   }
-  if (lane == 0) s_w[warp] = wtot;
+  const int64_t ttot = loc[ITEMS - 1];
+  int64_t winc = ttot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(FULL, winc, o);
+    if (lane >= o) winc += y;
+  }
+  if (lane == 31) s_w[warp] = (uint64_t)winc;
   __syncthreads();
   if (warp == 0) {
     uint64_t c = lane < WARPS ? s_w[lane] : 0;
@@ -1766,13 +1783,18 @@ k_scan_i32(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out,
     if (lane == 0) s_texcl = excl;
   }
   __syncthreads();
-  const int64_t add = (int64_t)(s_texcl + s_w[warp]);
+  const int64_t pre = (int64_t)(s_texcl + s_w[warp]) + winc - ttot;   // sum of every item before base
+  if (full && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+    longlong2* o2 = reinterpret_cast<longlong2*>(out + base);
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int64_t idx = chunk + i * 32 + lane;
-    if (idx < n) out[idx + 1] = v[i] + add;
+    for (int q = 0; q < ITEMS / 2; ++q)
+      o2[q] = make_longlong2(pre + (q ? loc[2 * q - 1] : 0), pre + loc[2 * q]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k)
+      if (base + k < n) out[base + k] = pre + (k ? loc[k - 1] : 0);
   }
-  if (tile == 0 && tid == 0) out[0] = 0;
+  if (base < n && base + ITEMS >= n) out[n] = pre + ttot;
 }
 
 // ================================================================================================
