@@ -609,6 +609,20 @@ def run_ours(args):
                 "alg_bytes_per_launch": top["alg_bytes"] / top["launches"],
                 "avg_launch_ms": top["ms"] / top["launches"],
                 "share_of_kernel_time": top["ms"] / tot_ms if tot_ms else None}
+    # secondary: the same kernel against the instruction-issue roofline (warp instructions per launch
+    # from a committed ncu capture, profiles/issue.json; 148 SMs x 4 schedulers x sm clock)
+    ip = os.path.join(ROOT, "profiles", "issue.json")
+    if os.path.exists(ip):
+        inst = json.load(open(ip)).get(f"config{args.config}/n{world}/{top['name']}")
+        if inst:
+            clk_mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0)) \
+                if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0
+            ipeak = 148 * 4 * clk_mhz * 1e6
+            iach = inst / (roofline["avg_launch_ms"] / 1e3)
+            roofline["issue"] = {"warp_instructions_per_launch": inst, "achieved_per_s": iach,
+                                 "peak_per_s": ipeak, "frac": iach / ipeak,
+                                 "source": "ncu smsp__inst_executed.sum (profiles/issue.json); peak = 148 SMs x 4 "
+                                           "issue slots x sm_max clock"}
     kernels = [{"name": e["name"], "launches_per_step": e["launches"] / args.steps,
                 "ms_per_step": e["ms"] / args.steps, "share": e["ms"] / tot_ms if tot_ms else None,
                 "GBps": (e["alg_bytes"] / (e["ms"] / 1e3) / 1e9) if e["ms"] > 0 else None} for e in prof]
