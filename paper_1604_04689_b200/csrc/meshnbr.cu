@@ -1196,10 +1196,10 @@ static mn_status small_path(const Plan& P, const int32_t* conn, Mem& mem, bool w
                                    (we ? 4.0 * P.Pe : 0.0), s, [&] {
     if (aligned)
       k_small_both<T, true><<<1, kSmallThreads, smem, s>>>(conn, (int)P.M, (int)P.N, elem_off, elem_idx, node_off,
-                                                            (uint32_t*)node_idx, (volatile unsigned long long*)host);
+                                                            (uint32_t*)node_idx, (unsigned long long*)host);
     else
       k_small_both<T, false><<<1, kSmallThreads, smem, s>>>(conn, (int)P.M, (int)P.N, elem_off, elem_idx, node_off,
-                                                             (uint32_t*)node_idx, (volatile unsigned long long*)host);
+                                                             (uint32_t*)node_idx, (unsigned long long*)host);
   }));
   MN_CUDA(cudaStreamSynchronize(s));
   st = decode_err(host[0], err);

@@ -96,7 +96,7 @@ template <int T, bool ALIGNED>
 __global__ void __launch_bounds__(kSmallThreads, 1)
 k_small_both(const int32_t* __restrict__ conn, int M, int N, int64_t* __restrict__ elem_off,
              int32_t* __restrict__ elem_idx, int64_t* __restrict__ node_off, uint32_t* __restrict__ fin,
-             volatile unsigned long long* __restrict__ ctrl) {
+             unsigned long long* __restrict__ ctrl) {
   constexpr int K = Elem<T>::K, C = Elem<T>::C;
   constexpr bool simplex = (C == K - 1);
   extern __shared__ int sm[];
@@ -141,7 +141,7 @@ k_small_both(const int32_t* __restrict__ conn, int M, int N, int64_t* __restrict
   }
   __syncthreads();
   if (s_err != ERR_NONE) {
-    if (t == 0) { ctrl[1] = 0; ctrl[2] = 0; __threadfence_system(); ctrl[0] = s_err; }
+    if (t == 0) { ctrl[0] = s_err; ctrl[1] = 0; ctrl[2] = 0; }
     return;
   }
   // ---- a5 (elements): offsets ----
@@ -213,10 +213,10 @@ k_small_both(const int32_t* __restrict__ conn, int M, int N, int64_t* __restrict
   }
   __syncthreads();
   if (t == 0) {
+    // (read by the host after the stream sync, which makes every write of the kernel visible: no fence)
+    ctrl[0] = ERR_NONE;
     ctrl[1] = (node_off && !s_big) ? (unsigned long long)s_ncnt[N] : 0ull;
     ctrl[2] = s_big ? 1ull : 0ull;
-    __threadfence_system();
-    ctrl[0] = ERR_NONE;
   }
 }
 
