@@ -290,20 +290,25 @@ mn_status mn_dist_finish(mn_elem_type type, const uint64_t* d_pairs, int64_t n, 
  * [global_elem_base, global_elem_base + shard_elems) of a mesh of num_nodes nodes (shards
  * contiguous, ascending with the rank) and receives the CSR slices of the nodes it owns,
  * [lo, hi) = [r * ceil(N/G), (r+1) * ceil(N/G)) clipped to N.  Inside one call, on `stream`:
- *   1. validate the shard and bucket its (node, element) incidences stably by owner (one onesweep
- *      pass, pairs created from conn), with one element row per (remote owner, element);
- *   2. count exchange: one all-gather of every rank's [error word, status, incidence counts,
- *      row counts]; the lowest error over all ranks is returned by EVERY rank (so no rank is left
+ *   1. validate the shard, count its incidences per owner and (when the shard is coherent: the
+ *      locality sample of the 1-GPU path) collect its REMOTE incidences (owner != r);
+ *   2. count exchange: one all-gather of every rank's [error word, status, counts per owner,
+ *      locality]; the lowest error over all ranks is returned by EVERY rank (so no rank is left
  *      waiting in a collective), before any payload moves;
- *   3. payload exchange: one grouped all-to-all(v) of the remote incidences, the remote element
- *      ids and their rows; an owner's own incidences never travel (read in place from step 1);
- *   4. local finish: element CSR slice by a stable sort on the local node id (transpose or LSD, as
- *      the 1-GPU path), node CSR slice by per-node expansion + dedupe (rows from the own shard or
- *      the received table);
+ *   3. bucket-and-send: one owner-digit onesweep pass stores each remote incidence and its element
+ *      row at its place in the owner's receive layout (source-rank order, element-major) — in a
+ *      local send buffer followed by ONE grouped all-to-all(v) (mn_find_neighbors_dist), or directly
+ *      in the owner's symmetric heap over peer memory followed by an all-gather as a barrier
+ *      (mn_find_neighbors_dist_p2p);
+ *   4. local finish: if every shard is coherent, an owner's own incidences are never materialised —
+ *      its element CSR slice is the chunk transpose of (own shard filtered to [lo, hi)) + (received
+ *      incidences), its node slice the per-node expansion + dedupe with rows from the own shard or
+ *      the received rows; otherwise the own bucket is kept in place between the received ones and
+ *      the slice is built from all of them (stable LSD on the local node id);
  *   5. one all-gather of the slice nnz values: the global offset bases of the slices.
  * Concatenating the slices of all ranks in rank order (offsets shifted by the bases) is
- * bit-identical to the single-GPU CSRs.  Blocks the calling thread four times (steps 1, 2, 4, 5).
- * All collectives are called in the same order on every rank.
+ * bit-identical to the single-GPU CSRs.  Blocks the calling thread a few times (the locality
+ * sample, steps 1, 2, 4, 5).  All collectives are called in the same order on every rank.
  * ------------------------------------------------------------------------------------------- */
 
 /* One all-to-all(v) exchange of a group: rank r sends send_counts[g] elements of elem_bytes bytes,
@@ -402,8 +407,9 @@ mn_status mn_comm_from_nccl(void* nccl_comm, mn_comm* out);
 /* Host-only exchange plan of step 2 (used by mn_find_neighbors_dist; exported so the protocol can
  * be checked without a GPU).  gathered: world rows of (2 + 2 * world) int64 each, row g =
  * [error word of rank g, status of rank g, counts_g[0..world), row_counts_g[0..world)]
- * where counts_g[h] / row_counts_g[h] are the incidences / rows rank g sends to rank h.  Writes
- * recv_counts[g] = counts_g[rank] and recv_row_counts[g] = row_counts_g[rank] and returns the
+ * where counts_g[h] are the incidences rank g sends to rank h and aux_g[h] a per-destination
+ * auxiliary count (mn_find_neighbors_dist stores rank g's locality flag in aux_g[0]).  Writes
+ * recv_counts[g] = counts_g[rank] and recv_row_counts[g] = aux_g[rank] and returns the
  * global outcome: the first nonzero status in rank order, else the error of the lowest error word
  * (detail decoded into err), else MN_OK.  Error word: (global element << 5) | (repeated node << 4)
  * | position, all ones when the shard is valid — so the lowest word is the lowest element, and

@@ -94,172 +94,6 @@ static mn_status dist_plan(int world, int rank, const int64_t* all, int64_t* rc,
   return decode_err(lowest, err);
 }
 
-// ------------------------------------------------------------------------------------------------
-// the whole call
-// ------------------------------------------------------------------------------------------------
-template <int T>
-static mn_status dist_impl(const int32_t* conn, int64_t M, int64_t base, int64_t N, const mn_comm* comm, Mem& mem,
-                           mn_csr* node_slice, mn_csr* elem_slice, mn_dist_info* info, mn_error_detail* err) {
-  constexpr int K = Elem<T>::K;
-  cudaStream_t s = mem.s;
-  const int G = comm->world, self = comm->rank;
-  const int W = 2 + 2 * G;
-  const int64_t Pe = M * K;
-  mn_status st = MN_OK, local = MN_OK;
-  std::memset(node_slice, 0, sizeof(*node_slice));
-  std::memset(elem_slice, 0, sizeof(*elem_slice));
-  std::vector<int64_t> hc(G, 0), hrc(G, 0), rc(G, 0), rr(G, 0), row((size_t)W, 0), all((size_t)W * G, 0);
-  uint64_t ew = ERR_NONE;
-  int32_t *relems = nullptr, *rrows = nullptr;
-  uint64_t* pairs = nullptr;
-  uint64_t *recv_pairs = nullptr;
-  int32_t *recv_elems = nullptr, *recv_rows = nullptr;
-  int64_t* dx = nullptr;   // device staging of the all-gathers
-  int64_t lo = 0, hi = 0, before = 0, after = 0, nr = 0, own = 0;
-  std::vector<int64_t> sd(G, 0), rd(G, 0), sdr(G, 0), rdr(G, 0), sc(G, 0), rcz(G, 0);
-  int64_t nnz2[2] = {0, 0};
-  std::vector<int64_t> nnz_all((size_t)2 * G, 0);
-  const uint64_t chunk = (uint64_t)((N + G - 1) / G > 0 ? (N + G - 1) / G : 1);
-  lo = std::min<int64_t>(N, (int64_t)chunk * self);
-  hi = std::min<int64_t>(N, (int64_t)chunk * (self + 1));
-
-  // the all-gather staging first: past this point every failure still joins the count exchange
-  dx = (int64_t*)mem.get((size_t)W * (G + 1) * 8);
-  if (!dx) return MN_ERR_OOM;
-  // ---- 1. validate + bucket (a local failure is carried into the count exchange) ----
-  if (Pe > 0) {
-    pairs = (uint64_t*)mem.get((size_t)Pe * 8);
-    if (!pairs) local = MN_ERR_OOM;
-  }
-  if (local == MN_OK) {
-    local = (G <= 256 ? dist_bucket_impl<T, 256> : dist_bucket_impl<T, 512>)(
-        conn, M, base, N, G, self, pairs, hc.data(), &relems, &rrows, hrc.data(), mem, err, &ew);
-  }
-  if (local != MN_OK) {
-    std::fill(hc.begin(), hc.end(), 0);
-    std::fill(hrc.begin(), hrc.end(), 0);
-  }
-  // ---- 2. count exchange: one all-gather of [error word, status, counts, row counts] ----
-  row[0] = (int64_t)ew;
-  row[1] = local;
-  for (int g = 0; g < G; ++g) { row[2 + g] = hc[g]; row[2 + G + g] = hrc[g]; }
-  MN_CUDA(cudaMemcpyAsync(dx, row.data(), (size_t)W * 8, cudaMemcpyHostToDevice, s));
-  if (comm->allgather(comm->ctx, dx, dx + W, (size_t)W * 8, (mn_stream)s) != 0) { st = MN_ERR_COMM; goto done; }
-  MN_CUDA(cudaMemcpyAsync(all.data(), dx + W, (size_t)W * G * 8, cudaMemcpyDeviceToHost, s));
-  MN_CUDA(cudaStreamSynchronize(s));
-  st = dist_plan(G, self, all.data(), rc.data(), rr.data(), err);
-  if (st != MN_OK) goto done;
-
-  // ---- 3. payload exchange: remote incidences, remote element ids, their rows ----
-  for (int g = 0; g < G; ++g) {
-    if (g < self) before += rc[g];
-    if (g > self) after += rc[g];
-    if (g != self) nr += rr[g];
-  }
-  own = rc[self];
-  {
-    int64_t a = 0, b = 0, c = 0, d = 0;
-    for (int g = 0; g < G; ++g) {
-      sd[g] = a; a += hc[g];                  // pairs: bucket g starts at the prefix of the counts
-      sc[g] = g == self ? 0 : hc[g];
-      rd[g] = b; if (g != self) b += rc[g];   // received pairs packed without the own bucket
-      rcz[g] = g == self ? 0 : rc[g];
-      sdr[g] = c; c += hrc[g];                // rows: grouped by destination (none for self)
-      rdr[g] = d; d += g == self ? 0 : rr[g];
-    }
-  }
-  if (before + after > 0) {
-    recv_pairs = (uint64_t*)mem.get((size_t)(before + after) * 8);
-    if (!recv_pairs) { st = MN_ERR_OOM; goto done; }
-  }
-  if (nr > 0) {
-    recv_elems = (int32_t*)mem.get((size_t)nr * 4);
-    recv_rows = (int32_t*)mem.get((size_t)nr * K * 4);
-    if (!recv_elems || !recv_rows) { st = MN_ERR_OOM; goto done; }
-  }
-  {
-    std::vector<int64_t> rrz(G);
-    for (int g = 0; g < G; ++g) rrz[g] = g == self ? 0 : rr[g];
-    const mn_a2a_op ops[3] = {
-        {pairs, sc.data(), sd.data(), recv_pairs, rcz.data(), rd.data(), 8},
-        {relems, hrc.data(), sdr.data(), recv_elems, rrz.data(), rdr.data(), 4},
-        {rrows, hrc.data(), sdr.data(), recv_rows, rrz.data(), rdr.data(), (size_t)K * 4},
-    };
-    if (comm->alltoallv(comm->ctx, ops, 3, (mn_stream)s) != 0) { st = MN_ERR_COMM; goto done; }
-  }
-  if (info) {
-    int64_t sent = 0, got = 0;
-    for (int g = 0; g < G; ++g)
-      if (g != self) {
-        sent += hc[g] * 8 + hrc[g] * 4 * (K + 1);
-        got += rc[g] * 8 + rr[g] * 4 * (K + 1);
-      }
-    info->sent_bytes = sent;
-    info->recv_bytes = got;
-    info->own_incidences = own;
-  }
-
-  // ---- 4. local finish over (lower ranks' pairs, own bucket in place, higher ranks' pairs) ----
-  {
-    const uint64_t* ownp = pairs ? pairs + sd[self] : recv_pairs;
-    const PairSrc ps{{recv_pairs, ownp, recv_pairs ? recv_pairs + before : ownp},
-                     {before, before + own, before + own + after}};
-    const int64_t n = before + own + after;
-    if (n > INT32_MAX) { st = MN_ERR_CAPACITY; goto done; }
-    st = dist_finish_impl<T>(ps, n, recv_elems, recv_rows, nr, conn, base, M, N, lo, hi, mem, node_slice, elem_slice);
-    if (st != MN_OK) goto done;
-  }
-  mem.put(pairs); pairs = nullptr;
-  mem.put(recv_pairs); recv_pairs = nullptr;
-  mem.put(recv_elems); recv_elems = nullptr;
-  mem.put(recv_rows); recv_rows = nullptr;
-  mem.put(relems); relems = nullptr;
-  mem.put(rrows); rrows = nullptr;
-
-  // ---- 5. global offset bases: all-gather of the slice nnz values ----
-  nnz2[0] = node_slice->nnz;
-  nnz2[1] = elem_slice->nnz;
-  MN_CUDA(cudaMemcpyAsync(dx, nnz2, 16, cudaMemcpyHostToDevice, s));
-  if (comm->allgather(comm->ctx, dx, dx + 2, 16, (mn_stream)s) != 0) { st = MN_ERR_COMM; goto done; }
-  MN_CUDA(cudaMemcpyAsync(nnz_all.data(), dx + 2, (size_t)16 * G, cudaMemcpyDeviceToHost, s));
-  MN_CUDA(cudaStreamSynchronize(s));
-  mem.put(dx); dx = nullptr;
-  if (info) {
-    info->lo = lo;
-    info->hi = hi;
-    info->node_base = info->elem_base = info->node_nnz_total = info->elem_nnz_total = 0;
-    for (int g = 0; g < G; ++g) {
-      if (g < self) { info->node_base += nnz_all[2 * g]; info->elem_base += nnz_all[2 * g + 1]; }
-      info->node_nnz_total += nnz_all[2 * g];
-      info->elem_nnz_total += nnz_all[2 * g + 1];
-    }
-  }
-  return MN_OK;
-done:
-  cudaStreamSynchronize(s);
-  mem.put(pairs);
-  mem.put(recv_pairs);
-  mem.put(recv_elems);
-  mem.put(recv_rows);
-  mem.put(relems);
-  mem.put(rrows);
-  mem.put(dx);
-  mn_csr_release(node_slice, (mn_stream)s);
-  mn_csr_release(elem_slice, (mn_stream)s);
-  return st;
-}
-
-static mn_status dist_dispatch(mn_elem_type t, const int32_t* conn, int64_t M, int64_t base, int64_t N,
-                               const mn_comm* comm, Mem& mem, mn_csr* ns, mn_csr* es, mn_dist_info* info,
-                               mn_error_detail* err) {
-  switch (t) {
-    case MN_TRI3: return dist_impl<MN_TRI3>(conn, M, base, N, comm, mem, ns, es, info, err);
-    case MN_QUAD4: return dist_impl<MN_QUAD4>(conn, M, base, N, comm, mem, ns, es, info, err);
-    case MN_TET4: return dist_impl<MN_TET4>(conn, M, base, N, comm, mem, ns, es, info, err);
-    default: return dist_impl<MN_HEX8>(conn, M, base, N, comm, mem, ns, es, info, err);
-  }
-}
-
 // ================================================================================================
 // Fused bucket-and-send over peer memory (mn_find_neighbors_dist_p2p).  Instead of bucketing into a
 // local buffer and then moving the remote buckets with an all-to-all, the owner-digit onesweep pass
@@ -337,12 +171,209 @@ k_remote_elems(const uint64_t* __restrict__ pairs, int64_t nr, int64_t own0, int
     out[i] = (int32_t)(pairs[i < own0 ? i : i + own] & 0xffffffffull);
 }
 
+// ================================================================================================
+// The multi-GPU path (mn_find_neighbors_dist and _p2p).  One orchestration, two exchanges:
+//   1. validation + incidence counts per owner (one read of the shard) and the shard's locality
+//      sample, one host read;
+//   2. count exchange: one all-gather of [error word, status, counts per owner, locality]; the
+//      lowest error of all ranks is returned by every rank;
+//   3. bucket-and-send: one owner-digit onesweep pass stores every REMOTE incidence, with its element
+//      row, at its place in its owner's receive layout (source-rank order, element-major) — into a
+//      local send buffer (then one grouped NCCL all-to-all) or straight into the owner's symmetric
+//      heap over peer memory (then an all-gather as a barrier);
+//   4. finish: when every shard has locality, the own incidences are never materialised: the
+//      element CSR slice is the chunk transpose of (own shard filtered to [lo, hi)) + (received
+//      incidences), the node slice the gather with rows from the own shard or the received rows;
+//      otherwise the own bucket is written in place between the received ones and the slice built
+//      from all of them (stable LSD needs them element-major);
+//   5. one all-gather of the slice nnz values.
+// ================================================================================================
+
+// Element + node CSR slices of nodes [lo, hi) from the own shard (filtered) and the nr received
+// remote incidences (pairs, their rows rr, element ids relems ascending).  Transpose path only.
+template <int T>
+static mn_status finish_own_conn(const int32_t* conn, int64_t Ms, int64_t base, int64_t own, const uint64_t* rp,
+                                 int64_t nr, const int32_t* relems, const int32_t* rr, int64_t lo, int64_t hi,
+                                 Mem& mem, mn_csr* node_slice, mn_csr* elem_slice) {
+  cudaStream_t s = mem.s;
+  mn_status st = MN_OK;
+  constexpr int C = Elem<T>::C;
+  uint64_t* host = pinned_pair();
+  if (!host) return MN_ERR_CUDA;
+  const int64_t nloc = hi - lo, n = own + nr;
+  const bool aligned = ((uintptr_t)conn & 15) == 0 && ((uintptr_t)rr & 15) == 0;
+  std::memset(node_slice, 0, sizeof(*node_slice));
+  std::memset(elem_slice, 0, sizeof(*elem_slice));
+  int64_t* noff = (int64_t*)mem.get((size_t)(nloc + 1) * 8);
+  int64_t* eoff = (int64_t*)mem.get((size_t)(nloc + 1) * 8);
+  int32_t* eidx = n ? (int32_t*)mem.get((size_t)n * 4 + 16) : nullptr;
+  void* ws = nullptr;
+  if (!noff || !eoff || (n && !eidx)) { st = MN_ERR_OOM; goto done; }
+  if (n == 0 || nloc == 0) {
+    MN_CUDA(cudaMemsetAsync(noff, 0, (size_t)(nloc + 1) * 8, s));
+    MN_CUDA(cudaMemsetAsync(eoff, 0, (size_t)(nloc + 1) * 8, s));
+    MN_CUDA(cudaStreamSynchronize(s));
+  } else {
+    const int64_t nch = tiles_of(nloc, kChunkNodes);
+    Arena ar;
+    unsigned long long* errw = ar.take<unsigned long long>(2);
+    uint32_t* tickets = ar.take<uint32_t>(8);
+    unsigned int* ngiant = ar.take<unsigned int>(1);
+    unsigned int* nsgiant = ar.take<unsigned int>(1);
+    unsigned int* ovf = ar.take<unsigned int>(1);
+    uint64_t* sstatus = ar.take<uint64_t>((size_t)tiles_of(nloc, kScanTile) + 1);
+    int32_t* ccur = ar.take<int32_t>((size_t)nch + 1);    // fixed-bucket cursors
+    int32_t* ccnt = ar.take<int32_t>((size_t)nch + 1);    // fallback counts
+    int32_t* cnt = ar.take<int32_t>((size_t)nloc + 1);
+    int32_t* lofs = ar.take<int32_t>((size_t)nloc + 1);
+    const size_t head = ar.off;
+    int64_t* cbase = ar.take<int64_t>((size_t)nch + 1);
+    uint32_t* temp = ar.take<uint32_t>((size_t)std::max<int64_t>(C * n, 2 * n + 64));   // buckets, then node lists
+    uint8_t* bnode = ar.take<uint8_t>((size_t)2 * n + 64);
+    uint32_t* giants = ar.take<uint32_t>((size_t)nloc + 1);
+    uint32_t* sgiants = ar.take<uint32_t>((size_t)nloc + 1);
+    ws = mem.get(ar.off);
+    if (!ws) { st = MN_ERR_OOM; goto done; }
+    {
+      char* bb = (char*)ws;
+      auto fix = [&](auto* q) { return (decltype(q))(bb + (size_t)q); };
+      errw = fix(errw); tickets = fix(tickets); ngiant = fix(ngiant); nsgiant = fix(nsgiant); ovf = fix(ovf);
+      sstatus = fix(sstatus); ccur = fix(ccur); ccnt = fix(ccnt); cnt = fix(cnt); lofs = fix(lofs);
+      cbase = fix(cbase); temp = fix(temp); bnode = fix(bnode); giants = fix(giants); sgiants = fix(sgiants);
+      int32_t* belem = reinterpret_cast<int32_t*>(temp);
+      MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
+      MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
+      int64_t capl = (2 * n / nch) & ~(int64_t)31;
+      const int ovr = g_chunk_cap.load();
+      if (ovr > 0 && ovr < capl) capl = ovr;
+      if (capl > (int64_t)INT32_MAX - 4096) capl = (int64_t)INT32_MAX - 4096;
+      const int cap = (int)capl;
+      const PairSrc ps = pair_src(rp, nr);
+      // element CSR slice: own shard (range-filtered) + received incidences into the same fixed
+      // chunk buckets; the guarded counted fallback replaces them when a bucket overflows
+      MN_CUDA(launch("elem_scatter", 4.0 * Elem<T>::K * Ms + 5.0 * own, s, [&] {
+        if (aligned)
+          k_chunk_scatter_fixed<T, true, 1, true><<<hist_grid(Ms), 256, 0, s>>>(conn, Ms, INT32_MAX, cap, ccur, belem,
+                                                                            bnode, errw, ovf, lo, hi, base);
+        else
+          k_chunk_scatter_fixed<T, false, 1, true><<<hist_grid(Ms), 256, 0, s>>>(conn, Ms, INT32_MAX, cap, ccur,
+                                                                             belem, bnode, errw, ovf, lo, hi, base);
+      }));
+      if (nr > 0)
+        MN_CUDA(launch("elem_scatter", 13.0 * nr, s, [&] {
+          k_pairs_chunk_scatter<true><<<stream_grid(nr), 256, 0, s>>>(ps, nr, lo, cap, nullptr, ccur, belem, bnode,
+                                                                      ovf);
+        }));
+      MN_CUDA(launch("scan_counts", 12.0 * nch, s, [&] {
+        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nch, kScanTile), kScanThreads, 0, s>>>(
+            ccur, nch, cbase, sstatus, tickets + 0, 1);
+      }));
+      MN_CUDA(launch("count_fallback", 0.0, s, [&] {
+        if (aligned)
+          k_chunk_count<T, true, true><<<count_grid(Ms), 256, 0, s>>>(conn, Ms, INT32_MAX, ccnt, errw, lo, hi, ovf);
+        else
+          k_chunk_count<T, false, true><<<count_grid(Ms), 256, 0, s>>>(conn, Ms, INT32_MAX, ccnt, errw, lo, hi, ovf);
+        if (nr > 0) k_pairs_chunk_count<<<stream_grid(nr), 256, 0, s>>>(ps, nr, lo, ccnt, ovf);
+      }));
+      MN_CUDA(launch("scan_fallback", 0.0, s, [&] {
+        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nch, kScanTile), kScanThreads, 0, s>>>(
+            ccnt, nch, cbase, sstatus, tickets + 1, 2, ovf);
+      }));
+      MN_CUDA(launch("scatter_fallback", 0.0, s, [&] {
+        if (aligned)
+          k_chunk_scatter<T, true, true><<<hist_grid(Ms), 256, 0, s>>>(conn, Ms, cbase, lofs, belem, bnode, errw, lo,
+                                                                      hi, ovf, base);
+        else
+          k_chunk_scatter<T, false, true><<<hist_grid(Ms), 256, 0, s>>>(conn, Ms, cbase, lofs, belem, bnode, errw,
+                                                                       lo, hi, ovf, base);
+        if (nr > 0)
+          k_pairs_chunk_scatter<false><<<stream_grid(nr), 256, 0, s>>>(ps, nr, lo, 0, cbase, lofs, belem, bnode, ovf);
+      }));
+      MN_CUDA(launch("elem_segsort", 9.0 * n + 8.0 * (nloc + 1), s, [&] {
+        k_chunk_sort<true><<<(unsigned)nch, kChunkNodes, 0, s>>>(cbase, nloc, belem, bnode, eoff, eidx, sgiants,
+                                                                  nsgiant, errw, ovf, cap);
+      }));
+      const int scap = 48 * 1024;
+      cudaFuncSetAttribute(k_segsort_giant, cudaFuncAttributeMaxDynamicSharedMemorySize, scap * 4);
+      MN_CUDA(launch("segsort_giant", 0.0, s, [&] {
+        k_segsort_giant<<<148, 1024, scap * 4, s>>>(eoff, eidx, sgiants, nsgiant, scap, errw);
+      }));
+      MN_CUDA(cudaMemsetAsync(lofs, 0, (size_t)(nloc + 1) * 4, s));
+      // node CSR slice: rows of own elements from the shard, of remote ones from the received table
+      const RowSrc rs{conn, base, Ms, relems, rr, nr};
+      const unsigned ng = (unsigned)tiles_of(nloc, kNodeThreads);
+      MN_CUDA(launch("node_gather", 8.0 * (nloc + 1) + 4.0 * n + 4.0 * Elem<T>::K * (Ms + nr) + 8.0 * nloc, s, [&] {
+        if (aligned)
+          k_node_gather_t<T, true, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, nloc, temp, cnt, lofs, giants,
+                                                                     ngiant, errw, lo);
+        else
+          k_node_gather_t<T, false, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, nloc, temp, cnt, lofs, giants,
+                                                                      ngiant, errw, lo);
+      }));
+      const int cap2 = 48 * 1024;
+      static PerDevice attr;
+      attr.once([&] {
+        cudaFuncSetAttribute(k_node_giant<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap2 * 4);
+        cudaFuncSetAttribute(k_node_giant<T, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap2 * 4);
+        return 0;
+      });
+      MN_CUDA(launch("node_giant", 0.0, s, [&] {
+        if (aligned)
+          k_node_giant<T, true, true><<<148, 1024, cap2 * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap2,
+                                                                 errw, lo);
+        else
+          k_node_giant<T, false, true><<<148, 1024, cap2 * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant,
+                                                                  cap2, errw, lo);
+      }));
+      MN_CUDA(launch("scan_counts", 12.0 * nloc, s, [&] {
+        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kScanThreads, 0, s>>>(
+            cnt, nloc, noff, sstatus, tickets + 2, 3);
+      }));
+      MN_CUDA(cudaMemcpyAsync(host + 1, noff + nloc, 8, cudaMemcpyDeviceToHost, s));
+      MN_CUDA(cudaStreamSynchronize(s));
+      const int64_t U = (int64_t)host[1];
+      prof_add_bytes("node_gather", 4.0 * U);
+      if (U) {
+        node_slice->indices = (int32_t*)mem.get((size_t)U * 4);
+        if (!node_slice->indices) { st = MN_ERR_OOM; goto done; }
+        MN_CUDA(launch("node_compact", 8.0 * U + 24.0 * nloc, s, [&] {
+          k_node_compact<<<(unsigned)tiles_of(nloc, kNodeThreads), kNodeThreads, 0, s>>>(eoff, C, temp, lofs, noff,
+                                                                                       nloc, node_slice->indices);
+        }));
+      }
+      node_slice->nnz = U;
+    }
+  }
+  node_slice->num_nodes = nloc;
+  node_slice->offsets = noff;
+  node_slice->owner = mem.a;
+  elem_slice->num_nodes = nloc;
+  elem_slice->nnz = n;
+  elem_slice->offsets = eoff;
+  elem_slice->indices = eidx;
+  elem_slice->owner = mem.a;
+  mem.put(ws);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return MN_ERR_CUDA;
+  return MN_OK;
+done:
+  cudaStreamSynchronize(s);
+  mem.put(ws);
+  mem.put(noff);
+  mem.put(eoff);
+  mem.put(eidx);
+  if (node_slice->indices) mem.put(node_slice->indices);
+  std::memset(node_slice, 0, sizeof(*node_slice));
+  std::memset(elem_slice, 0, sizeof(*elem_slice));
+  return st;
+}
+
 template <int T, int BINS>
-static mn_status dist_p2p_impl(const int32_t* conn, int64_t M, int64_t base, int64_t N, mn_symm* h, Mem& mem,
-                               mn_csr* node_slice, mn_csr* elem_slice, mn_dist_info* info, mn_error_detail* err) {
+static mn_status dist2_impl(const int32_t* conn, int64_t M, int64_t base, int64_t N, const mn_comm* comm, mn_symm* h,
+                            Mem& mem, mn_csr* node_slice, mn_csr* elem_slice, mn_dist_info* info,
+                            mn_error_detail* err) {
   constexpr int K = Elem<T>::K;
   cudaStream_t s = mem.s;
-  const mn_comm* comm = &h->comm;
+  const bool p2p = h != nullptr;
   const int G = comm->world, self = comm->rank;
   const int W = 2 + 2 * G;
   const Plan P = make_plan(T, M, N);
@@ -358,38 +389,77 @@ static mn_status dist_p2p_impl(const int32_t* conn, int64_t M, int64_t base, int
   std::vector<unsigned long long> hh(BINS, 0);
   std::vector<uint64_t*> dsth(G, nullptr);
   std::vector<int32_t*> rowh(G, nullptr);
+  std::vector<int64_t> sc(G, 0), sd(G, 0), rcn(G, 0), rd(G, 0), sdr(G, 0), rdr(G, 0);
   int64_t nnz2[2] = {0, 0};
   uint64_t ew = ERR_NONE;
-  int64_t in = 0, own = 0, own0 = 0;
-  size_t pairs_bytes = 0;
-  int32_t* relems = nullptr;
-  // staging: all-gather rows + per-destination pointer tables; workspace: err, tickets, histogram,
-  // bases, look-back status words
+  bool all_local = false;
+  int64_t in = 0, own = 0, own0 = 0, nr = 0;
+  uint64_t *sendp = nullptr, *recvp = nullptr;
+  int32_t *sendr = nullptr, *recvr = nullptr, *relems = nullptr;
+  const uint64_t* rpairs = nullptr;   // the received (and, without locality, own) incidences
+  const int32_t* rrows = nullptr;
   int64_t* dx = (int64_t*)mem.get((size_t)W * (G + 1) * 8 + (size_t)G * 16);
   if (!dx) return MN_ERR_OOM;
   void** dptr = (void**)(dx + (size_t)W * (G + 1));
   const int64_t tiles = tiles_of(Pe, kTile);
   Arena ar;
   unsigned long long* errw = ar.take<unsigned long long>(2);
+  unsigned long long* smp = ar.take<unsigned long long>(2);
   uint32_t* tickets = ar.take<uint32_t>(8);
   unsigned long long* hist = ar.take<unsigned long long>(BINS);
+  unsigned long long* hist2 = ar.take<unsigned long long>(BINS);
   uint64_t* bases = ar.take<uint64_t>(BINS);
   uint64_t* status = ar.take<uint64_t>((size_t)(tiles ? tiles : 1) * BINS);
+  unsigned long long* dnrem = ar.take<unsigned long long>(1);
   const size_t head = ar.off;
   char* ws = (char*)mem.get(ar.off);
+  bool loc = false;        // this shard's locality (the element algorithm of the 1-GPU path)
+  int64_t nrem = 0;        // remote incidences of this shard
+  uint64_t* rem = nullptr;   // (coherent shards) the remote incidences in element order
   if (!ws) local = MN_ERR_OOM;
   if (local == MN_OK) {
-    errw = (unsigned long long*)(ws + (size_t)errw); tickets = (uint32_t*)(ws + (size_t)tickets);
-    hist = (unsigned long long*)(ws + (size_t)hist); bases = (uint64_t*)(ws + (size_t)bases);
-    status = (uint64_t*)(ws + (size_t)status);
-    // ---- 1. validation + incidence counts per owner (one read of conn) ----
+    errw = (unsigned long long*)(ws + (size_t)errw); smp = (unsigned long long*)(ws + (size_t)smp);
+    tickets = (uint32_t*)(ws + (size_t)tickets); hist = (unsigned long long*)(ws + (size_t)hist);
+    hist2 = (unsigned long long*)(ws + (size_t)hist2);
+    bases = (uint64_t*)(ws + (size_t)bases); status = (uint64_t*)(ws + (size_t)status);
+    dnrem = (unsigned long long*)(ws + (size_t)dnrem);
+    const bool aligned = ((uintptr_t)conn & 15) == 0;
     if (cudaMemsetAsync(ws, 0, head, s) != cudaSuccess || cudaMemsetAsync(errw, 0xFF, 8, s) != cudaSuccess)
       local = MN_ERR_CUDA;
-    if (local == MN_OK && M > 0) {
-      if (launch("hist_validate", 4.0 * P.K * M, s, [&] {
-            k_hist_validate<T, BINS, false><<<hist_grid(M), 256, 0, s>>>(conn, M, N, base, P.dp, 1, chunk, hist, errw);
-          }) != cudaSuccess)
+    // ---- 0. locality of the shard (decides whether the remote incidences are compacted) ----
+    const int mode = g_elem_path.load();
+    if (local == MN_OK && M > 0 && mode == 0) {
+      if (launch("locality_sample", 0.0, s, [&] {
+            if (aligned) k_locality_sample<T, true><<<64, 256, 0, s>>>(conn, M, smp);
+            else k_locality_sample<T, false><<<64, 256, 0, s>>>(conn, M, smp);
+          }) != cudaSuccess ||
+          cudaMemcpyAsync(host + 2, smp, 16, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+          cudaStreamSynchronize(s) != cudaSuccess)
         local = MN_ERR_CUDA;
+    }
+    loc = M == 0 || mode == 2 ||
+          (mode == 0 && local == MN_OK && host[3] > 0 && (double)host[2] < kTransposeMaxGroupRatio * (double)host[3]);
+    if (loc && M > 0 && local == MN_OK) {
+      rem = (uint64_t*)mem.get((size_t)Pe * 8);
+      if (!rem) local = MN_ERR_OOM;
+    }
+    // ---- 1. validation + incidence counts per owner (+ the remote incidences), one host read ----
+    if (local == MN_OK && M > 0) {
+      cudaError_t e;
+      if (rem)
+        e = launch("hist_remote", 4.0 * P.K * M, s, [&] {
+          if (aligned)
+            k_hist_remote<T, BINS, true><<<hist_grid(M), 256, 0, s>>>(conn, M, N, base, chunk, G, self, hist, errw,
+                                                                        rem, dnrem);
+          else
+            k_hist_remote<T, BINS, false><<<hist_grid(M), 256, 0, s>>>(conn, M, N, base, chunk, G, self, hist, errw,
+                                                                         rem, dnrem);
+        });
+      else
+        e = launch("hist_validate", 4.0 * P.K * M, s, [&] {
+          k_hist_validate<T, BINS, false><<<hist_grid(M), 256, 0, s>>>(conn, M, N, base, P.dp, 1, chunk, hist, errw);
+        });
+      if (e != cudaSuccess) local = MN_ERR_CUDA;
     }
     if (local == MN_OK &&
         (cudaMemcpyAsync(hh.data(), hist, BINS * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -397,47 +467,130 @@ static mn_status dist_p2p_impl(const int32_t* conn, int64_t M, int64_t base, int
          cudaStreamSynchronize(s) != cudaSuccess))
       local = MN_ERR_CUDA;
     if (local == MN_OK) ew = host[0];
+    for (int g = 0; g < G; ++g)
+      if (g != self) nrem += (int64_t)hh[g];
   }
-  // ---- 2. count exchange + plan (the lowest error over all ranks is returned by every rank) ----
+  // ---- 2. count exchange: [error word, status, counts per owner, locality flag] ----
   row[0] = (int64_t)ew;
   row[1] = local;
   if (local == MN_OK && ew == ERR_NONE)
     for (int g = 0; g < G; ++g) row[2 + g] = (int64_t)hh[g];
+  row[2 + G] = (local == MN_OK && loc) ? 1 : 0;
   MN_CUDA(cudaMemcpyAsync(dx, row.data(), (size_t)W * 8, cudaMemcpyHostToDevice, s));
   if (comm->allgather(comm->ctx, dx, dx + W, (size_t)W * 8, (mn_stream)s) != 0) { st = MN_ERR_COMM; goto done; }
   MN_CUDA(cudaMemcpyAsync(all.data(), dx + W, (size_t)W * G * 8, cudaMemcpyDeviceToHost, s));
   MN_CUDA(cudaStreamSynchronize(s));
   st = dist_plan(G, self, all.data(), rc.data(), rr.data(), err);
   if (st != MN_OK) goto done;
-  // ---- 3. receive layouts of every rank (all ranks compute all of them), heap capacity ----
+  all_local = true;
+  for (int g = 0; g < G; ++g) all_local = all_local && all[(size_t)g * W + 2 + G] != 0;
+  // ---- 3. receive layouts (source-rank order; the own block only without locality) ----
   {
     auto cnt = [&](int r, int g) { return all[(size_t)r * W + 2 + g]; };
-    auto pbytes = [](int64_t n) { return ((size_t)n * 8 + 255) & ~(size_t)255; };   // pairs region
+    auto pbytes = [](int64_t n) { return ((size_t)n * 8 + 255) & ~(size_t)255; };
+    std::vector<int64_t> ing(G, 0), offp(G, 0), offr(G, 0);
     size_t need = 0;
-    std::vector<int64_t> offp(G, 0), offr(G, 0), ing(G, 0);
     for (int g = 0; g < G; ++g) {
-      for (int r = 0; r < G; ++r) ing[g] += cnt(r, g);
-      need = std::max(need, pbytes(ing[g]) + (size_t)(ing[g] - cnt(g, g)) * 4 * K + 256);
-      // where this rank's bucket for g starts in g's pairs region, and in g's row table (rows are
-      // kept for remote sources only: sources after g skip g's own block)
-      for (int r = 0; r < self; ++r) offp[g] += cnt(r, g);
-      offr[g] = offp[g] - (self > g ? cnt(g, g) : 0);
+      for (int r = 0; r < G; ++r)
+        if (r != g || !all_local) ing[g] += cnt(r, g);
+      const int64_t remote_in = ing[g] - (all_local ? 0 : cnt(g, g));
+      need = std::max(need, pbytes(ing[g]) + (size_t)remote_in * 4 * K + 256);
+      for (int r = 0; r < self; ++r)
+        if (r != g || !all_local) offp[g] += cnt(r, g);
+      // rows: remote sources only; sources after g skip g's own block (present without locality)
+      offr[g] = offp[g] - (!all_local && self > g ? cnt(g, g) : 0);
     }
     in = ing[self];
     own = cnt(self, self);
-    own0 = offp[self];
-    pairs_bytes = pbytes(in);
-    st = symm_reserve(h, need, s);
-    if (st != MN_OK) goto done;
-    for (int g = 0; g < G; ++g) {
-      dsth[g] = reinterpret_cast<uint64_t*>(h->peer[g]) + offp[g];
-      rowh[g] = g == self ? nullptr : reinterpret_cast<int32_t*>(h->peer[g] + pbytes(ing[g])) + offr[g] * K;
+    own0 = all_local ? 0 : offp[self];
+    nr = in - (all_local ? 0 : own);
+    if (p2p) {
+      st = symm_reserve(h, need, s);
+      if (st != MN_OK) goto done;
+      for (int g = 0; g < G; ++g) {
+        dsth[g] = (g == self && all_local) ? nullptr : reinterpret_cast<uint64_t*>(h->peer[g]) + offp[g];
+        rowh[g] = g == self ? nullptr : reinterpret_cast<int32_t*>(h->peer[g] + pbytes(ing[g])) + offr[g] * K;
+      }
+      rpairs = reinterpret_cast<const uint64_t*>(h->local);
+      rrows = reinterpret_cast<const int32_t*>(h->local + pbytes(in));
+    } else {
+      // local send buffers (remote buckets in rank order), receive buffers in source-rank order
+      int64_t ns = 0;
+      for (int g = 0; g < G; ++g)
+        if (g != self) ns += cnt(self, g);
+      sendp = ns ? (uint64_t*)mem.get((size_t)ns * 8) : nullptr;
+      sendr = ns ? (int32_t*)mem.get((size_t)ns * 4 * K) : nullptr;
+      recvp = in ? (uint64_t*)mem.get((size_t)in * 8) : nullptr;
+      recvr = nr ? (int32_t*)mem.get((size_t)nr * 4 * K) : nullptr;
+      if ((ns && (!sendp || !sendr)) || (in && !recvp) || (nr && !recvr)) { st = MN_ERR_OOM; goto done; }
+      int64_t a = 0, b = 0, c = 0;
+      for (int g = 0; g < G; ++g) {
+        if (g == self) {
+          dsth[g] = all_local ? nullptr : recvp + own0;   // own bucket in place (no exchange)
+        } else {
+          dsth[g] = sendp + a;
+          rowh[g] = sendr + a * K;
+          sd[g] = a;
+          sc[g] = cnt(self, g);
+          a += sc[g];
+        }
+        rd[g] = b;   // pairs received from g (own block skipped: not exchanged)
+        rcn[g] = g == self ? 0 : cnt(g, self);
+        b += (g == self) ? (all_local ? 0 : own) : rcn[g];
+        rdr[g] = c;
+        c += rcn[g];
+      }
+      rpairs = recvp;
+      rrows = recvr;
     }
   }
-  // ---- 4. fused bucket-and-send: one onesweep pass storing into the owners' heaps ----
+  // ---- 4. bucket-and-send: one onesweep pass over the shard's incidences ----
   MN_CUDA(cudaMemcpyAsync(dptr, dsth.data(), (size_t)G * 8, cudaMemcpyHostToDevice, s));
   MN_CUDA(cudaMemcpyAsync(dptr + G, rowh.data(), (size_t)G * 8, cudaMemcpyHostToDevice, s));
-  if (M > 0) {
+  if (M > 0 && all_local && nrem > 0) {
+    // only the remote incidences (appended by pass 1) are put in element order, bucketed and sent
+    {
+      uint32_t* rk = (uint32_t*)mem.get((size_t)nrem * 8);
+      if (!rk) { st = MN_ERR_OOM; goto done; }
+      uint32_t* rv = rk + nrem;
+      MN_CUDA(launch("remote_order", 16.0 * nrem, s, [&] {
+        k_split_pairs<<<stream_grid(nrem), 256, 0, s>>>(rem, nrem, base, rk, rv);
+      }));
+      st = lsd_sort<uint32_t, true>(rk, rv, nrem, node_bits(M), mem);
+      if (st == MN_OK)
+        MN_CUDA(launch("remote_order", 16.0 * nrem, s, [&] {
+          k_join_pairs<<<stream_grid(nrem), 256, 0, s>>>(rk, rv, nrem, base, rem);
+        }));
+      mem.put(rk);
+      if (st != MN_OK) goto done;
+    }
+    MN_CUDA(cudaMemcpyAsync(hist2, hist, BINS * 8, cudaMemcpyDeviceToDevice, s));
+    MN_CUDA(cudaMemsetAsync(hist2 + self, 0, 8, s));
+    BasesDesc bd{};
+    bd.npass = 1;
+    bd.hidx[0] = 0;
+    bd.mult[0] = 1;
+    MN_CUDA(launch("bucket_bases", 0.0, s, [&] { k_bucket_bases<BINS><<<1, BINS, 0, s>>>(hist2, bd, bases, errw); }));
+    PassArgs pe{};
+    pe.keys_in = rem; pe.conn = conn; pe.elem_base = base; pe.n = nrem;
+    pe.pd.shift = 32; pe.pd.div = chunk; pe.pd.mask = 0;
+    pe.bases = bases; pe.status = status; pe.ticket = tickets; pe.epoch = 1; pe.err = errw;
+    pe.dst = (uint64_t* const*)dptr;
+    pe.rowdst = (int32_t* const*)(dptr + G);
+    pe.self = self;
+    using Sm = OnesweepSmem<kPassThreads, kPassItems, BINS>;
+    const size_t smem = ((sizeof(Sm) + 15) & ~size_t(15)) + (size_t)kTile * 8;
+    auto kern = k_onesweep<uint64_t, 0, T, false, true, BINS, kPassThreads, kPassItems, kPassWindow, kPassMinBlocks,
+                           0, false, false, true>;
+    static PerDevice attr0;
+    attr0.once([&] {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      return 0;
+    });
+    MN_CUDA(launch(p2p ? "bucket_send_p2p" : "bucket_send", (16.0 + 4.0 * K) * nrem, s, [&] {
+      kern<<<(unsigned)tiles_of(nrem, kTile), kPassThreads, smem, s>>>(pe);
+    }));
+  } else if (M > 0 && !all_local) {
     BasesDesc bd{};
     bd.npass = 1;
     bd.hidx[0] = 0;
@@ -459,43 +612,56 @@ static mn_status dist_p2p_impl(const int32_t* conn, int64_t M, int64_t base, int
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       return 0;
     });
-    MN_CUDA(launch("bucket_send_p2p", 4.0 * Pe + 8.0 * Pe, s, [&] {
+    MN_CUDA(launch(p2p ? "bucket_send_p2p" : "bucket_send", 4.0 * Pe + 8.0 * Pe, s, [&] {
       kern<<<(unsigned)tiles, kPassThreads, smem, s>>>(pe);
     }));
   }
-  // ---- 5. barrier: every rank's stores into this heap are complete past this all-gather ----
-  MN_CUDA(cudaMemcpyAsync(dx, nnz2, 8, cudaMemcpyHostToDevice, s));
-  if (comm->allgather(comm->ctx, dx, dx + 2, 8, (mn_stream)s) != 0) { st = MN_ERR_COMM; goto done; }
-  // ---- 6. local finish over the heap (pairs in source-rank order, remote rows + their ids) ----
-  {
-    const int64_t nr = in - own;
-    const uint64_t* hp = (const uint64_t*)h->local;
-    const int32_t* hr = (const int32_t*)(h->local + pairs_bytes);
-    if (nr > 0) {
-      relems = (int32_t*)mem.get((size_t)nr * 4);
-      if (!relems) { st = MN_ERR_OOM; goto done; }
-      MN_CUDA(launch("remote_elems", 12.0 * nr, s, [&] {
-        k_remote_elems<<<stream_grid(nr), 256, 0, s>>>(hp, nr, own0, own, relems);
-      }));
-    }
-    if (in > INT32_MAX) { st = MN_ERR_CAPACITY; goto done; }
-    st = dist_finish_impl<T>(pair_src(hp, in), in, relems, hr, nr, conn, base, M, N, lo, hi, mem, node_slice,
-                             elem_slice);
-    if (st != MN_OK) goto done;
-    mem.put(relems);
-    relems = nullptr;
-    if (info) {
-      int64_t sent = 0, got = 0;
-      for (int g = 0; g < G; ++g)
-        if (g != self) {
-          sent += all[(size_t)self * W + 2 + g] * (8 + 4 * K);
-          got += all[(size_t)g * W + 2 + self] * (8 + 4 * K);
-        }
-      info->sent_bytes = sent;
-      info->recv_bytes = got;
-      info->own_incidences = own;
-    }
+  // ---- 5. the exchange ----
+  if (p2p) {   // barrier: every rank's stores into this heap are complete past this all-gather
+    MN_CUDA(cudaMemcpyAsync(dx, nnz2, 8, cudaMemcpyHostToDevice, s));
+    if (comm->allgather(comm->ctx, dx, dx + 2, 8, (mn_stream)s) != 0) { st = MN_ERR_COMM; goto done; }
+  } else {
+    std::vector<int64_t> scr(G, 0);
+    for (int g = 0; g < G; ++g) scr[g] = g == self ? 0 : sc[g];
+    const mn_a2a_op ops[2] = {
+        {sendp, scr.data(), sd.data(), recvp, rcn.data(), rd.data(), 8},
+        {sendr, scr.data(), sd.data(), recvr, rcn.data(), rdr.data(), (size_t)K * 4},
+    };
+    if (comm->alltoallv(comm->ctx, ops, 2, (mn_stream)s) != 0) { st = MN_ERR_COMM; goto done; }
+    mem.put(sendp); sendp = nullptr;
+    mem.put(sendr); sendr = nullptr;
   }
+  if (info) {
+    int64_t sent = 0, got = 0;
+    for (int g = 0; g < G; ++g)
+      if (g != self) {
+        sent += all[(size_t)self * W + 2 + g] * (8 + 4 * K);
+        got += all[(size_t)g * W + 2 + self] * (8 + 4 * K);
+      }
+    info->sent_bytes = sent;
+    info->recv_bytes = got;
+    info->own_incidences = own;
+  }
+  // ---- 6. finish ----
+  if (nr > 0) {
+    relems = (int32_t*)mem.get((size_t)nr * 4);
+    if (!relems) { st = MN_ERR_OOM; goto done; }
+    MN_CUDA(launch("remote_elems", 12.0 * nr, s, [&] {
+      k_remote_elems<<<stream_grid(nr), 256, 0, s>>>(rpairs, nr, all_local ? nr : own0, all_local ? 0 : own, relems);
+    }));
+  }
+  if (all_local) {
+    st = finish_own_conn<T>(conn, M, base, own, rpairs, nr, relems, rrows, lo, hi, mem, node_slice, elem_slice);
+  } else {
+    if (in > INT32_MAX) { st = MN_ERR_CAPACITY; goto done; }
+    st = dist_finish_impl<T>(pair_src(rpairs, in), in, relems, rrows, nr, conn, base, M, N, lo, hi, mem, node_slice,
+                             elem_slice);
+  }
+  if (st != MN_OK) goto done;
+  mem.put(relems); relems = nullptr;
+  mem.put(recvp); recvp = nullptr;
+  mem.put(recvr); recvr = nullptr;
+  mem.put(rem); rem = nullptr;
   // ---- 7. global offset bases ----
   nnz2[0] = node_slice->nnz;
   nnz2[1] = elem_slice->nnz;
@@ -520,23 +686,29 @@ done:
   cudaStreamSynchronize(s);
   mem.put(ws);
   mem.put(dx);
+  mem.put(sendp);
+  mem.put(sendr);
+  mem.put(recvp);
+  mem.put(recvr);
   mem.put(relems);
+  mem.put(rem);
   mn_csr_release(node_slice, (mn_stream)s);
   mn_csr_release(elem_slice, (mn_stream)s);
   return st;
 }
 
-static mn_status dist_p2p_dispatch(mn_elem_type t, const int32_t* conn, int64_t M, int64_t base, int64_t N, mn_symm* h,
-                                   Mem& mem, mn_csr* ns, mn_csr* es, mn_dist_info* info, mn_error_detail* err) {
-  const bool b512 = h->comm.world > 256;
-#define MN_P2P(TT) \
-  return b512 ? dist_p2p_impl<TT, 512>(conn, M, base, N, h, mem, ns, es, info, err) \
-              : dist_p2p_impl<TT, 256>(conn, M, base, N, h, mem, ns, es, info, err)
+static mn_status dist2_dispatch(mn_elem_type t, const int32_t* conn, int64_t M, int64_t base, int64_t N,
+                                const mn_comm* comm, mn_symm* h, Mem& mem, mn_csr* ns, mn_csr* es, mn_dist_info* info,
+                                mn_error_detail* err) {
+  const bool b512 = comm->world > 256;
+#define MN_D2(TT) \
+  return b512 ? dist2_impl<TT, 512>(conn, M, base, N, comm, h, mem, ns, es, info, err) \
+              : dist2_impl<TT, 256>(conn, M, base, N, comm, h, mem, ns, es, info, err)
   switch (t) {
-    case MN_TRI3: MN_P2P(MN_TRI3);
-    case MN_QUAD4: MN_P2P(MN_QUAD4);
-    case MN_TET4: MN_P2P(MN_TET4);
-    default: MN_P2P(MN_HEX8);
+    case MN_TRI3: MN_D2(MN_TRI3);
+    case MN_QUAD4: MN_D2(MN_QUAD4);
+    case MN_TET4: MN_D2(MN_TET4);
+    default: MN_D2(MN_HEX8);
   }
-#undef MN_P2P
+#undef MN_D2
 }

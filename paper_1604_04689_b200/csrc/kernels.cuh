@@ -471,11 +471,12 @@ k_onesweep(PassArgs pa) {
       const uint32_t dg = digit_of<KeyT, OWNER>(k, pa.pd, BINS - 1);
       const uint64_t g = sm.gofs[dg] + li;
       if constexpr (P2P) {
-        static_assert(SRC == 3 && OWNER, "P2P is the fused dist bucketing pass");
+        static_assert((SRC == 3 || SRC == 0) && OWNER, "P2P is the dist bucketing pass");
         constexpr int K = Elem<T>::K;
         const uint64_t r = g - pa.bases[dg];   // rank inside the bucket of owner dg
-        pa.dst[dg][r] = (uint64_t)k;
-        if ((int)dg != pa.self) {
+        uint64_t* dd = pa.dst[dg];
+        if (dd) dd[r] = (uint64_t)k;           // (a null destination drops the bucket: the own one,
+        if ((int)dg != pa.self && dd) {        //  when the owner reads its incidences from conn)
           const int64_t e = (int64_t)((uint64_t)k & 0xffffffffull) - pa.elem_base;
           int row[K];
           load_row<T, false>(pa.conn, e, row);
@@ -1260,7 +1261,7 @@ __global__ void __launch_bounds__(256)
 k_chunk_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __restrict__ cbase,
                 int32_t* __restrict__ ccur, int32_t* __restrict__ belem, uint8_t* __restrict__ bnode,
                 const unsigned long long* __restrict__ err, int64_t lo = 0, int64_t hi = INT64_MAX,
-                const unsigned int* __restrict__ guard = nullptr) {
+                const unsigned int* __restrict__ guard = nullptr, int64_t ebase = 0) {
   constexpr int K = Elem<T>::K;
   if (guard && *guard == 0u) return;   // fallback after a fixed-capacity bucket overflowed
   if (*err != ERR_NONE) return;
@@ -1282,7 +1283,7 @@ k_chunk_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __re
       b = __shfl_sync(FULL, b, leader);
       if (mine) {
         const int64_t pos = cbase[x] + b + __popc(peers & lanemask_lt());
-        belem[pos] = (int32_t)e;
+        belem[pos] = (int32_t)(ebase + e);
         bnode[pos] = (uint8_t)((RANGE ? (int)(v[p] - lo) : v[p]) & (kChunkNodes - 1));
       }
     }
@@ -1295,27 +1296,30 @@ k_chunk_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __re
 // cap sets *ovf and keeps only its first cap entries: the host queues the counted path
 // (k_chunk_count -> k_scan_i32 -> k_chunk_scatter, each guarded by *ovf) behind it, so the result
 // never depends on cap.  Saves the count pass's read of conn (config 5: 1.08 ms of 11.3).
-template <int T, bool ALIGNED, int MINB = 1>
+// RANGE (multi-GPU owners): only nodes of [lo, hi) are kept (local ids node - lo) and element ids
+// are written as ebase + e (the shard's global ids).
+template <int T, bool ALIGNED, int MINB = 1, bool RANGE = false>
 __global__ void __launch_bounds__(256, MINB)
 k_chunk_scatter_fixed(const int32_t* __restrict__ conn, int64_t M, int64_t N, int cap,
                       int32_t* __restrict__ ccur, int32_t* __restrict__ belem, uint8_t* __restrict__ bnode,
-                      unsigned long long* __restrict__ err, unsigned int* __restrict__ ovf) {
+                      unsigned long long* __restrict__ err, unsigned int* __restrict__ ovf, int64_t lo = 0,
+                      int64_t hi = INT64_MAX, int64_t ebase = 0) {
   constexpr int K = Elem<T>::K;
   const int lane = threadIdx.x & 31;
   // (grid-stride; a blocked assignment, each CTA on its own contiguous element range so that few
   // CTAs share a chunk counter at a time, measured the same: 2.10-2.28 vs 2.14 ms on config 5)
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
-  const int64_t hi = M;
+  const int64_t end = M;
   int nv[K];   // the next row, loaded one iteration ahead
-  if (base + lane < hi) load_row<T, ALIGNED>(conn, base + lane, nv);
-  for (; base < hi; base += stride) {
+  if (base + lane < end) load_row<T, ALIGNED>(conn, base + lane, nv);
+  for (; base < end; base += stride) {
     const int64_t e = base + lane;
-    const bool in = e < hi;
+    const bool in = e < end;
     int v[K];
 #pragma unroll
     for (int p = 0; p < K; ++p) v[p] = nv[p];
-    if (base + stride + lane < hi) load_row<T, ALIGNED>(conn, base + stride + lane, nv);
+    if (base + stride + lane < end) load_row<T, ALIGNED>(conn, base + stride + lane, nv);
     int bad = -1, kind = 0;
     if (in) {
 #pragma unroll
@@ -1338,20 +1342,21 @@ k_chunk_scatter_fixed(const int32_t* __restrict__ conn, int64_t M, int64_t N, in
     unsigned peers[K];
 #pragma unroll
     for (int p = 0; p < K; ++p) {
-      x[p] = ok ? (v[p] >> kChunkShift) : -1;   // one shared sentinel (match cost grows with distinct values)
+      const bool mine = ok && (!RANGE || (v[p] >= lo && v[p] < hi));
+      x[p] = mine ? (int)((RANGE ? v[p] - lo : v[p]) >> kChunkShift) : -1;   // one shared sentinel (match cost grows with distinct values)
       peers[p] = __match_any_sync(FULL, x[p]);
       b[p] = 0;
-      if (ok && lane == __ffs(peers[p]) - 1) b[p] = atomicAdd(ccur + x[p], (int)__popc(peers[p]));
+      if (x[p] >= 0 && lane == __ffs(peers[p]) - 1) b[p] = atomicAdd(ccur + x[p], (int)__popc(peers[p]));
     }
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       const int leader = __ffs(peers[p]) - 1;
-      if (ok && lane == leader && b[p] + (int)__popc(peers[p]) > cap) *ovf = 1u;
+      if (x[p] >= 0 && lane == leader && b[p] + (int)__popc(peers[p]) > cap) *ovf = 1u;
       const int q = __shfl_sync(FULL, b[p], leader) + __popc(peers[p] & lanemask_lt());
-      if (ok && q < cap) {
+      if (x[p] >= 0 && q < cap) {
         const int64_t pos = (int64_t)x[p] * cap + q;
-        belem[pos] = (int32_t)e;
-        bnode[pos] = (uint8_t)(v[p] & (kChunkNodes - 1));
+        belem[pos] = (int32_t)(ebase + e);
+        bnode[pos] = (uint8_t)((RANGE ? v[p] - lo : v[p]) & (kChunkNodes - 1));
       }
     }
   }
@@ -1885,6 +1890,98 @@ __global__ void __launch_bounds__(256)
 k_shift_offsets(const int64_t* __restrict__ in, int64_t n, int64_t base, int64_t* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = in[i] + base;
+}
+
+// Multi-GPU pass 1 for coherent meshes (one read of the shard, grid-stride like k_hist_validate):
+// validation (reading R8), the incidence count per owner rank, and the REMOTE incidences (owner !=
+// self) appended to rem[] (node << 32 | global element) with one atomic per warp and incidence slot
+// — in no particular order; the few remote incidences are put in element order afterwards.
+template <int T, int BINS, bool ALIGNED>
+__global__ void __launch_bounds__(256)
+k_hist_remote(const int32_t* __restrict__ conn, int64_t M, int64_t N, int64_t elem_base, uint64_t owner_div,
+              int world, int self, unsigned long long* __restrict__ hist, unsigned long long* __restrict__ err,
+              uint64_t* __restrict__ rem, unsigned long long* __restrict__ nrem) {
+  constexpr int K = Elem<T>::K;
+  __shared__ uint32_t sh[BINS];
+  for (int i = threadIdx.x; i < BINS; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int nown = 0;   // own incidences counted in a register (one shared atomic per warp at the end)
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < M; base += stride) {
+    const int64_t e = base + lane;
+    const bool in = e < M;
+    int v[K];
+    if (in) load_row<T, ALIGNED>(conn, e, v);
+    int bad = -1, kind = 0;
+    if (in) {
+#pragma unroll
+      for (int p = K - 1; p >= 0; --p)
+        if (v[p] < 0 || (int64_t)v[p] >= N) bad = p;
+      if (bad < 0) {
+#pragma unroll
+        for (int p = K - 1; p >= 1; --p) {
+          bool dup = false;
+#pragma unroll
+          for (int q = 0; q < p; ++q) dup |= (v[q] == v[p]);
+          if (dup) { bad = p; kind = 1; }
+        }
+      }
+      if (bad >= 0) atomicMin(err, (unsigned long long)err_encode((uint64_t)(elem_base + e), kind, bad));
+    }
+    const bool ok = in && bad < 0;
+    uint32_t rmask = 0;   // incidences of this element owned by another rank
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      if (!ok) continue;
+      uint64_t o = owner_div <= 0xFFFFFFFFull ? (uint64_t)((uint32_t)v[p] / (uint32_t)owner_div)
+                                              : (uint64_t)v[p] / owner_div;
+      o = o < (uint64_t)world ? o : (uint64_t)world - 1;
+      if ((int)o != self) {
+        atomicAdd(&sh[o], 1u);
+        rmask |= 1u << p;
+      } else {
+        ++nown;
+      }
+    }
+    if (__any_sync(FULL, rmask != 0)) {   // rare on a coherent mesh: one atomic per warp and slot
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        const bool remote = (rmask >> p) & 1u;
+        const unsigned rb = __ballot_sync(FULL, remote);
+        if (!rb) continue;
+        unsigned long long at = 0;
+        if (lane == __ffs(rb) - 1) at = atomicAdd(nrem, (unsigned long long)__popc(rb));
+        at = __shfl_sync(FULL, at, __ffs(rb) - 1);
+        if (remote)
+          rem[at + __popc(rb & lanemask_lt())] = ((uint64_t)(uint32_t)v[p] << 32) | (uint64_t)(elem_base + e);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nown += __shfl_xor_sync(FULL, nown, o);
+  if (lane == 0 && nown) atomicAdd(&sh[self], (uint32_t)nown);
+  __syncthreads();
+  for (int i = threadIdx.x; i < BINS; i += blockDim.x)
+    if (sh[i]) atomicAdd(hist + i, (unsigned long long)sh[i]);
+}
+
+// (node << 32 | element) pairs <-> (element - base key, node payload) for sorting the remote
+// incidences by element with the u32 onesweep.
+__global__ void __launch_bounds__(256)
+k_split_pairs(const uint64_t* __restrict__ pairs, int64_t n, int64_t base, uint32_t* __restrict__ keys,
+              uint32_t* __restrict__ vals) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t q = pairs[i];
+    keys[i] = (uint32_t)((int64_t)(q & 0xffffffffull) - base);
+    vals[i] = (uint32_t)(q >> 32);
+  }
+}
+__global__ void __launch_bounds__(256)
+k_join_pairs(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t n, int64_t base,
+             uint64_t* __restrict__ pairs) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    pairs[i] = ((uint64_t)vals[i] << 32) | (uint64_t)(base + (int64_t)keys[i]);
 }
 
 // The incidences an owner finishes, in source-rank order, as up to three pieces: those received

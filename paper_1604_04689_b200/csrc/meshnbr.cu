@@ -2362,7 +2362,7 @@ mn_status mn_find_neighbors_dist(mn_elem_type t, const int32_t* d_conn, int64_t 
   if (base + M > INT32_MAX) return MN_ERR_CAPACITY;
   if (info) std::memset(info, 0, sizeof(*info));
   Mem mem(a, (cudaStream_t)stream);
-  return dist_dispatch(t, d_conn, M, base, N, comm, mem, node_slice, elem_slice, info, err);
+  return dist2_dispatch(t, d_conn, M, base, N, comm, nullptr, mem, node_slice, elem_slice, info, err);
 }
 
 mn_status mn_symm_create(const mn_comm* comm, size_t initial_bytes, mn_symm** out) {
@@ -2410,7 +2410,7 @@ mn_status mn_find_neighbors_dist_p2p(mn_elem_type t, const int32_t* d_conn, int6
   if (base + M > INT32_MAX) return MN_ERR_CAPACITY;
   if (info) std::memset(info, 0, sizeof(*info));
   Mem mem(a, (cudaStream_t)stream);
-  return dist_p2p_dispatch(t, d_conn, M, base, N, symm, mem, node_slice, elem_slice, info, err);
+  return dist2_dispatch(t, d_conn, M, base, N, &symm->comm, symm, mem, node_slice, elem_slice, info, err);
 }
 
 static mn_status dist_one(bool node, mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t base, int64_t N,

@@ -285,7 +285,10 @@ def _edge_worker(rank, world, port, q):
             ("empty mesh", meshgen.HEX8, (torch.zeros((0, 8), dtype=torch.int32), 11)),
             ("fan hub owned by rank 0", meshgen.TRI3, meshgen.nonmanifold_fan(300)),
         ]
-        for name, et, (conn, N) in cases:
+        cases.append(("kuhn 9 (coherent)", meshgen.TET4, meshgen.kuhn_tets(9)))
+        cases.append(("hex 6 relabelled", meshgen.HEX8, (meshgen.relabel(*meshgen.hex_grid(6), 3, 4), 343)))
+        for (name, et, (conn, N)), path in [(c, p) for c in cases for p in ("auto", "radix", "transpose")]:
+            mn.set_elem_path(path)   # radix: every shard "without locality"; transpose: "with"
             M = conn.shape[0]
             s0, s1 = rank * M // world, (rank + 1) * M // world
             ro, ri = oracle.node_csr(et, conn, N)
@@ -296,8 +299,9 @@ def _edge_worker(rank, world, port, q):
                 good = (np.array_equal(no.cpu().numpy(), ro) and np.array_equal(ni.cpu().numpy(), ri)
                         and np.array_equal(eo.cpu().numpy(), so) and np.array_equal(ei.cpu().numpy(), si))
                 if not good:
-                    q.put((rank, False, f"{name} p2p={p2p}"))
+                    q.put((rank, False, f"{name} {path} p2p={p2p}"))
                     ok = False
+        mn.set_elem_path("auto")
         release_comms()
         q.put((rank, bool(ok), "edge cases"))
     except Exception as e:  # noqa: BLE001
