@@ -406,7 +406,7 @@ mn_status mn_comm_from_nccl(void* nccl_comm, mn_comm* out);
 
 /* Host-only exchange plan of step 2 (used by mn_find_neighbors_dist; exported so the protocol can
  * be checked without a GPU).  gathered: world rows of (2 + 2 * world) int64 each, row g =
- * [error word of rank g, status of rank g, counts_g[0..world), row_counts_g[0..world)]
+ * [error word of rank g, status of rank g, counts_g[0..world), aux_g[0..world)]
  * where counts_g[h] are the incidences rank g sends to rank h and aux_g[h] a per-destination
  * auxiliary count (mn_find_neighbors_dist stores rank g's locality flag in aux_g[0]).  Writes
  * recv_counts[g] = counts_g[rank] and recv_row_counts[g] = aux_g[rank] and returns the
