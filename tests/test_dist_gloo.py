@@ -139,8 +139,9 @@ def test_dist_plan_gloo(world, bad):
 # 2. model of the whole call: partition, in-place own bucket, exchange, finish, bases
 # ------------------------------------------------------------------------------------------------
 def _bucket_model(conn, etype, base, N, world, rank):
-    """Stand-in for step 1 (CUDA in the product): incidences (node << 32 | element) stably bucketed
-    by owner; one remote row per (destination != rank, element), grouped by destination."""
+    """Stand-in for steps 1 and 3 (CUDA in the product): incidences (node << 32 | element) stably
+    bucketed by owner, element-major inside a bucket; each REMOTE incidence travels with its
+    element's row (the product's bucket-and-send); the own bucket stays in place."""
     k = stages.ARITY[etype]
     en, ee = stages.expand_elem_pairs(etype, conn)
     own = _owner(en, N, world)
@@ -149,7 +150,7 @@ def _bucket_model(conn, etype, base, N, world, rank):
     owns, elems = own[order], ee[order]
     relems, rows = [], []
     for g in range(world):
-        sel = np.unique(elems[owns == g]) if g != rank else np.zeros(0, np.int64)
+        sel = elems[owns == g] if g != rank else np.zeros(0, np.int64)
         relems.append(sel + base)
         rows.append(conn.reshape(-1, k)[sel])
     return pairs, np.bincount(own, minlength=world), relems, rows
@@ -211,7 +212,7 @@ def _model_worker(rank, world, port, name, q):
         s0, s1 = rank * M // world, (rank + 1) * M // world
         shard = conn[s0:s1]
         pairs, counts, relems, rows = _bucket_model(shard, et, s0, N, world, rank)
-        row = np.concatenate([[-1, 0], counts, [len(r) for r in relems]]).astype(np.int64)
+        row = np.concatenate([[-1, 0], counts, [len(r) for r in relems]]).astype(np.int64)   # aux: rows sent
         st, rc, rr, _, _ = mn.dist_plan(world, rank, _gather_rows(row, world))
         assert st == mn.MN_OK
         splits = np.split(pairs, np.cumsum(counts)[:-1])
@@ -246,3 +247,4 @@ def _model_worker(rank, world, port, name, q):
 def test_dist_protocol_model_gloo(world, name):
     for rank, ok, info in _spawn(_model_worker, world, name):
         assert ok, f"rank {rank}: {info}"
+        assert isinstance(info, int)
