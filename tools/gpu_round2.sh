@@ -5,6 +5,8 @@
 TAG=${1:-r2}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; tail -1 gpurun_out/smoke_$TAG.log
+timeout 2400 python -m pytest tests -q -m gpu --durations=15 > gpurun_out/pytest_gpu_$TAG.log 2>&1; tail -2 gpurun_out/pytest_gpu_$TAG.log
+python tools/dist_world1.py 5 > gpurun_out/dist_world1_${TAG}_cfg5.json 2>/dev/null
 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -1 gpurun_out/bench_$TAG.err
 for c in 1 2 3 4 6; do
   python bench.py --config $c --cpu-seconds 6 > gpurun_out/bench_${TAG}_cfg$c.json 2>/dev/null
