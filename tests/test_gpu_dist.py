@@ -328,3 +328,131 @@ def test_dist_edge_cases_multi_rank_one_gpu():
         p.join(timeout=60)
     for rank, ok, info in out:
         assert ok, f"rank {rank}: {info}"
+
+
+# ------------------------------------------------------------------------------------------------
+# The PRODUCT multi-GPU path (mn_find_neighbors_dist) with G ranks as G threads of one process on
+# one GPU: a thread-based mn_comm (host-staged all-gather / all-to-all(v), threading barriers)
+# stands in for NCCL, each rank on its own CUDA stream.
+# ------------------------------------------------------------------------------------------------
+class _ThreadComm:
+    def __init__(self, shared, rank):
+        import paper_1604_04689_b200 as mn
+        self.sh, self.rank = shared, rank
+        self.struct = mn.Comm()
+        self.struct.rank, self.struct.world = rank, shared["world"]
+        self._ag = mn.ALLGATHER_FN(self._allgather)
+        self._a2a = mn.ALLTOALLV_FN(self._alltoallv)
+        self.struct.allgather, self.struct.alltoallv = self._ag, self._a2a
+
+    def _allgather(self, ctx, d_send, d_recv, nbytes, stream):
+        import paper_1604_04689_b200 as mn
+        try:
+            sh, W = self.sh, self.sh["world"]
+            h = torch.empty(nbytes, dtype=torch.uint8)
+            mn.memcpy_sync(h.data_ptr(), d_send, nbytes, stream)
+            sh["parts"][self.rank] = h
+            sh["bar"].wait()
+            cat = torch.cat([sh["parts"][g] for g in range(W)])
+            mn.memcpy_sync(d_recv, cat.data_ptr(), nbytes * W, stream)
+            sh["bar"].wait()
+            return 0
+        except Exception:  # noqa: BLE001
+            sh["bar"].abort()
+            return 1
+
+    def _alltoallv(self, ctx, ops, n_ops, stream):
+        import paper_1604_04689_b200 as mn
+        try:
+            sh, W = self.sh, self.sh["world"]
+            for o in range(n_ops):
+                op = ops[o]
+                eb = int(op.elem_bytes)
+                for g in range(W):
+                    n = int(op.send_counts[g]) * eb
+                    h = torch.empty(n, dtype=torch.uint8)
+                    if n:
+                        mn.memcpy_sync(h.data_ptr(), op.send + int(op.send_displs[g]) * eb, n, stream)
+                    sh["box"][(self.rank, g, o)] = h
+                sh["bar"].wait()
+                for g in range(W):
+                    h = sh["box"][(g, self.rank, o)]
+                    n = int(op.recv_counts[g]) * eb
+                    assert h.numel() == n
+                    if n:
+                        mn.memcpy_sync(op.recv + int(op.recv_displs[g]) * eb, h.data_ptr(), n, stream)
+                sh["bar"].wait()
+            return 0
+        except Exception:  # noqa: BLE001
+            sh["bar"].abort()
+            return 1
+
+
+def _threaded_ranks(conn, et, N, G):
+    import threading
+
+    import paper_1604_04689_b200 as mn
+    M = conn.shape[0]
+    shared = {"world": G, "parts": [None] * G, "box": {}, "bar": threading.Barrier(G)}
+    results, errors = [None] * G, []
+
+    def run(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            comm = _ThreadComm(shared, r)
+            s0, s1 = r * M // G, (r + 1) * M // G
+            with torch.cuda.stream(s):
+                shard = conn[s0:s1].contiguous()
+                results[r] = mn.find_neighbors_dist_comm(shard, et, s0, N, comm.struct, stream=s)
+            s.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errors.append((r, repr(e)))
+            shared["bar"].abort()
+
+    torch.cuda.synchronize()   # conn is complete before the ranks' streams read it
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(G)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    out = []
+    for which in (0, 1):
+        offs, idxs, tot = [], [], 0
+        for r in range(G):
+            off, idx = results[r][which]
+            offs.append(off[:-1] + tot)
+            idxs.append(idx)
+            tot += idx.numel()
+        out.append((torch.cat(offs + [torch.tensor([tot], device=offs[0].device)]), torch.cat(idxs)))
+    return out, [results[r][2] for r in range(G)]
+
+
+@pytest.mark.parametrize("G", [2, 3, 5])
+@pytest.mark.parametrize("name,et,make", [
+    ("kuhn_10", meshgen.TET4, lambda: meshgen.kuhn_tets(10)),
+    ("hex_8_perm", meshgen.HEX8, lambda: (meshgen.relabel(*meshgen.hex_grid(8), 5, 6), 729)),
+])
+def test_product_path_threaded_ranks(G, name, et, make):
+    conn, N = make()
+    (no, ni), (eo, ei) = _threaded_ranks(conn.cuda(), et, N, G)[0]
+    ro, ri = oracle.node_csr(et, conn, N)
+    so, si = oracle.elem_csr(et, conn, N)
+    assert np.array_equal(no.cpu().numpy(), ro) and np.array_equal(ni.cpu().numpy(), ri)
+    assert np.array_equal(eo.cpu().numpy(), so) and np.array_equal(ei.cpu().numpy(), si)
+
+
+@pytest.mark.slow
+def test_product_path_full_config5_eight_ranks():
+    """Full config 5 through mn_find_neighbors_dist with 8 ranks (threads on one GPU): the
+    concatenated slices equal the 1-GPU CSRs bit for bit; remote traffic is the boundary layer."""
+    import paper_1604_04689_b200 as mn
+    et, conn, N = meshgen.make_config(5, device="cuda")
+    ref = [(a.cpu(), b.cpu()) for a, b in mn.find_neighbors(conn, et, N)]
+    torch.cuda.empty_cache()
+    got, infos = _threaded_ranks(conn, et, N, 8)
+    for a, b in zip(ref, got):
+        assert torch.equal(a[0], b[0].cpu()) and torch.equal(a[1], b[1].cpu())
+    own = sum(i.own_incidences for i in infos)
+    assert 0.95 < own / (4 * conn.shape[0]) < 1.0
