@@ -168,6 +168,32 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// ---- bulk asynchronous copies (TMA 1-D, cp.async.bulk) into shared memory, mbarrier completion ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");   // visible to the async proxy
+}
+// arrive (one of the init count) and expect `bytes` of transactions on the current phase
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// global -> shared bulk copy: dst, src 16-byte aligned, bytes a multiple of 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n MN_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MN_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // Streaming loads that do not pollute L1 (each key is read exactly once per pass).
 __device__ __forceinline__ uint64_t ld_stream(const uint64_t* p) {
   uint64_t v;
@@ -203,6 +229,37 @@ template <> struct Elem<MN_HEX8> {   // VTK: (0,1)(1,2)(2,3)(3,0)(4,5)(5,6)(6,7)
   static constexpr uint64_t A_LO = 0x4776655403322110ull, A_HI = 0x73625140ull,
                             B_LO = 0x7467564530231201ull, B_HI = 0x37261504ull;
 };
+
+// Validation of one element row (R8): the lowest offending position, an index outside
+// [0, N) before a repeated node (kind 0 / 1), or -1.  N <= INT32_MAX (checked at the C ABI), so one
+// unsigned compare per entry covers both bounds; the common valid row costs one OR-chain of
+// compares and the position is only worked out for a bad row.
+template <int K>
+__device__ __forceinline__ int row_bad(const int (&v)[K], uint32_t N, int& kind) {
+  bool any = false;
+#pragma unroll
+  for (int p = 0; p < K; ++p) any |= (uint32_t)v[p] >= N;
+#pragma unroll
+  for (int p = 1; p < K; ++p)
+#pragma unroll
+    for (int q = 0; q < p; ++q) any |= v[q] == v[p];
+  kind = 0;
+  if (!any) return -1;
+  int bad = -1;
+#pragma unroll
+  for (int p = K - 1; p >= 0; --p)
+    if ((uint32_t)v[p] >= N) bad = p;
+  if (bad >= 0) return bad;
+#pragma unroll
+  for (int p = K - 1; p >= 1; --p) {
+    bool dup = false;
+#pragma unroll
+    for (int q = 0; q < p; ++q) dup |= (v[q] == v[p]);
+    if (dup) bad = p;
+  }
+  kind = 1;
+  return bad;
+}
 
 template <int T>
 __device__ __forceinline__ void slot_locals(int r, int& la, int& lb) {

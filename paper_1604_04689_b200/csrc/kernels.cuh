@@ -81,20 +81,9 @@ k_hist_validate(const int32_t* __restrict__ conn, int64_t M, int64_t N, int64_t 
 #pragma unroll
       for (int p = 0; p < K; ++p) v[p] = 0;
     }
-    int bad = -1, kind = 0;
+    int kind = 0;
+    const int bad = in ? row_bad<K>(v, (uint32_t)N, kind) : -1;
     if (in) {
-#pragma unroll
-      for (int p = K - 1; p >= 0; --p)
-        if (v[p] < 0 || (int64_t)v[p] >= N) bad = p;
-      if (bad < 0) {
-#pragma unroll
-        for (int p = K - 1; p >= 1; --p) {
-          bool dup = false;
-#pragma unroll
-          for (int q = 0; q < p; ++q) dup |= (v[q] == v[p]);
-          if (dup) { bad = p; kind = 1; }
-        }
-      }
       if (bad >= 0) atomicMin(err, (unsigned long long)err_encode((uint64_t)(elem_base + e), kind, bad));
     }
     const bool ok = in && bad < 0;
@@ -677,7 +666,11 @@ struct RowSrc {
 
 template <int T, bool ALIGNED, bool DIST>
 __device__ __forceinline__ void fetch_row(const RowSrc& rs, int64_t e, int (&row)[Elem<T>::K]) {
-  if (!DIST || (e >= rs.base && e < rs.base + rs.M)) {
+  if (!DIST) {   // 0 <= e < 2^31: 32-bit index, one wide multiply-add for the row address
+    load_row<T, ALIGNED>(rs.conn, (uint64_t)(uint32_t)e, row);
+    return;
+  }
+  if (e >= rs.base && e < rs.base + rs.M) {
     load_row<T, ALIGNED>(rs.conn, e - rs.base, row);
     return;
   }
@@ -840,12 +833,13 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
         const int4* ap = reinterpret_cast<const int4*>(ad & ~(uintptr_t)15);
         const int4 lo = __ldg(ap);
         const int4 hi = r + n > 4 ? __ldg(ap + 1) : lo;
-        const int w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+        // e[q] = word q + r of the 8-word window: a two-level select on the bits of r (10 selects,
+        // no divergent branches on the lane-dependent r)
+        const bool r1 = (r & 2) != 0, r0 = (r & 1) != 0;
+        const int u[5] = {r1 ? lo.z : lo.x, r1 ? lo.w : lo.y, r1 ? hi.x : lo.z, r1 ? hi.y : lo.w,
+                          r1 ? hi.z : hi.x};
 #pragma unroll
-        for (int q = 0; q < B; ++q) {
-          const int v = r == 0 ? w[q] : r == 1 ? w[q + 1] : r == 2 ? w[q + 2] : w[q + 3];
-          e[q] = q < n ? v : -1;
-        }
+        for (int q = 0; q < B; ++q) e[q] = q < n ? (r0 ? u[q + 1] : u[q]) : -1;
       }
       int row[B][K];
 #pragma unroll
@@ -1213,6 +1207,7 @@ constexpr int kChunkShift = MN_CHUNK_SHIFT;
 constexpr int kChunkNodes = 1 << kChunkShift;
 static_assert(kChunkNodes <= 256, "local node ids are bytes");
 constexpr int kChunkCap = 4096;   // bucket entries staged in shared memory (Kuhn tets: 3072)
+constexpr int kStage = 3584;      // k_chunk_sort: bucket entries read by bulk copy (larger: register loads; 6 CTAs/SM)
 
 // RANGE: only nodes of [lo, hi) (the memory-bounded mode); compiled out of the whole-path kernels
 template <int T, bool ALIGNED, bool RANGE = false>
@@ -1229,20 +1224,9 @@ k_chunk_count(const int32_t* __restrict__ conn, int64_t M, int64_t N, int32_t* _
     const bool in = e < M;
     int v[K];
     if (in) load_row<T, ALIGNED>(conn, e, v);
-    int bad = -1, kind = 0;
+    int kind = 0;
+    const int bad = in ? row_bad<K>(v, (uint32_t)N, kind) : -1;
     if (in) {
-#pragma unroll
-      for (int p = K - 1; p >= 0; --p)
-        if (v[p] < 0 || (int64_t)v[p] >= N) bad = p;
-      if (bad < 0) {
-#pragma unroll
-        for (int p = K - 1; p >= 1; --p) {
-          bool dup = false;
-#pragma unroll
-          for (int q = 0; q < p; ++q) dup |= (v[q] == v[p]);
-          if (dup) { bad = p; kind = 1; }
-        }
-      }
       if (bad >= 0) atomicMin(err, (unsigned long long)err_encode((uint64_t)e, kind, bad));
     }
     const bool ok = in && bad < 0;
@@ -1308,32 +1292,23 @@ k_chunk_scatter_fixed(const int32_t* __restrict__ conn, int64_t M, int64_t N, in
   const int lane = threadIdx.x & 31;
   // (grid-stride; a blocked assignment, each CTA on its own contiguous element range so that few
   // CTAs share a chunk counter at a time, measured the same: 2.10-2.28 vs 2.14 ms on config 5)
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
-  const int64_t end = M;
+  // 32-bit element indices (M <= INT32_MAX, checked at the C ABI; base + stride < 2^32)
+  const uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  const uint32_t end = (uint32_t)M;
+  bool over = false;   // some incidence of this thread found its bucket full (flagged once at the end)
   int nv[K];   // the next row, loaded one iteration ahead
-  if (base + lane < end) load_row<T, ALIGNED>(conn, base + lane, nv);
+  if (base + lane < end) load_row<T, ALIGNED>(conn, (uint64_t)(base + lane), nv);
   for (; base < end; base += stride) {
-    const int64_t e = base + lane;
+    const uint32_t e = base + lane;
     const bool in = e < end;
     int v[K];
 #pragma unroll
     for (int p = 0; p < K; ++p) v[p] = nv[p];
-    if (base + stride + lane < end) load_row<T, ALIGNED>(conn, base + stride + lane, nv);
-    int bad = -1, kind = 0;
+    if (base + stride + lane < end) load_row<T, ALIGNED>(conn, (uint64_t)(base + stride + lane), nv);
+    int kind = 0;
+    const int bad = in ? row_bad<K>(v, (uint32_t)N, kind) : -1;
     if (in) {
-#pragma unroll
-      for (int p = K - 1; p >= 0; --p)
-        if (v[p] < 0 || (int64_t)v[p] >= N) bad = p;
-      if (bad < 0) {
-#pragma unroll
-        for (int p = K - 1; p >= 1; --p) {
-          bool dup = false;
-#pragma unroll
-          for (int q = 0; q < p; ++q) dup |= (v[q] == v[p]);
-          if (dup) { bad = p; kind = 1; }
-        }
-      }
       if (bad >= 0) atomicMin(err, (unsigned long long)err_encode((uint64_t)e, kind, bad));
     }
     const bool ok = in && bad < 0;
@@ -1348,18 +1323,23 @@ k_chunk_scatter_fixed(const int32_t* __restrict__ conn, int64_t M, int64_t N, in
       b[p] = 0;
       if (x[p] >= 0 && lane == __ffs(peers[p]) - 1) b[p] = atomicAdd(ccur + x[p], (int)__popc(peers[p]));
     }
+    const int32_t eid = (int32_t)(ebase + e);
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       const int leader = __ffs(peers[p]) - 1;
-      if (x[p] >= 0 && lane == leader && b[p] + (int)__popc(peers[p]) > cap) *ovf = 1u;
       const int q = __shfl_sync(FULL, b[p], leader) + __popc(peers[p] & lanemask_lt());
-      if (x[p] >= 0 && q < cap) {
-        const int64_t pos = (int64_t)x[p] * cap + q;
-        belem[pos] = (int32_t)(ebase + e);
-        bnode[pos] = (uint8_t)((RANGE ? v[p] - lo : v[p]) & (kChunkNodes - 1));
+      if (x[p] >= 0) {
+        if (q < cap) {
+          const uint64_t pos = (uint64_t)(uint32_t)x[p] * (uint32_t)cap + (uint32_t)q;   // one wide multiply-add
+          belem[pos] = eid;
+          bnode[pos] = (uint8_t)((RANGE ? v[p] - lo : v[p]) & (kChunkNodes - 1));
+        } else {
+          over = true;
+        }
       }
     }
   }
+  if (over) *ovf = 1u;
 }
 
 // One CTA (kChunkNodes threads) per chunk, one pass over the bucket (SORT = false, node-only
@@ -1383,7 +1363,7 @@ __device__ __forceinline__ void sort_slot_column(int32_t* slots, int t, int d) {
     if (i < d) slots[i * kSlotPitch + t] = v[i];
 }
 
-template <bool SORT, int MINB = 1024 / kChunkNodes>
+template <bool SORT, int MINB = 6>
 __global__ void __launch_bounds__(kChunkNodes, MINB)
 k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __restrict__ belem,
               const uint8_t* __restrict__ bnode, int64_t* __restrict__ eoff, int32_t* __restrict__ eidx,
@@ -1395,6 +1375,9 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
   __shared__ int s_ex[kChunkNodes];
   __shared__ int s_wsum[kChunkNodes / 32];
   __shared__ int s_over;
+  __shared__ alignas(16) int32_t s_el[kStage];   // the bucket, brought in by two bulk copies
+  __shared__ alignas(16) uint8_t s_nd[kStage];
+  __shared__ alignas(8) uint64_t s_bar;
   if (err && *err != ERR_NONE) return;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t c = blockIdx.x;
@@ -1402,12 +1385,42 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
   const int64_t b0 = cbase[c], b1 = cbase[c + 1];
   const int n = (int)(b1 - b0);
   // where the bucket is: fixed-capacity layout (k_chunk_scatter_fixed) unless it overflowed
-  const int64_t bb = (ovf && *ovf == 0u) ? c * (int64_t)cap : b0;
+  const bool fixed = ovf && *ovf == 0u;
+  const int64_t bb = fixed ? c * (int64_t)cap : b0;
+  // CTA-uniform: a fixed-capacity bucket (cap a multiple of 16, so the copies rounded up to 16
+  // entries stay inside it) that fits the stage is read with TMA bulk copies -- the whole bucket in
+  // flight at once instead of one 4-entry group per thread (the register-load version waited on
+  // its loads for 35% of its samples, ncu r1v)
+  const bool bulk = fixed && (cap & 15) == 0 && n > 0 && n <= kStage;
+  if (bulk && t == 0) mbar_init(&s_bar, 1);
   s_cnt[t] = 0;
   if (t == 0) s_over = 0;
   __syncthreads();
   constexpr int U = 4;
-  if ((bb & 15) == 0) {   // CTA-uniform: 16-byte aligned bucket (the fixed layout) -> vector loads
+  if (bulk) {
+    if (t == 0) {
+      const uint32_t be = (uint32_t)((n + 3) & ~3) * 4u, bn = (uint32_t)((n + 15) & ~15);   // within cap
+      mbar_arrive_expect_tx(&s_bar, be + bn);
+      bulk_g2s(s_el, belem + bb, be, &s_bar);
+      bulk_g2s(s_nd, bnode + bb, bn, &s_bar);
+    }
+    mbar_wait(&s_bar, 0);
+    for (int i0 = 0; i0 < n; i0 += U * kChunkNodes) {
+      const int i = i0 + U * t;
+      if (i >= n) break;
+      const uint32_t nq = *reinterpret_cast<const uint32_t*>(s_nd + i);
+      const int4 eq = *reinterpret_cast<const int4*>(s_el + i);
+      const int nd[U] = {(int)(nq & 255), (int)((nq >> 8) & 255), (int)((nq >> 16) & 255), (int)(nq >> 24)};
+      const int32_t el[U] = {eq.x, eq.y, eq.z, eq.w};
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i + u < n) {
+          const int pos = atomicAdd(&s_cnt[nd[u]], 1);
+          if (pos < kSegMax) slots[pos * kSlotPitch + nd[u]] = el[u];
+          else s_over = 1;
+        }
+    }
+  } else if ((bb & 15) == 0) {   // CTA-uniform: 16-byte aligned bucket (the fixed layout) -> vector loads
     // thread t takes entries [i0 + 4t, i0 + 4t + 4): one 4-byte node load + one int4 element load
     for (int i0 = 0; i0 < n; i0 += U * kChunkNodes) {
       const int i = i0 + U * t;
@@ -1913,20 +1926,9 @@ k_hist_remote(const int32_t* __restrict__ conn, int64_t M, int64_t N, int64_t el
     const bool in = e < M;
     int v[K];
     if (in) load_row<T, ALIGNED>(conn, e, v);
-    int bad = -1, kind = 0;
+    int kind = 0;
+    const int bad = in ? row_bad<K>(v, (uint32_t)N, kind) : -1;
     if (in) {
-#pragma unroll
-      for (int p = K - 1; p >= 0; --p)
-        if (v[p] < 0 || (int64_t)v[p] >= N) bad = p;
-      if (bad < 0) {
-#pragma unroll
-        for (int p = K - 1; p >= 1; --p) {
-          bool dup = false;
-#pragma unroll
-          for (int q = 0; q < p; ++q) dup |= (v[q] == v[p]);
-          if (dup) { bad = p; kind = 1; }
-        }
-      }
       if (bad >= 0) atomicMin(err, (unsigned long long)err_encode((uint64_t)(elem_base + e), kind, bad));
     }
     const bool ok = in && bad < 0;

@@ -670,14 +670,17 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       if (ovr > 0 && ovr < capl) capl = ovr;
       if (capl > (int64_t)INT32_MAX - 4096) capl = (int64_t)INT32_MAX - 4096;
       const int cap = (int)capl;
-      // one resident wave (grid-stride): the occupancy of this instantiation x the SM count
-      static PerDevice wave;
-      const int fixed_wave = wave.once([&] {
-        int occ = 0, sms = 148;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chunk_scatter_fixed<T, true>, 256, 0);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device());
-        return (occ > 0 ? occ : 4) * sms;
+      // grid-stride over 256-thread CTAs, 4 per SM (3 for meshes of >= 2^26 elements): the grid sets
+      // how wide the element window in flight is; wider (5-6 CTAs per SM, the occupancy limit at 40
+      // registers) measured slower on config 5 (2.47 / 2.64 ms vs 2.14 at 4 and 2.07 at 3; 2 CTAs:
+      // 2.72), config 3 is fastest at 4 (0.157 ms vs 0.165 at 3)
+      static PerDevice sm_count;
+      const int sms = sm_count.once([&] {
+        int n = 148;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, current_device());
+        return n;
       });
+      const int64_t fixed_wave = (int64_t)(P.M >= ((int64_t)1 << 26) ? 3 : 4) * sms;
       const int fgrid = (int)std::min<int64_t>(fixed_wave, (P.M + 255) / 256 > 0 ? (P.M + 255) / 256 : 1);
       MN_CUDA(launch("elem_scatter", 4.0 * P.K * P.M + 5.0 * P.Pe, s, [&] {
         if (aligned)

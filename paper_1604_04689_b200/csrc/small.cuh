@@ -119,19 +119,8 @@ k_small_both(const int32_t* __restrict__ conn, int M, int N, int64_t* __restrict
     load_row<T, ALIGNED>(conn, e, row);
 #pragma unroll
     for (int p = 0; p < K; ++p) s_conn[e * K + p] = row[p];
-    int bad = -1, kind = 0;
-#pragma unroll
-    for (int p = K - 1; p >= 0; --p)
-      if (row[p] < 0 || row[p] >= N) bad = p;
-    if (bad < 0) {
-#pragma unroll
-      for (int p = K - 1; p >= 1; --p) {
-        bool dup = false;
-#pragma unroll
-        for (int q = 0; q < p; ++q) dup |= row[q] == row[p];
-        if (dup) { bad = p; kind = 1; }
-      }
-    }
+    int kind = 0;
+    const int bad = row_bad<K>(row, (uint32_t)N, kind);
     if (bad >= 0) {
       atomicMin(&s_err, (unsigned long long)err_encode((uint64_t)e, kind, bad));
     } else {
