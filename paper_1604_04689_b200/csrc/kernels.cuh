@@ -1274,6 +1274,59 @@ k_chunk_scatter(const int32_t* __restrict__ conn, int64_t M, const int64_t* __re
   }
 }
 
+// One warp-block (32 consecutive elements) of k_chunk_scatter_fixed between its two stages.
+template <int K>
+struct ScatterBlock {
+  uint32_t e;
+  int v[K], x[K], b[K];
+  unsigned peers[K];
+};
+
+// Stage A: validation, chunk of every incidence, warp groups (__match_any_sync), and the leader's
+// returning atomic on the chunk cursor (its result is consumed one block later, in stage B).
+template <int K, bool RANGE>
+__device__ __forceinline__ void scatter_stage_a(ScatterBlock<K>& s, uint32_t base, int lane, uint32_t end,
+                                                const int (&row)[K], uint32_t N, int64_t lo, int64_t hi,
+                                                int32_t* __restrict__ ccur, unsigned long long* __restrict__ err) {
+  s.e = base + lane;
+  const bool in = s.e < end;
+#pragma unroll
+  for (int p = 0; p < K; ++p) s.v[p] = row[p];
+  int kind = 0;
+  const int bad = in ? row_bad<K>(s.v, N, kind) : -1;
+  if (in && bad >= 0) atomicMin(err, (unsigned long long)err_encode((uint64_t)s.e, kind, bad));
+  const bool ok = in && bad < 0;
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    const bool mine = ok && (!RANGE || (s.v[p] >= lo && s.v[p] < hi));
+    s.x[p] = mine ? (int)((RANGE ? s.v[p] - lo : s.v[p]) >> kChunkShift) : -1;   // one shared sentinel (match cost grows with distinct values)
+    s.peers[p] = __match_any_sync(FULL, s.x[p]);
+    s.b[p] = 0;
+    if (s.x[p] >= 0 && lane == __ffs(s.peers[p]) - 1) s.b[p] = atomicAdd(ccur + s.x[p], (int)__popc(s.peers[p]));
+  }
+}
+
+// Stage B: each incidence's slot = its leader's cursor value + its rank in the group; writes.
+template <int K, bool RANGE>
+__device__ __forceinline__ void scatter_stage_b(const ScatterBlock<K>& s, int lane, int cap, int64_t lo, int64_t ebase,
+                                                int32_t* __restrict__ belem, uint8_t* __restrict__ bnode, bool& over) {
+  const int32_t eid = (int32_t)(ebase + s.e);
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    const int leader = __ffs(s.peers[p]) - 1;
+    const int q = __shfl_sync(FULL, s.b[p], leader) + __popc(s.peers[p] & lanemask_lt());
+    if (s.x[p] >= 0) {
+      if (q < cap) {
+        const uint64_t pos = (uint64_t)(uint32_t)s.x[p] * (uint32_t)cap + (uint32_t)q;   // one wide multiply-add
+        belem[pos] = eid;
+        bnode[pos] = (uint8_t)((RANGE ? s.v[p] - lo : s.v[p]) & (kChunkNodes - 1));
+      } else {
+        over = true;
+      }
+    }
+  }
+}
+
 // Single-read variant for the whole-path call (no count pass): validation (as k_chunk_count) and
 // the scatter into fixed-capacity buckets, chunk x at [x * cap, (x + 1) * cap).  The cursors end as
 // the chunk counts; a scan of them gives the element-CSR chunk bases.  A chunk whose count exceeds
@@ -1292,52 +1345,40 @@ k_chunk_scatter_fixed(const int32_t* __restrict__ conn, int64_t M, int64_t N, in
   const int lane = threadIdx.x & 31;
   // (grid-stride; a blocked assignment, each CTA on its own contiguous element range so that few
   // CTAs share a chunk counter at a time, measured the same: 2.10-2.28 vs 2.14 ms on config 5)
-  // 32-bit element indices (M <= INT32_MAX, checked at the C ABI; base + stride < 2^32)
+  // 32-bit element indices (M <= INT32_MAX, checked at the C ABI; base + stride < 2^32).
+  // Software-pipelined by one block: the returning cursor atomics of block i + 1 are issued before
+  // the writes of block i wait on block i's (60% of the stall samples sat on those results, r2o).
   const uint32_t stride = gridDim.x * blockDim.x;
   uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31);
   const uint32_t end = (uint32_t)M;
   bool over = false;   // some incidence of this thread found its bucket full (flagged once at the end)
-  int nv[K];   // the next row, loaded one iteration ahead
+  if (base >= end) return;
+  ScatterBlock<K> cur, nxt;
+  int nv[K];   // the row of the block after the one in stage A, loaded one block ahead
   if (base + lane < end) load_row<T, ALIGNED>(conn, (uint64_t)(base + lane), nv);
+  if (base + stride + lane < end) {
+    int r[K];
+    load_row<T, ALIGNED>(conn, (uint64_t)(base + stride + lane), r);
+    scatter_stage_a<K, RANGE>(cur, base, lane, end, nv, (uint32_t)N, lo, hi, ccur, err);
+#pragma unroll
+    for (int p = 0; p < K; ++p) nv[p] = r[p];
+  } else {
+    scatter_stage_a<K, RANGE>(cur, base, lane, end, nv, (uint32_t)N, lo, hi, ccur, err);
+  }
   for (; base < end; base += stride) {
-    const uint32_t e = base + lane;
-    const bool in = e < end;
-    int v[K];
+    const uint32_t next = base + stride;
+    if (next < end) {
+      int r[K];
+      const bool pre = next + stride + lane < end;
+      if (pre) load_row<T, ALIGNED>(conn, (uint64_t)(next + stride + lane), r);
+      scatter_stage_a<K, RANGE>(nxt, next, lane, end, nv, (uint32_t)N, lo, hi, ccur, err);
+      if (pre) {
 #pragma unroll
-    for (int p = 0; p < K; ++p) v[p] = nv[p];
-    if (base + stride + lane < end) load_row<T, ALIGNED>(conn, (uint64_t)(base + stride + lane), nv);
-    int kind = 0;
-    const int bad = in ? row_bad<K>(v, (uint32_t)N, kind) : -1;
-    if (in) {
-      if (bad >= 0) atomicMin(err, (unsigned long long)err_encode((uint64_t)e, kind, bad));
-    }
-    const bool ok = in && bad < 0;
-    // all K returning atomics issued before any result is used (one L2 round trip per row, not K)
-    int x[K], b[K];
-    unsigned peers[K];
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const bool mine = ok && (!RANGE || (v[p] >= lo && v[p] < hi));
-      x[p] = mine ? (int)((RANGE ? v[p] - lo : v[p]) >> kChunkShift) : -1;   // one shared sentinel (match cost grows with distinct values)
-      peers[p] = __match_any_sync(FULL, x[p]);
-      b[p] = 0;
-      if (x[p] >= 0 && lane == __ffs(peers[p]) - 1) b[p] = atomicAdd(ccur + x[p], (int)__popc(peers[p]));
-    }
-    const int32_t eid = (int32_t)(ebase + e);
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const int leader = __ffs(peers[p]) - 1;
-      const int q = __shfl_sync(FULL, b[p], leader) + __popc(peers[p] & lanemask_lt());
-      if (x[p] >= 0) {
-        if (q < cap) {
-          const uint64_t pos = (uint64_t)(uint32_t)x[p] * (uint32_t)cap + (uint32_t)q;   // one wide multiply-add
-          belem[pos] = eid;
-          bnode[pos] = (uint8_t)((RANGE ? v[p] - lo : v[p]) & (kChunkNodes - 1));
-        } else {
-          over = true;
-        }
+        for (int p = 0; p < K; ++p) nv[p] = r[p];
       }
     }
+    scatter_stage_b<K, RANGE>(cur, lane, cap, lo, ebase, belem, bnode, over);
+    cur = nxt;
   }
   if (over) *ovf = 1u;
 }

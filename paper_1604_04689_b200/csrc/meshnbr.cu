@@ -674,13 +674,19 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       // how wide the element window in flight is; wider (5-6 CTAs per SM, the occupancy limit at 40
       // registers) measured slower on config 5 (2.47 / 2.64 ms vs 2.14 at 4 and 2.07 at 3; 2 CTAs:
       // 2.72), config 3 is fastest at 4 (0.157 ms vs 0.165 at 3)
-      static PerDevice sm_count;
+      // (never more than are resident at once: hex rows need 106 registers, 2 CTAs per SM)
+      static PerDevice sm_count, occ_scatter;
       const int sms = sm_count.once([&] {
         int n = 148;
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, current_device());
         return n;
       });
-      const int64_t fixed_wave = (int64_t)(P.M >= ((int64_t)1 << 26) ? 3 : 4) * sms;
+      const int occ = occ_scatter.once([&] {
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_chunk_scatter_fixed<T, true>, 256, 0);
+        return o > 0 ? o : 1;
+      });
+      const int64_t fixed_wave = (int64_t)std::min(P.M >= ((int64_t)1 << 26) ? 3 : 4, occ) * sms;
       const int fgrid = (int)std::min<int64_t>(fixed_wave, (P.M + 255) / 256 > 0 ? (P.M + 255) / 256 : 1);
       MN_CUDA(launch("elem_scatter", 4.0 * P.K * P.M + 5.0 * P.Pe, s, [&] {
         if (aligned)
