@@ -183,6 +183,35 @@ mn_status mn_find_neighbors_both_host(mn_elem_type type, const int32_t* h_conn, 
                                       const mn_allocator* host_alloc, mn_stream stream,
                                       mn_csr* node_out, mn_csr* elem_out, mn_error_detail* err);
 
+/* Pipelined host-buffer form (a stream of meshes, e.g. many time steps or many parts): the same
+ * outputs as mn_find_neighbors_both_host, but the PCIe transfers of consecutive meshes overlap.
+ * The pipeline owns three streams on the current device: upload (H2D of the connectivity), compute
+ * (mn_find_neighbors_both) and download (D2H of both CSRs; the element CSR starts during the node
+ * pass).  PCIe is full duplex, so the upload of mesh i + 1 runs while the download of mesh i is
+ * still in flight (B200 box, measured: 55 GB/s one way, 92 GB/s both ways at once).
+ *   create:  dev_alloc / host_alloc as for mn_find_neighbors_both_host (NULL dev_alloc =
+ *            cudaMallocAsync on the stream given to alloc); device = the current device.
+ *   submit:  validates and copies h_conn (host memory, pinned for full speed; it must stay
+ *            unchanged until mn_host_pipeline_wait(ticket) returns), computes both CSRs (blocks
+ *            like mn_find_neighbors_both: one read of the validation word and nnz), enqueues the
+ *            downloads and returns.  node_out / elem_out receive host CSRs (owner = host_alloc)
+ *            whose CONTENTS are valid only after mn_host_pipeline_wait(*ticket).  On an error
+ *            (invalid mesh: lowest element, then position, reading R8) nothing is returned and no
+ *            ticket is issued; earlier tickets are unaffected.
+ *   wait:    blocks until the downloads of `ticket` are complete, then releases its device
+ *            buffers.  Tickets may be waited in any order; each exactly once.
+ *   destroy: waits for every outstanding ticket and releases the streams.
+ * Device memory: the workspace of one call plus, per outstanding ticket, its connectivity and
+ * device CSRs.  Not thread-safe per pipeline. */
+typedef struct mn_host_pipeline mn_host_pipeline;
+mn_status mn_host_pipeline_create(const mn_allocator* dev_alloc, const mn_allocator* host_alloc,
+                                  mn_host_pipeline** out);
+mn_status mn_host_pipeline_submit(mn_host_pipeline* p, mn_elem_type type, const int32_t* h_conn, int64_t num_elems,
+                                  int64_t num_nodes, mn_csr* node_out, mn_csr* elem_out, int64_t* ticket,
+                                  mn_error_detail* err);
+mn_status mn_host_pipeline_wait(mn_host_pipeline* p, int64_t ticket);
+void mn_host_pipeline_destroy(mn_host_pipeline* p);
+
 /* Releases offsets/indices through csr->owner on `stream` and zeroes the struct. */
 void mn_csr_release(mn_csr* csr, mn_stream stream);
 

@@ -19,7 +19,7 @@ import torch
 __all__ = [
     "TRI3", "QUAD4", "TET4", "HEX8", "MeshError", "lib_path", "load",
     "find_node_neighbors", "find_node_neighbors_sortpairs", "find_node_neighbors_shared", "find_elem_neighbors",
-    "find_poly_neighbors", "find_neighbors", "find_neighbors_host", "load_off", "load_obj",
+    "find_poly_neighbors", "find_neighbors", "find_neighbors_host", "HostPipeline", "load_off", "load_obj",
     "workspace_bytes", "node_key_bits", "node_key_bytes", "find_neighbors_chunked", "chunk_workspace_bytes",
     "emit_node_pairs", "emit_elem_pairs", "radix_sort_keys", "radix_sort_pairs_u32",
     "unique_node_csr", "elem_offsets", "exclusive_scan",
@@ -123,6 +123,10 @@ def _declare(lib):
                                        _P(_Csr), _P(_ErrDetail)]),
         "mn_find_neighbors_both": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _VP, _P(_Csr), _P(_Csr),
                                        _P(_ErrDetail)]),
+        "mn_host_pipeline_create": (S, [_P(_Allocator), _P(_Allocator), _P(_VP)]),
+        "mn_host_pipeline_submit": (S, [_VP, _INT, _VP, _I64, _I64, _P(_Csr), _P(_Csr), _P(_I64), _P(_ErrDetail)]),
+        "mn_host_pipeline_wait": (S, [_VP, _I64]),
+        "mn_host_pipeline_destroy": (None, [_VP]),
         "mn_find_neighbors_both_host": (S, [_INT, _VP, _I64, _I64, _P(_Allocator), _P(_Allocator), _VP,
                                             _P(_Csr), _P(_Csr), _P(_ErrDetail)]),
         "mn_find_neighbors_both_chunked": (S, [_INT, _VP, _I64, _I64, ctypes.c_size_t, _P(_Allocator), _VP,
@@ -260,7 +264,10 @@ class _TorchAllocator:
 
     def _alloc(self, ctx, nbytes, stream):
         try:
-            if self.stream is not None:
+            if stream:   # the stream the library allocates on (header: "allocates ... on `stream`")
+                with torch.cuda.stream(torch.cuda.ExternalStream(int(stream), device=self.device)):
+                    t = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+            elif self.stream is not None:
                 with torch.cuda.stream(self.stream):
                     t = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
             else:
@@ -520,6 +527,58 @@ def find_neighbors_host(conn_host: torch.Tensor, etype, num_nodes: int, device=N
                                              ctypes.byref(eo), ctypes.byref(err))
     _check(rc, err)
     return _take(hal, no), _take(hal, eo)
+
+
+class HostPipeline:
+    """A stream of meshes with host buffers (include/meshnbr.h mn_host_pipeline_*): submit() uploads
+    one mesh's connectivity, computes both CSRs and starts their download; wait(ticket) returns them
+    as pinned host tensors once the download is complete.  The upload of the next mesh overlaps the
+    download of the previous one (PCIe is full duplex).  conn_host must stay unchanged until its
+    ticket is waited."""
+
+    def __init__(self, device=None):
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._dal, self._hal = _TorchAllocator(self.device), _PinnedAllocator()
+        self._p = ctypes.c_void_p()
+        self._lib = load()
+        with torch.cuda.device(self.device):
+            _check(self._lib.mn_host_pipeline_create(ctypes.byref(self._dal.struct), ctypes.byref(self._hal.struct),
+                                                     ctypes.byref(self._p)))
+        self._pending = {}
+
+    def submit(self, conn_host: torch.Tensor, etype, num_nodes: int) -> int:
+        et = _etype(etype)
+        if conn_host.is_cuda or conn_host.dtype != torch.int32:
+            raise TypeError("conn_host must be a host int32 tensor")
+        c = conn_host.contiguous()
+        M = c.numel() // ARITY[et]
+        no, eo, err, tk = _Csr(), _Csr(), _ErrDetail(), ctypes.c_int64()
+        with torch.cuda.device(self.device):
+            rc = self._lib.mn_host_pipeline_submit(self._p, et, c.data_ptr(), M, int(num_nodes), ctypes.byref(no),
+                                                   ctypes.byref(eo), ctypes.byref(tk), ctypes.byref(err))
+        _check(rc, err)
+        self._pending[tk.value] = (c, _take(self._hal, no), _take(self._hal, eo))
+        return tk.value
+
+    def wait(self, ticket: int):
+        """((node offsets, node indices), (elem offsets, elem indices)) of `ticket`, pinned host tensors."""
+        _, node, elem = self._pending.pop(ticket)
+        with torch.cuda.device(self.device):
+            _check(self._lib.mn_host_pipeline_wait(self._p, int(ticket)))
+        return node, elem
+
+    def close(self):
+        if self._p:
+            with torch.cuda.device(self.device):
+                self._lib.mn_host_pipeline_destroy(self._p)
+            self._p = ctypes.c_void_p()
+            self._pending.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def workspace_bytes(etype, num_elems: int, num_nodes: int, modes: int = 3) -> int:

@@ -259,6 +259,47 @@ def test_host_buffers_errors_and_empty():
     assert no.tolist() == [0] * 8 and eo.tolist() == [0] * 8 and ni.numel() == 0 and ei_.numel() == 0
 
 
+def test_host_pipeline_stream_of_meshes():
+    """mn_host_pipeline_*: a stream of meshes of different types and sizes with overlapping
+    transfers; every ticket's CSRs equal the oracle's; tickets waited out of order; an invalid mesh
+    is rejected at submit without disturbing the tickets in flight; an empty mesh."""
+    pl = mn().HostPipeline()
+    meshes = [(name, et, make()) for name, et, make in SMALL[:6]] + [
+        ("kuhn_40", meshgen.TET4, meshgen.kuhn_tets(40))]
+    tickets = []
+    for name, et, (conn, N) in meshes:
+        tickets.append((pl.submit(conn.contiguous().pin_memory(), et, N), name, et, conn, N))
+        if len(tickets) == 3:   # an invalid mesh in the middle of the stream
+            bad = torch.tensor([[0, 1, 2], [1, 2, 9]], dtype=torch.int32).pin_memory()
+            with pytest.raises(mn().MeshError) as ei:
+                pl.submit(bad, 0, 5)
+            assert (ei.value.code, ei.value.elem, ei.value.pos) == (2, 1, 2)
+    empty = pl.submit(torch.zeros((0, 4), dtype=torch.int32), 2, 7)
+    for tk, name, et, conn, N in tickets[::-1]:   # reverse order
+        (no, ni), (eo, ei) = pl.wait(tk)
+        assert no.is_pinned() and ei.is_pinned()
+        _assert_csr((no, ni), oracle.node_csr(et, conn, N), name + " pipeline node")
+        _assert_csr((eo, ei), oracle.elem_csr(et, conn, N), name + " pipeline elem")
+    (no, ni), (eo, ei) = pl.wait(empty)
+    assert no.tolist() == [0] * 8 and eo.tolist() == [0] * 8 and ni.numel() == 0 and ei.numel() == 0
+    pl.close()
+
+
+def test_host_pipeline_matches_device_call_config3():
+    """Config 3 (12.6 M tets) twice through the pipeline (two tickets in flight) == the
+    device-buffer call, bit for bit."""
+    et, conn, N = meshgen.make_config(3)
+    ref = mn().find_neighbors(conn.cuda(), et, N)
+    pl = mn().HostPipeline()
+    h = conn.contiguous().pin_memory()
+    t0, t1 = pl.submit(h, et, N), pl.submit(h, et, N)
+    for tk in (t0, t1):
+        got = pl.wait(tk)
+        for (a, b), (c, d) in zip(got, ref):
+            assert torch.equal(a, c.cpu()) and torch.equal(b, d.cpu())
+    pl.close()
+
+
 def test_config2_sphere_full(elem_path):
     et, conn, N = meshgen.make_config(2)
     (no, ni), (eo, ei) = mn().find_neighbors(conn.cuda(), et, N)
