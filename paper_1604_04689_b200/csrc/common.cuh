@@ -206,6 +206,15 @@ __device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
   return v;
 }
 
+// 16-byte read-only load with the L2 fill limited to 64 bytes (random row gathers: the default fill
+// brings more sectors than the one row needs)
+__device__ __forceinline__ int4 ldg_l2_64(const int4* p) {
+  int4 v;
+  asm volatile("ld.global.nc.L2::64B.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
 // ------------------------------------------------------------------------------------------------
 // Element types.  For node pairs, slot r in [0, 2E) of an element holds (conn[la(r)], conn[lb(r)]):
 // r = 2j is edge j forward, r = 2j+1 edge j reversed (R5).  la/lb are 4-bit local

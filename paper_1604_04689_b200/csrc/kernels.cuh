@@ -53,7 +53,7 @@ __device__ __forceinline__ uint32_t digit_of(KeyT key, const PassDigit& pd, uint
 // k_hist_validate: one thread per element.  Validation (reading R8) + per-digit histograms of the
 // node ids of valid elements.  Histograms are CTA-private in shared memory, flushed once.
 // ================================================================================================
-template <int T, bool ALIGNED>
+template <int T, bool ALIGNED, bool RAND = false>
 __device__ __forceinline__ void load_row(const int32_t* __restrict__ conn, int64_t e, int (&row)[Elem<T>::K]);
 
 // The warp walks 32 consecutive elements per step.  A digit that is the same in all 32 lanes
@@ -637,14 +637,14 @@ __device__ __forceinline__ bool hash_insert(unsigned long long* tab, unsigned lo
   return false;
 }
 
-template <int T, bool ALIGNED>
+template <int T, bool ALIGNED, bool RAND>
 __device__ __forceinline__ void load_row(const int32_t* __restrict__ conn, int64_t e, int (&row)[Elem<T>::K]) {
   constexpr int K = Elem<T>::K;
   if (ALIGNED && (K == 4 || K == 8)) {
     const int4* p = reinterpret_cast<const int4*>(conn + e * K);
 #pragma unroll
     for (int q = 0; q < K / 4; ++q) {
-      const int4 x = __ldg(p + q);
+      const int4 x = RAND ? ldg_l2_64(p + q) : __ldg(p + q);
       row[4 * q] = x.x; row[4 * q + 1] = x.y; row[4 * q + 2] = x.z; row[4 * q + 3] = x.w;
     }
   } else {
@@ -664,10 +664,10 @@ struct RowSrc {
   int64_t nr;
 };
 
-template <int T, bool ALIGNED, bool DIST>
+template <int T, bool ALIGNED, bool DIST, bool RAND = false>
 __device__ __forceinline__ void fetch_row(const RowSrc& rs, int64_t e, int (&row)[Elem<T>::K]) {
   if (!DIST) {   // 0 <= e < 2^31: 32-bit index, one wide multiply-add for the row address
-    load_row<T, ALIGNED>(rs.conn, (uint64_t)(uint32_t)e, row);
+    load_row<T, ALIGNED, RAND>(rs.conn, (uint64_t)(uint32_t)e, row);
     return;
   }
   if (e >= rs.base && e < rs.base + rs.M) {
@@ -788,7 +788,7 @@ __device__ __forceinline__ void sort_small(uint32_t (*tab)[kNodeThreads], int t,
 // of a 4-incidence batch loading its home slot before any insert, 5.07 vs 4.13 ms on config 5; a
 // per-batch instead of per-candidate set-capacity check with scalar incidence loads, 4.33-4.44 ms.
 // DESIGN.md §5.)
-template <int T, bool ALIGNED, bool DIST = false, bool SHARED = false,
+template <int T, bool ALIGNED, bool DIST = false, bool SHARED = false, bool RAND = false,
           int MINB = (Elem<T>::K <= 4) ? 10 : 1>
 __global__ void __launch_bounds__(kNodeThreads, MINB)
 k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, RowSrc rs,
@@ -844,7 +844,7 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
       int row[B][K];
 #pragma unroll
       for (int q = 0; q < B; ++q)
-        if (e[q] >= 0) fetch_row<T, ALIGNED, DIST>(rs, e[q], row[q]);
+        if (e[q] >= 0) fetch_row<T, ALIGNED, DIST, RAND>(rs, e[q], row[q]);
 #pragma unroll
       for (int q = 0; q < B; ++q) {
         if (e[q] < 0) continue;

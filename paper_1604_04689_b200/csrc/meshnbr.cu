@@ -869,12 +869,21 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       if (P.N > 0) {   // (M > 0 with N == 0 always fails validation: nothing to expand)
         MN_CUDA(launch("node_gather", gb, s, [&] {
           const RowSrc rs{conn, 0, P.M, nullptr, nullptr, 0};
-          if (shared && aligned)
+          // meshes without locality (the LSD element path) gather their rows at random: those loads
+          // fill 64 bytes of L2 instead of the default 128 (config 4: DRAM 15.4 -> 8.7 GB per launch; time
+          // 2.57 -> 2.42 ms in one A/B, 2.61-2.63 on another box: the kernel is latency-bound there)
+          if (shared && aligned && !transpose)
+            k_node_gather_t<T, true, false, true, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt,
+                                                                                   lofs, giants, ngiant, errw);
+          else if (shared && aligned)
             k_node_gather_t<T, true, false, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs,
                                                                               giants, ngiant, errw);
           else if (shared)
             k_node_gather_t<T, false, false, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs,
                                                                                giants, ngiant, errw);
+          else if (aligned && !transpose)
+            k_node_gather_t<T, true, false, false, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt,
+                                                                                    lofs, giants, ngiant, errw);
           else if (aligned)
             k_node_gather_t<T, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs, giants,
                                                                  ngiant, errw);
