@@ -46,6 +46,15 @@ def main():
     got = mn.find_poly_neighbors(off.cuda(), idx.cuda(), N, node=True, elem=True, shared=True)
     check(got, (oracle.poly_node_csr(off, idx, N), oracle.poly_elem_csr(off, idx, N),
                 oracle.poly_shared_csr(off, idx, N)), "poly")
+    # the pipelined host API: three streams, readbacks through k_read_words, two meshes in flight
+    pl = mn.HostPipeline()
+    tks = [(pl.submit(conn.contiguous().pin_memory(), et, N), et, conn, N) for _, et, (conn, N) in cases[:3]]
+    for tk, et, conn, N in tks:
+        node, elem = pl.wait(tk)
+        for (go, gi), (eo, ei) in zip((node, elem), (oracle.node_csr(et, conn, N), oracle.elem_csr(et, conn, N))):
+            assert np.array_equal(go.numpy(), eo) and np.array_equal(gi.numpy(), ei), "pipeline"
+    pl.close()
+    print("ok pipeline", flush=True)
     print("ok all", flush=True)
 
 
