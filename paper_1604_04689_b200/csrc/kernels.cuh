@@ -1446,20 +1446,26 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
       bulk_g2s(s_nd, bnode + bb, bn, &s_bar);
     }
     mbar_wait(&s_bar, 0);
-    for (int i0 = 0; i0 < n; i0 += U * kChunkNodes) {
+    const int nfull = n & ~(U - 1);   // full 4-entry groups without per-entry bounds checks
+    for (int i0 = 0; i0 < nfull; i0 += U * kChunkNodes) {
       const int i = i0 + U * t;
-      if (i >= n) break;
+      if (i >= nfull) break;
       const uint32_t nq = *reinterpret_cast<const uint32_t*>(s_nd + i);
       const int4 eq = *reinterpret_cast<const int4*>(s_el + i);
       const int nd[U] = {(int)(nq & 255), (int)((nq >> 8) & 255), (int)((nq >> 16) & 255), (int)(nq >> 24)};
       const int32_t el[U] = {eq.x, eq.y, eq.z, eq.w};
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (i + u < n) {
-          const int pos = atomicAdd(&s_cnt[nd[u]], 1);
-          if (pos < kSegMax) slots[pos * kSlotPitch + nd[u]] = el[u];
-          else s_over = 1;
-        }
+      for (int u = 0; u < U; ++u) {
+        const int pos = atomicAdd(&s_cnt[nd[u]], 1);
+        if (pos < kSegMax) slots[pos * kSlotPitch + nd[u]] = el[u];
+        else s_over = 1;
+      }
+    }
+    if (t < n - nfull) {   // the <= 3 entries of the last partial group
+      const int i = nfull + t, nd = s_nd[i];
+      const int pos = atomicAdd(&s_cnt[nd], 1);
+      if (pos < kSegMax) slots[pos * kSlotPitch + nd] = s_el[i];
+      else s_over = 1;
     }
   } else if ((bb & 15) == 0) {   // CTA-uniform: 16-byte aligned bucket (the fixed layout) -> vector loads
     // thread t takes entries [i0 + 4t, i0 + 4t + 4): one 4-byte node load + one int4 element load
@@ -1538,11 +1544,12 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
     if (n >= 8 * kChunkNodes) {   // (config 5, mean 24: 2.69 ms this way, 3.25 position-mapped)
       // long lists (mean >= 8): warp w copies the lists of nodes 32w .. 32w+31, lane i writing
       // entry i of the node (one coalesced store per node)
-#pragma unroll 4
+      int32_t* const ob = eidx + b0;   // (32-bit offsets inside the chunk's output range)
+#pragma unroll 8
       for (int q = 0; q < 32; ++q) {
         const int nodeq = warp * 32 + q;
         const int dq = s_cnt[nodeq];
-        if (lane < dq) eidx[b0 + s_ex[nodeq] + lane] = slots[lane * kSlotPitch + nodeq];
+        if (lane < dq) ob[s_ex[nodeq] + lane] = slots[lane * kSlotPitch + nodeq];
       }
     } else {
       // short lists: thread i writes chunk output position i; its node by binary search in s_ex
