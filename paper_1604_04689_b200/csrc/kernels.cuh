@@ -838,16 +838,19 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
         const bool r1 = (r & 2) != 0, r0 = (r & 1) != 0;
         const int u[5] = {r1 ? lo.z : lo.x, r1 ? lo.w : lo.y, r1 ? hi.x : lo.z, r1 ? hi.y : lo.w,
                           r1 ? hi.z : hi.x};
+        // past the node's last incidence (n < B, a tail batch) the first incidence is repeated: its
+        // candidates are already in the set, so the repeat only hits, and no incidence is skipped
+        // by a branch (config 5's 24-incidence nodes have no tail batch)
 #pragma unroll
-        for (int q = 0; q < B; ++q) e[q] = q < n ? (r0 ? u[q + 1] : u[q]) : -1;
+        for (int q = 0; q < B; ++q) e[q] = r0 ? u[q + 1] : u[q];
+#pragma unroll
+        for (int q = 1; q < B; ++q) e[q] = q < n ? e[q] : e[0];
       }
       int row[B][K];
 #pragma unroll
-      for (int q = 0; q < B; ++q)
-        if (e[q] >= 0) fetch_row<T, ALIGNED, DIST, RAND>(rs, e[q], row[q]);
+      for (int q = 0; q < B; ++q) fetch_row<T, ALIGNED, DIST, RAND>(rs, e[q], row[q]);
 #pragma unroll
       for (int q = 0; q < B; ++q) {
-        if (e[q] < 0) continue;
         // simplices (TRI3, TET4): every other node of the element is an edge neighbour, so the
         // candidates are the row values != a; otherwise the local neighbour table is used
         constexpr bool simplex = (C == K - 1);   // simplices and SHARED: all other row values
