@@ -5,16 +5,21 @@
 //   otherwise:
 //     k_locality_sample (+ 1 blocking read)   choose the element-CSR algorithm (meshes >= 2^20 elements)
 //     element CSR, locality (config 5):       k_chunk_scatter_fixed (a1/a2 validation + one read of conn
-//                                             into fixed 128-node chunk buckets), k_scan_i32 (chunk
-//                                             bases), guarded counted fallback, k_chunk_sort (a3e/a4/a5)
+//                                             into fixed 128-node chunk buckets, cursor atomics
+//                                             pipelined across warp-blocks), k_scan_i32 (chunk bases),
+//                                             guarded counted fallback, k_chunk_sort (a3e/a4/a5; bucket
+//                                             read by TMA bulk copies)
 //     element CSR, no locality (config 4):    k_hist_validate, k_bucket_bases, k_onesweep x nd (LSD,
 //                                             pass 0 creates the pairs from conn, last pass writes the
 //                                             payloads + run lengths), k_scan_i32 (a5)
 //     node CSR:                               k_node_gather_t (a1/a3n/a4: per-node expansion of the
 //                                             element CSR, hash-set dedupe, register sort), k_node_giant,
 //                                             k_scan_i32 (a5)
-//     D2H(err, nnz) + one stream sync          a6
+//     k_read_words(err, nnz) + one stream sync a6 (a kernel store into pinned memory, not a D2H copy
+//                                             that could queue behind a download on the copy engine)
 //     exact-size node indices, k_node_compact  a6
+// Host buffers: mn_find_neighbors_both_host (one call), mn_host_pipeline_* (a stream of meshes on
+// three streams: the upload of mesh i+1 overlaps the download of mesh i).
 // The paper-literal node pipeline (all node pairs, LSD over 2b key bits, k_unique_node) is
 // mn_find_node_neighbors_sortpairs.  Polygons: poly.cuh; small meshes: small.cuh; multi-GPU:
 // dist.cuh (bucket + NCCL all-to-all, or the fused bucket-and-send over peer memory).
