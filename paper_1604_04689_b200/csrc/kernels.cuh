@@ -794,7 +794,8 @@ __global__ void __launch_bounds__(kNodeThreads, MINB)
 k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, RowSrc rs,
                 int64_t N, uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, int32_t* __restrict__ lofs,
                 uint32_t* __restrict__ giants, unsigned int* __restrict__ ngiant,
-                const unsigned long long* __restrict__ err, int64_t a_base = 0) {
+                const unsigned long long* __restrict__ err, int64_t a_base = 0,
+                int32_t* __restrict__ csum = nullptr) {
   constexpr int K = Elem<T>::K, B = 4;                   // incidences in flight per thread
   constexpr int C = SHARED ? K - 1 : Elem<T>::C;          // candidates per incidence
   constexpr uint32_t EMPTY = 0xFFFFFFFFu;
@@ -918,6 +919,12 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
 #pragma unroll
   for (int w = 0; w < kNodeThreads / 32; ++w)
     if (w < warp) excl += s_wsum[w];
+  if (csum && t == 0) {   // the chunk's list total (giants counted raw; k_node_giant corrects them)
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < kNodeThreads / 32; ++w) tot += s_wsum[w];
+    csum[blockIdx.x] = (int32_t)tot;
+  }
   if (!valid) return;
   lofs[a] = (int32_t)excl;
   if (giant) {
@@ -1034,7 +1041,7 @@ __global__ void __launch_bounds__(1024)
 k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx, RowSrc rs,
              uint32_t* __restrict__ temp, int32_t* __restrict__ cnt, const int32_t* __restrict__ lofs,
              const uint32_t* __restrict__ giants, const unsigned int* __restrict__ ngiant, int smem_cap,
-             const unsigned long long* __restrict__ err, int64_t a_base = 0) {
+             const unsigned long long* __restrict__ err, int64_t a_base = 0, int32_t* __restrict__ csum = nullptr) {
   constexpr int K = Elem<T>::K;
   constexpr int C = SHARED ? K - 1 : Elem<T>::C;
   extern __shared__ uint32_t sv[];
@@ -1064,7 +1071,10 @@ k_node_giant(const int64_t* __restrict__ eoff, const int32_t* __restrict__ eidx,
     }
     __syncthreads();
     const int u = block_sort_dedupe(buf, raw, out);
-    if (threadIdx.x == 0) cnt[a] = u;
+    if (threadIdx.x == 0) {
+      cnt[a] = u;
+      if (csum) atomicAdd(csum + a / kNodeThreads, u - (int)raw);   // the chunk total held it raw
+    }
     __syncthreads();
   }
 }
@@ -1103,6 +1113,65 @@ k_node_compact(const int64_t* __restrict__ eoff, int C, const uint32_t* __restri
       if (s_dst[mid] <= o) lo = mid; else hi = mid - 1;
     }
     out[o] = (int32_t)temp[s_src[lo] + (o - s_dst[lo])];
+  }
+}
+
+// k_node_compact with the node-offset scan folded in: a chunk's base is cb[chunk] (the exclusive scan
+// of the per-chunk list totals k_node_gather_t / k_node_giant leave in csum), each node's offset is
+// that base + the CTA's exclusive scan of the node counts; writes offsets[n0 .. n0 + nloc) (and
+// offsets[N] in the last chunk) and copies the lists (none when out == nullptr, i.e. nnz == 0).
+// Replaces a look-back scan over the N counts (0.17 ms on config 5) by one over N / 128 totals.
+__global__ void __launch_bounds__(kNodeThreads)
+k_node_compact_cb(const int64_t* __restrict__ eoff, int C, const uint32_t* __restrict__ temp,
+                  const int32_t* __restrict__ lofs, const int32_t* __restrict__ cnt, const int64_t* __restrict__ cb,
+                  int64_t N, int64_t* __restrict__ noff, int32_t* __restrict__ out) {
+  __shared__ int64_t s_src[kNodeThreads];
+  __shared__ int64_t s_dst[kNodeThreads + 1];
+  __shared__ int s_w[kNodeThreads / 32];
+  const int64_t n0 = (int64_t)blockIdx.x * kNodeThreads;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int nloc = (int)(N - n0 < kNodeThreads ? N - n0 : kNodeThreads);
+  const int64_t base = (int64_t)C * eoff[n0];
+  const int d = t < nloc ? cnt[n0 + t] : 0;
+  int incl = d;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  int excl = incl - d;
+#pragma unroll
+  for (int w = 0; w < kNodeThreads / 32; ++w)
+    if (w < warp) excl += s_w[w];
+  const int64_t o = cb[blockIdx.x] + excl;
+  if (t < nloc) {
+    s_src[t] = base + lofs[n0 + t];
+    s_dst[t] = o;
+    noff[n0 + t] = o;
+  }
+  if (t == nloc - 1) {
+    s_dst[nloc] = o + d;
+    if (n0 + nloc == N) noff[N] = o + d;
+  }
+  __syncthreads();
+  if (!out) return;
+  const int64_t o0 = s_dst[0], o1 = s_dst[nloc];
+  // without a giant in the chunk the packed source layout equals the destination layout
+  const bool packed = __syncthreads_and(t >= nloc || s_src[t] - base == s_dst[t] - o0);
+  if (packed) {
+    const uint32_t* src = temp + base - o0;
+    for (int64_t i = o0 + t; i < o1; i += kNodeThreads) out[i] = (int32_t)src[i];
+    return;
+  }
+  for (int64_t i = o0 + t; i < o1; i += kNodeThreads) {
+    int lo = 0, hi = nloc - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_dst[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    out[i] = (int32_t)temp[s_src[lo] + (i - s_dst[lo])];
   }
 }
 

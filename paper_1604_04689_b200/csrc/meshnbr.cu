@@ -609,6 +609,8 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
     unsigned int* ngiant = nullptr;
     uint64_t *bases = nullptr, *status = nullptr, *sstatus = nullptr;
     int32_t *cnt = nullptr, *ecnt = nullptr, *lofs = nullptr, *cursor = nullptr;
+    int32_t* ncsum = nullptr;   // per 128-node chunk: node-list total (k_node_gather_t, k_node_giant)
+    int64_t* ncb = nullptr;     // its exclusive scan: the chunks' node-CSR bases
     uint32_t* sgiants = nullptr;
     unsigned int* nsgiant = nullptr;
     int64_t* eoff = elem_off;
@@ -651,6 +653,8 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       if (want_node) {
         cnt = a.take<int32_t>((size_t)P.N);
         lofs = a.take<int32_t>((size_t)P.N);
+        ncsum = a.take<int32_t>((size_t)tiles_of(P.N, kNodeThreads) + 1);
+        ncb = a.take<int64_t>((size_t)tiles_of(P.N, kNodeThreads) + 1);
         giants = a.take<uint32_t>((size_t)(giant_cap ? giant_cap : 1));
         if (!want_elem) {
           eoff = a.take<int64_t>((size_t)P.N + 1);
@@ -879,22 +883,22 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
           // 2.57 -> 2.42 ms in one A/B, 2.61-2.63 on another box: the kernel is latency-bound there)
           if (shared && aligned && !transpose)
             k_node_gather_t<T, true, false, true, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt,
-                                                                                   lofs, giants, ngiant, errw);
+                                                                                   lofs, giants, ngiant, errw, 0, ncsum);
           else if (shared && aligned)
             k_node_gather_t<T, true, false, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs,
-                                                                              giants, ngiant, errw);
+                                                                              giants, ngiant, errw, 0, ncsum);
           else if (shared)
             k_node_gather_t<T, false, false, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs,
-                                                                               giants, ngiant, errw);
+                                                                               giants, ngiant, errw, 0, ncsum);
           else if (aligned && !transpose)
             k_node_gather_t<T, true, false, false, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt,
-                                                                                    lofs, giants, ngiant, errw);
+                                                                                    lofs, giants, ngiant, errw, 0, ncsum);
           else if (aligned)
             k_node_gather_t<T, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs, giants,
-                                                                 ngiant, errw);
+                                                                 ngiant, errw, 0, ncsum);
           else
             k_node_gather_t<T, false><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, P.N, temp, cnt, lofs, giants,
-                                                                  ngiant, errw);
+                                                                  ngiant, errw, 0, ncsum);
         }));
       }
       const int cap = 48 * 1024;   // uint32 entries sorted in shared memory by k_node_giant (192 KB)
@@ -909,21 +913,26 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       MN_CUDA(launch("node_giant", 0.0, s, [&] {
         const RowSrc rs{conn, 0, P.M, nullptr, nullptr, 0};
         if (shared && aligned)
-          k_node_giant<T, true, false, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw);
+          k_node_giant<T, true, false, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw, 0, ncsum);
         else if (shared)
-          k_node_giant<T, false, false, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw);
+          k_node_giant<T, false, false, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw, 0, ncsum);
         else if (aligned)
-          k_node_giant<T, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw);
+          k_node_giant<T, true><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw, 0, ncsum);
         else
-          k_node_giant<T, false><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw);
+          k_node_giant<T, false><<<148, 1024, cap * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap, errw, 0, ncsum);
       }));
-      // ---- a5 (nodes): exclusive scan of the unique counts -> offsets ----
-      if (P.N > 0)   // N == 0 with M > 0 always fails validation; nothing to scan
-      MN_CUDA(launch("scan_counts", 4.0 * P.N + 8.0 * (P.N + 1), s, [&] {
-        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)scan_tiles, kScanThreads, 0, s>>>(cnt, P.N, node_off, sstatus,
-                                                                                 tickets + 31, 2);
-      }));
-      MN_CUDA(read_words(host + 1, node_off + P.N, 8, s));
+      // ---- a5 (nodes): exclusive scan of the per-chunk list totals -> chunk bases, nnz; the node
+      // offsets are written by k_node_compact_cb (block scan of the counts + the chunk base) ----
+      const int64_t nch_nodes = tiles_of(P.N, kNodeThreads);
+      if (P.N > 0) {   // N == 0 with M > 0 always fails validation; nothing to scan
+        MN_CUDA(launch("scan_counts", 12.0 * nch_nodes, s, [&] {
+          k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nch_nodes, kScanTile), kScanThreads, 0, s>>>(
+              ncsum, nch_nodes, ncb, sstatus, tickets + 31, 2);
+        }));
+        MN_CUDA(read_words(host + 1, ncb + nch_nodes, 8, s));
+      } else {
+        host[1] = 0;
+      }
     }
     // ---- a6: the one blocking read (validation word, node nnz) ----
     MN_CUDA(read_words(host, errw, 8, s));
@@ -935,11 +944,13 @@ static mn_status pipeline_inc(const Plan& P, const int32_t* conn, Mem& mem, bool
       prof_add_bytes("node_gather", 4.0 * U);
       int32_t* out = U ? (int32_t*)mem.get((size_t)U * 4) : nullptr;
       if (U && !out) { st = MN_ERR_OOM; goto done; }
-      if (U) {
+      if (P.N > 0) {   // (also when nnz == 0: it writes the offsets)
         MN_CUDA(launch("node_compact", 8.0 * U + 24.0 * P.N, s, [&] {
-          k_node_compact<<<(unsigned)tiles_of(P.N, kNodeThreads), kNodeThreads, 0, s>>>(eoff, CE, ekA, lofs,
-                                                                                         node_off, P.N, out);
+          k_node_compact_cb<<<(unsigned)tiles_of(P.N, kNodeThreads), kNodeThreads, 0, s>>>(eoff, CE, ekA, lofs, cnt,
+                                                                                            ncb, P.N, node_off, out);
         }));
+      } else {
+        MN_CUDA(cudaMemsetAsync(node_off, 0, 8, s));
       }
       node_out->num_nodes = P.N;
       node_out->nnz = U;
