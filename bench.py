@@ -590,8 +590,9 @@ def run_ours(args):
             del r
         walls.sort()
         latency = {"c_abi_median_us": c_med, "c_abi_min_us": c_min, "python_median_us": walls[len(walls) // 2],
-                   "reps": reps, "what": "host wall time per call, entry to return with both CSRs complete "
-                                         "(C ABI: mn_time_both, default allocator; python: find_neighbors + sync)"}
+                   "reps": reps, "what": "host wall time per call, from entry until both CSRs are complete on the "
+                                         "stream (C ABI: mn_time_both, default allocator, stream sync included; "
+                                         "python: find_neighbors + sync)"}
 
     # ---- roofline of the dominant kernel (live CUDA events on the launching stream) ----
     peak, peak_src = peaks()

@@ -489,8 +489,9 @@ mn_status mn_set_small_path(int64_t max_incidences);
 /* Latency of the C-ABI call: runs mn_find_neighbors_both `reps` times back to back (after 2
  * warm-up calls) with the default allocator (cudaMallocAsync on `stream`; the current device's
  * default pool is set to keep freed blocks) and reports the median (and minimum) host wall time
- * per call in microseconds — from entry to return with both CSRs complete on `stream`, the one
- * blocking read included.  Outputs are released after each call. */
+ * per call in microseconds — from entry until `stream` has finished the call's last kernel (the
+ * call itself returns with the node compaction still queued), the one blocking read included.
+ * Outputs are released after each call. */
 mn_status mn_time_both(mn_elem_type type, const int32_t* d_conn, int64_t num_elems, int64_t num_nodes, int reps,
                        mn_stream stream, double* median_us, double* min_us);
 

@@ -2722,11 +2722,12 @@ mn_status mn_time_both(mn_elem_type t, const int32_t* d_conn, int64_t M, int64_t
     mn_csr no{}, eo{};
     const auto t0 = std::chrono::steady_clock::now();
     const mn_status st = mn_find_neighbors_both(t, d_conn, M, N, nullptr, stream, &no, &eo, nullptr);
-    const auto t1 = std::chrono::steady_clock::now();
     if (st != MN_OK) return st;
+    // the call returns with its last kernel (the node compaction) still queued: wait for it
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return MN_ERR_CUDA;
+    const auto t1 = std::chrono::steady_clock::now();
     mn_csr_release(&no, stream);
     mn_csr_release(&eo, stream);
-    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return MN_ERR_CUDA;
     if (r >= 2) us.push_back(std::chrono::duration<double, std::micro>(t1 - t0).count());
   }
   std::sort(us.begin(), us.end());
