@@ -23,6 +23,8 @@
  *       - mn_find_poly_neighbors: three times (offset bounds; validation + element offsets; node nnz);
  *       - mn_find_neighbors_both_chunked: once per node range, plus once;
  *       - mn_find_neighbors_both_host: as _both, plus the final D2H;
+ *       - mn_host_pipeline_submit: as _both (its uploads and downloads do not block);
+ *         mn_host_pipeline_wait: until that ticket's downloads are complete;
  *       - mn_find_neighbors_dist: as _both, plus the exchange's count step (see there).
  *     Stage primitives (mn_emit_*, mn_radix_sort_*, ...) do not block unless stated.
  *   - Memory: outputs and workspace come from the caller's mn_allocator (NULL = the library's
