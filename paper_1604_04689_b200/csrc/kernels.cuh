@@ -1486,6 +1486,7 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
   __shared__ int32_t slots[kSegMax * kSlotPitch];
   __shared__ int s_cnt[kChunkNodes];
   __shared__ int s_ex[kChunkNodes];
+  __shared__ int2 s_ce[kChunkNodes];   // (count, offset) per node for the copy-out (one 8-byte load)
   __shared__ int s_wsum[kChunkNodes / 32];
   __shared__ int s_over;
   __shared__ alignas(16) int32_t s_el[kStage];   // the bucket, brought in by two bulk copies
@@ -1602,6 +1603,7 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
   if (a < N) eoff[a] = b0 + excl;
   if (a == N - 1) eoff[N] = b1;
   s_ex[t] = excl;
+  s_ce[t] = make_int2(d, excl);
   const bool over = s_over != 0;   // CTA-uniform (read after the barrier above)
   if (!over) {
     const int dd = SORT ? d : 0;
@@ -1620,8 +1622,8 @@ k_chunk_sort(const int64_t* __restrict__ cbase, int64_t N, const int32_t* __rest
 #pragma unroll 8
       for (int q = 0; q < 32; ++q) {
         const int nodeq = warp * 32 + q;
-        const int dq = s_cnt[nodeq];
-        if (lane < dq) ob[s_ex[nodeq] + lane] = slots[lane * kSlotPitch + nodeq];
+        const int2 ce = s_ce[nodeq];
+        if (lane < ce.x) ob[ce.y + lane] = slots[lane * kSlotPitch + nodeq];
       }
     } else {
       // short lists: thread i writes chunk output position i; its node by binary search in s_ex
