@@ -232,6 +232,9 @@ static mn_status finish_own_conn(const int32_t* conn, int64_t Ms, int64_t base, 
     uint8_t* bnode = ar.take<uint8_t>((size_t)2 * n + 64);
     uint32_t* giants = ar.take<uint32_t>((size_t)nloc + 1);
     uint32_t* sgiants = ar.take<uint32_t>((size_t)nloc + 1);
+    const int64_t ngn = tiles_of(nloc, kNodeThreads);         // node chunks of the gather
+    int32_t* ncsum = ar.take<int32_t>((size_t)ngn + 1);         // their list totals
+    int64_t* ncb = ar.take<int64_t>((size_t)ngn + 1);           // and bases
     ws = mem.get(ar.off);
     if (!ws) { st = MN_ERR_OOM; goto done; }
     {
@@ -240,6 +243,7 @@ static mn_status finish_own_conn(const int32_t* conn, int64_t Ms, int64_t base, 
       errw = fix(errw); tickets = fix(tickets); ngiant = fix(ngiant); nsgiant = fix(nsgiant); ovf = fix(ovf);
       sstatus = fix(sstatus); ccur = fix(ccur); ccnt = fix(ccnt); cnt = fix(cnt); lofs = fix(lofs);
       cbase = fix(cbase); temp = fix(temp); bnode = fix(bnode); giants = fix(giants); sgiants = fix(sgiants);
+      ncsum = fix(ncsum); ncb = fix(ncb);
       int32_t* belem = reinterpret_cast<int32_t*>(temp);
       MN_CUDA(cudaMemsetAsync(ws, 0, head, s));
       MN_CUDA(cudaMemsetAsync(errw, 0xFF, 8, s));
@@ -305,10 +309,10 @@ static mn_status finish_own_conn(const int32_t* conn, int64_t Ms, int64_t base, 
       MN_CUDA(launch("node_gather", 8.0 * (nloc + 1) + 4.0 * n + 4.0 * Elem<T>::K * (Ms + nr) + 8.0 * nloc, s, [&] {
         if (aligned)
           k_node_gather_t<T, true, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, nloc, temp, cnt, lofs, giants,
-                                                                     ngiant, errw, lo);
+                                                                     ngiant, errw, lo, ncsum);
         else
           k_node_gather_t<T, false, true><<<ng, kNodeThreads, 0, s>>>(eoff, eidx, rs, nloc, temp, cnt, lofs, giants,
-                                                                      ngiant, errw, lo);
+                                                                      ngiant, errw, lo, ncsum);
       }));
       const int cap2 = 48 * 1024;
       static PerDevice attr;
@@ -320,27 +324,28 @@ static mn_status finish_own_conn(const int32_t* conn, int64_t Ms, int64_t base, 
       MN_CUDA(launch("node_giant", 0.0, s, [&] {
         if (aligned)
           k_node_giant<T, true, true><<<148, 1024, cap2 * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant, cap2,
-                                                                 errw, lo);
+                                                                 errw, lo, ncsum);
         else
           k_node_giant<T, false, true><<<148, 1024, cap2 * 4, s>>>(eoff, eidx, rs, temp, cnt, lofs, giants, ngiant,
-                                                                  cap2, errw, lo);
+                                                                  cap2, errw, lo, ncsum);
       }));
-      MN_CUDA(launch("scan_counts", 12.0 * nloc, s, [&] {
-        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(nloc, kScanTile), kScanThreads, 0, s>>>(
-            cnt, nloc, noff, sstatus, tickets + 2, 3);
+      // node offsets as in the 1-GPU path: scan of the chunk totals, offsets written by the compaction
+      MN_CUDA(launch("scan_counts", 12.0 * ngn, s, [&] {
+        k_scan_i32<kScanThreads, kScanItems><<<(unsigned)tiles_of(ngn, kScanTile), kScanThreads, 0, s>>>(
+            ncsum, ngn, ncb, sstatus, tickets + 2, 3);
       }));
-      MN_CUDA(cudaMemcpyAsync(host + 1, noff + nloc, 8, cudaMemcpyDeviceToHost, s));
+      MN_CUDA(read_words(host + 1, ncb + ngn, 8, s));
       MN_CUDA(cudaStreamSynchronize(s));
       const int64_t U = (int64_t)host[1];
       prof_add_bytes("node_gather", 4.0 * U);
       if (U) {
         node_slice->indices = (int32_t*)mem.get((size_t)U * 4);
         if (!node_slice->indices) { st = MN_ERR_OOM; goto done; }
-        MN_CUDA(launch("node_compact", 8.0 * U + 24.0 * nloc, s, [&] {
-          k_node_compact<<<(unsigned)tiles_of(nloc, kNodeThreads), kNodeThreads, 0, s>>>(eoff, C, temp, lofs, noff,
-                                                                                       nloc, node_slice->indices);
-        }));
       }
+      MN_CUDA(launch("node_compact", 8.0 * U + 24.0 * nloc, s, [&] {
+        k_node_compact_cb<<<(unsigned)ngn, kNodeThreads, 0, s>>>(eoff, C, temp, lofs, cnt, ncb, nloc, noff,
+                                                                 node_slice->indices);
+      }));
       node_slice->nnz = U;
     }
   }
@@ -433,7 +438,7 @@ static mn_status dist2_impl(const int32_t* conn, int64_t M, int64_t base, int64_
             if (aligned) k_locality_sample<T, true><<<64, 256, 0, s>>>(conn, M, smp);
             else k_locality_sample<T, false><<<64, 256, 0, s>>>(conn, M, smp);
           }) != cudaSuccess ||
-          cudaMemcpyAsync(host + 2, smp, 16, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+          read_words(host + 2, smp, 16, s) != cudaSuccess ||
           cudaStreamSynchronize(s) != cudaSuccess)
         local = MN_ERR_CUDA;
     }
@@ -463,7 +468,7 @@ static mn_status dist2_impl(const int32_t* conn, int64_t M, int64_t base, int64_
     }
     if (local == MN_OK &&
         (cudaMemcpyAsync(hh.data(), hist, BINS * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-         cudaMemcpyAsync(host, errw, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+         read_words(host, errw, 8, s) != cudaSuccess ||
          cudaStreamSynchronize(s) != cudaSuccess))
       local = MN_ERR_CUDA;
     if (local == MN_OK) ew = host[0];
