@@ -775,6 +775,24 @@ __device__ __forceinline__ void sort_small(uint32_t (*tab)[kNodeThreads], int t,
     if (i < L) out[i] = (uint32_t)v[i];
 }
 
+// The L <= NET values in the occupied slots of a thread's set column (bit i of `used` = slot i),
+// read in slot order into registers (no compaction pass), sorted, written to out[0, L).
+template <int NET>
+__device__ __forceinline__ void sort_small_mask(uint32_t (*tab)[kNodeThreads], int t, uint32_t used, int L,
+                                                uint32_t* out) {
+  int32_t v[NET];
+#pragma unroll
+  for (int i = 0; i < NET; ++i) {
+    const int slot = __ffs((int)used) - 1;   // (-1 once the mask is empty: not read then)
+    used &= used - 1;
+    v[i] = i < L ? (int32_t)tab[slot < 0 ? 0 : slot][t] : INT32_MAX;
+  }
+  oddeven_sort<NET>(v);
+#pragma unroll
+  for (int i = 0; i < NET; ++i)
+    if (i < L) out[i] = (uint32_t)v[i];
+}
+
 // (Fusing the element-list sort of the transpose path into this kernel, with the CTA's incidence
 // range staged in shared memory, was measured slower on B200: the extra registers / shared memory
 // cost more occupancy than the saved pass.)
@@ -929,6 +947,15 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
   lofs[a] = (int32_t)excl;
   if (giant) {
     giants[atomicAdd(ngiant, 1u)] = (uint32_t)a;
+    return;
+  }
+  if (!WIDE) {   // (L <= kMaxUnique = 24): the values go straight from the occupied slots (the mask)
+    uint32_t* out = temp + (size_t)C * eoff[n0] + excl;
+    const int lmax = __reduce_max_sync(__activemask(), (unsigned)L);
+    if (lmax <= 8) sort_small_mask<8>(tab, t, (uint32_t)used, L, out);
+    else if (lmax <= 16) sort_small_mask<16>(tab, t, (uint32_t)used, L, out);
+    else sort_small_mask<24>(tab, t, (uint32_t)used, L, out);
+    cnt[a] = L;
     return;
   }
   {   // compact the set to its first L slots (write index <= read index)
