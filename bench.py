@@ -613,7 +613,7 @@ def run_ours(args):
     # secondary: the same kernel against the instruction-issue roofline (warp instructions per launch
     # from a committed ncu capture, profiles/issue.json; 148 SMs x 4 schedulers x sm clock)
     ip = os.path.join(ROOT, "profiles", "issue.json")
-    if os.path.exists(ip):
+    if os.path.exists(ip) and args.outputs == "both" and not args.max_workspace_gb:   # (the captured path only)
         inst = json.load(open(ip)).get(f"config{args.config}/n{world}/{top['name']}")
         if inst:
             clk_mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0)) \
