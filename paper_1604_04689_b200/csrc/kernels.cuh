@@ -825,13 +825,15 @@ k_node_gather_t(const int64_t* __restrict__ eoff, const int32_t* __restrict__ ei
   using Mask = typename std::conditional<(HS > 32), unsigned long long, uint32_t>::type;
   __shared__ uint32_t tab[HS][kNodeThreads];
   __shared__ uint32_t s_wsum[kNodeThreads / 32];
-  if (err && *err != ERR_NONE) return;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t n0 = (int64_t)blockIdx.x * kNodeThreads;
   const int64_t a = n0 + t;
   const bool valid = a < N;
+  // the validation word and the node's offsets are loaded together (one latency, not two)
+  const unsigned long long ev = err ? *err : ERR_NONE;
   const int64_t s0 = valid ? eoff[a] : 0;
   const int64_t d0 = valid ? eoff[a + 1] - s0 : 0;
+  if (ev != ERR_NONE) return;
   const int32_t* inc = eidx + s0;
   int L = 0;
   int64_t raw = 0;
